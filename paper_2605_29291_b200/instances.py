@@ -1,0 +1,204 @@
+"""Seeded synthetic instances for BASELINE.json configs C0-C4 (harness input).
+
+Random source: the reference's counter generator "splitmix64-boxmuller/v1"
+(``pkg/src/rapdb/rng.py:1-63``), restated so the same (seed, stream, index)
+yields the same doubles on every platform.  Raw draw i of stream s under seed q
+is ``mix(key + i)`` with ``key = mix(mix(q) + s)`` (``rng.py:35-45``); uniforms
+take the top 53 bits (``rng.py:52-54``); normals are Box-Muller with the radius
+from the first half of the raw draws and the angle from the second half
+(``rng.py:56-63``) -- so normals are NOT call-granularity invariant and the call
+sizes below are part of the contract.
+
+Stream convention "4i..4i+3 for the i-th object" follows ``generate.py:51-61``.
+Dense configs:
+
+* ``B_i = normal(n*r) / sqrt(n)`` on stream 4i, C-order reshape to n x r;
+* ``Q_i = 0.5*(M + M^T) + 0.1*I`` with ``M = B_i B_i^T`` (explicitly symmetrised);
+* ``c_i = normal(n)`` on stream 4i+2;
+* ``d_i = -uniform(1, 1, 2)`` on stream 4i+3 for i >= 1, ``d_0 = 0``;
+* box [-10, 10]^n, orthant cone, no equalities.
+
+Everything here builds host arrays once; they are fed unchanged to the device
+path and to the CPU oracle.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+GENERATOR_NAME = "splitmix64-boxmuller/v1"
+
+_M64 = 0xFFFFFFFFFFFFFFFF
+_INC = np.uint64(0x9E3779B97F4A7C15)
+_C1 = np.uint64(0xBF58476D1CE4E5B9)
+_C2 = np.uint64(0x94D049BB133111EB)
+_TWO_M53 = 2.0 ** -53
+
+
+def _finalize(z: np.ndarray) -> np.ndarray:
+    """splitmix64 output function on a uint64 array (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        z = z + _INC
+        z = (z ^ (z >> np.uint64(30))) * _C1
+        z = (z ^ (z >> np.uint64(27))) * _C2
+        return z ^ (z >> np.uint64(31))
+
+
+def _mix_int(v: int) -> int:
+    return int(_finalize(np.array([v & _M64], dtype=np.uint64))[0])
+
+
+class CounterRng:
+    """Stateless counter stream; each call consumes a contiguous index range."""
+
+    name = GENERATOR_NAME
+
+    def __init__(self, seed: int, stream: int = 0):
+        self.key = np.uint64(_mix_int((_mix_int(seed) + stream) & _M64))
+        self.counter = 0
+
+    def raw(self, count: int) -> np.ndarray:
+        idx = np.arange(self.counter, self.counter + count, dtype=np.uint64)
+        self.counter += count
+        with np.errstate(over="ignore"):
+            return _finalize(idx + self.key)
+
+    def uniform(self, count: int, low: float = 0.0, high: float = 1.0) -> np.ndarray:
+        u = (self.raw(count) >> np.uint64(11)).astype(np.float64) * _TWO_M53
+        return low + (high - low) * u
+
+    def normal(self, count: int) -> np.ndarray:
+        half = (count + 1) // 2
+        bits = self.raw(2 * half) >> np.uint64(11)
+        u1 = (bits[:half].astype(np.float64) + 1.0) * _TWO_M53
+        u2 = bits[half:].astype(np.float64) * _TWO_M53
+        rad = np.sqrt(-2.0 * np.log(u1))
+        ang = 2.0 * np.pi * u2
+        return np.concatenate([rad * np.cos(ang), rad * np.sin(ang)])[:count]
+
+
+@dataclass
+class QcqpArrays:
+    """Plain host arrays of one instance.  ``Q`` is a C-contiguous
+    ``(m+1, n, n)`` stack (index 0 = objective), ``q`` is ``(m+1, n)``."""
+
+    n: int
+    m: int
+    p: int
+    Q: np.ndarray
+    q: np.ndarray
+    r: np.ndarray
+    A: np.ndarray
+    b: np.ndarray
+    lower: np.ndarray
+    upper: np.ndarray
+    mu: float = 0.0
+    name: str = ""
+    meta: dict = field(default_factory=dict)
+
+    def Q_list(self) -> List[np.ndarray]:
+        return [self.Q[i] for i in range(self.m + 1)]
+
+    def q_list(self) -> List[np.ndarray]:
+        return [self.q[i] for i in range(self.m + 1)]
+
+
+def dense_qcqp(n: int, m: int, rank: int, seed: int = 0,
+               box: float = 10.0) -> QcqpArrays:
+    """BASELINE configs 0-2: ``Q_i = B_i B_i^T + 0.1 I`` (i = 0..m)."""
+    Q = np.empty((m + 1, n, n), dtype=np.float64)
+    q = np.empty((m + 1, n), dtype=np.float64)
+    r = np.zeros(m + 1, dtype=np.float64)
+    scale = 1.0 / np.sqrt(n)
+    for i in range(m + 1):
+        B = CounterRng(seed, 4 * i).normal(n * rank).reshape(n, rank) * scale
+        M = B @ B.T
+        Qi = Q[i]
+        np.add(M, M.T, out=Qi)
+        Qi *= 0.5
+        Qi[np.diag_indices(n)] += 0.1
+        q[i] = CounterRng(seed, 4 * i + 2).normal(n)
+        if i > 0:
+            r[i] = -float(CounterRng(seed, 4 * i + 3).uniform(1, 1.0, 2.0)[0])
+    return QcqpArrays(
+        n=n, m=m, p=0, Q=Q, q=q, r=r,
+        A=np.zeros((0, n)), b=np.zeros(0),
+        lower=np.full(n, -box), upper=np.full(n, box), mu=0.0,
+        name=f"dense-qcqp-n{n}-m{m}-r{rank}-s{seed}",
+        meta={"generator": GENERATOR_NAME, "seed": seed, "rank": rank})
+
+
+def kml_epigraph(N: int = 4000, d: int = 50, seed: int = 0,
+                 C: float = 1.0) -> QcqpArrays:
+    """BASELINE config 4: kernel-matrix-learning QCQP in epigraph form.
+
+    Points: ``a_k = y_k*0.5*1 + N(0, I_d)`` (normals on stream 0, N*d draws),
+    balanced labels (first half +1).  Kernels: RBF with widths
+    {0.1, 1, 10} x median pairwise distance (``exp(-|a-a'|^2/(2w^2))``),
+    ``(1 + a.a')^2`` and ``a.a'``; each scaled to trace N.  ``Q_j = diag(y) K_j
+    diag(y)``.  Variables ``(alpha, t)``, n = N+1; minimise t subject to
+    ``(1/N) alpha^T Q_j alpha - 2 1^T alpha - t <= 0``, i.e. ``Qt_j = (2/N) Q_j
+    (+) 0``, ``q_j = (-2*1, -1)``, ``r_j = 0``; ``y^T alpha = 0`` (p = 1);
+    ``0 <= alpha <= C``, t free.  Objective f = t (``Q_0 = 0``, ``q_0 = e_t``).
+    """
+    rng = CounterRng(seed, 0)
+    y = np.concatenate([np.ones(N // 2), -np.ones(N - N // 2)])
+    X = rng.normal(N * d).reshape(N, d) + 0.5 * y[:, None]
+    G = X @ X.T
+    sq = np.diag(G).copy()
+    D2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * G, 0.0)
+    iu = np.triu_indices(N, 1)
+    med = float(np.median(np.sqrt(D2[iu])))
+    kernels = []
+    for wmul in (0.1, 1.0, 10.0):
+        w = wmul * med
+        kernels.append(np.exp(-D2 / (2.0 * w * w)))
+    kernels.append((1.0 + G) ** 2)
+    kernels.append(G.copy())
+    n = N + 1
+    m = len(kernels)
+    Q = np.zeros((m + 1, n, n), dtype=np.float64)
+    q = np.zeros((m + 1, n), dtype=np.float64)
+    q[0, N] = 1.0
+    yy = np.outer(y, y)
+    for j, K in enumerate(kernels):
+        K = K * (N / np.trace(K))
+        H = yy * K
+        H = 0.5 * (H + H.T)
+        Q[j + 1, :N, :N] = (2.0 / N) * H
+        q[j + 1, :N] = -2.0
+        q[j + 1, N] = -1.0
+    A = np.zeros((1, n))
+    A[0, :N] = y
+    lower = np.zeros(n)
+    upper = np.full(n, C)
+    lower[N] = -np.inf
+    upper[N] = np.inf
+    return QcqpArrays(
+        n=n, m=m, p=1, Q=Q, q=q, r=np.zeros(m + 1), A=A, b=np.zeros(1),
+        lower=lower, upper=upper, mu=0.0, name=f"kml-epigraph-N{N}-d{d}-s{seed}",
+        meta={"generator": GENERATOR_NAME, "seed": seed, "median_dist": med})
+
+
+# BASELINE.json configs[0..2], [4]; config 3 (factored sparse) lives in sparse.py
+CONFIGS = {
+    "C0": dict(n=200, m=10, rank=20),
+    "C1": dict(n=2000, m=200, rank=200),
+    "C2": dict(n=4096, m=512, rank=256),
+}
+
+
+def config_instance(name: str, seed: int = 0, scale: Optional[float] = None) -> QcqpArrays:
+    """Instance for a BASELINE config name; ``scale`` shrinks n and m
+    proportionally (parity cases at sizes the oracle finishes quickly)."""
+    if name == "C4":
+        N = 4000 if scale is None else max(8, int(4000 * scale))
+        return kml_epigraph(N=N)
+    cfg = dict(CONFIGS[name])
+    if scale is not None:
+        cfg = dict(n=max(4, int(cfg["n"] * scale)), m=max(1, int(cfg["m"] * scale)),
+                   rank=max(2, int(cfg["rank"] * scale)))
+    return dense_qcqp(seed=seed, **cfg)
