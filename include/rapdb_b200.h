@@ -1,0 +1,144 @@
+/*
+ * rapdb_b200.h -- C ABI of the B200-native rAPDB hot path.
+ *
+ * The reference (arxiv 2605.29291, package `rapdb`, pure Python) has no FFI;
+ * its operator seam is the set of Python functions the engine calls
+ * (pkg/src/rapdb/problem.py:196-223 coupling_value / grad_x_coupling /
+ * grad_y_coupling, geometry.py:144-148 project_set, problem.py:182-186
+ * project_dual_cone) driven by ApdbEngine.step (engine.py:198-259) and
+ * run_restarted (restarts.py:82-170).  This library replaces that whole
+ * per-iteration path: the host binding (paper_2605_29291_b200/_capi.py,
+ * ctypes) calls these entry points from the drop-in Python API.
+ *
+ * Conventions
+ *  - Every large buffer (Q stack, q, r, A, b, bounds, workspace, trace) is a
+ *    caller-owned DEVICE allocation (a PyTorch CUDA tensor); the library never
+ *    frees caller memory.  Scalars and small result structs are host memory.
+ *  - Return codes: 0 ok, 1 input (InputError), 2 configuration
+ *    (ConfigurationError), 3 backtracking exhausted (NonConvergence), 4
+ *    CUDA/device.  rapdb_last_error() returns the message of the last failure.
+ *  - One context per (process, device); not thread-safe; all work is enqueued
+ *    on the stream given to rapdb_set_stream (default: legacy stream) and the
+ *    calls that return results synchronise that stream.
+ */
+#ifndef RAPDB_B200_H
+#define RAPDB_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAPDB_OK 0
+#define RAPDB_EINPUT 1
+#define RAPDB_ECONFIG 2
+#define RAPDB_ENONCONV 3
+#define RAPDB_EDEVICE 4
+
+/* run status codes (rapdb_run_result.status) */
+#define RAPDB_RUN_LIMIT 0        /* max_iters accepted iterations done           */
+#define RAPDB_RUN_CONVERGED 1    /* check_termination fired (diagnostics.py:252)  */
+#define RAPDB_RUN_BUDGET 2       /* total == budget (restarts.py:105, :166)       */
+#define RAPDB_RUN_CHECK_DUE 3    /* adaptive-restart gap check due (host side)    */
+#define RAPDB_RUN_FIXED_DUE 4    /* fixed restart due and caller wants the point  */
+#define RAPDB_RUN_NONCONV 5      /* backtracking exhausted (engine.py:222-226)    */
+#define RAPDB_RUN_ABORT 6        /* device watchdog fired                         */
+
+#define RAPDB_TRACE_COLS 11      /* iter,tau_start,tau,sigma,gamma,evals_iter,
+                                    evals_total,kkt,infeas,subopt,restart_flag  */
+
+typedef struct rapdb_ctx rapdb_ctx;
+
+typedef struct {
+  long long max_iters;     /* accepted iterations to run in this call (>= 1)       */
+  long long budget;        /* run_restarted budget: KKT forced at total == budget  */
+  long long stop_total;    /* return CHECK_DUE when total reaches it (<=0: never)  */
+  int metrics_every;       /* KKT cadence (restarts.py:115); <= 0: no KKT          */
+  int criterion;           /* 0 none, 1 conic, 2 paper51 (diagnostics.py:252-263) */
+  double eps, eps_kkt, eps_feas, f_star;
+  int has_f_star;
+  int fixed_period;        /* FixedRestart period, 0 = no fixed restarts           */
+  int fixed_point;         /* 0 last, 1 average                                    */
+  int warm_tau;            /* reinit keeps tau (engine.py:111)                     */
+  int stop_at_fixed;       /* return FIXED_DUE instead of restarting on device     */
+} rapdb_run_args;
+
+typedef struct {
+  int status;
+  long long iters_done;    /* accepted iterations performed by this call          */
+  long long total;         /* == engine.iters (cumulative accepted iterations)    */
+  long long inner;         /* iterations since the last restart                   */
+  long long evals_total;
+  double tau_cand, tau_prev, gamma, sigma_prev, T;
+  double fail_tau, fail_gamma;
+  long long fail_iter;
+  double metrics[8];       /* kkt, stationarity, primal_eq, complementarity,
+                              infeas, f_value, mean_pos_violation, subopt_abs     */
+  int has_metrics;
+  double sweep_ns;         /* device time spent in Q sweeps (globaltimer)         */
+  long long sweeps;        /* number of Q sweeps                                  */
+} rapdb_run_result;
+
+/* version of the ABI (bumped on incompatible change) */
+int rapdb_abi_version(void);
+
+/* context ------------------------------------------------------------------ */
+int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out);
+void rapdb_destroy(rapdb_ctx* ctx);
+int rapdb_last_error(const rapdb_ctx* ctx, char* buf, int size);
+int rapdb_set_stream(rapdb_ctx* ctx, void* cuda_stream);
+
+/* problem data: replaces ProblemInstance's Q/q/r/A/b/primal_set storage
+ * (problem.py:109-162, _as_operator problem.py:31-40).  Q is the local shard
+ * of the (m+1)-matrix stack, matrices k0..k1-1, laid out [k1-k0][n][ld] with
+ * ld even and ld >= n (zero padded).  q is [(m+1)][n], r [m+1], A [p][n],
+ * b [p], lower/upper [n] (+-inf allowed).  zero_flags (HOST, k1-k0 bytes)
+ * marks all-zero local matrices that the sweep skips.                         */
+int rapdb_bind_dense(rapdb_ctx* ctx, int n, int m, int p, int k0, int k1, long long ld,
+                     const double* Q, const double* q, const double* r,
+                     const double* A, const double* b,
+                     const double* lower, const double* upper, double mu,
+                     const unsigned char* zero_flags);
+
+/* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
+ * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */
+int rapdb_set_params(rapdb_ctx* ctx, int mode, double c_alpha, double c_beta, double delta,
+                     double eta, double tau_bar, double gamma0, int nonmonotone,
+                     int max_backtracks, int ball_kind, double r1, double r2);
+
+/* workspace: size query after bind+params, then a caller-owned device buffer */
+long long rapdb_workspace_bytes(rapdb_ctx* ctx);
+int rapdb_bind_workspace(rapdb_ctx* ctx, void* dptr, long long bytes);
+
+/* ApdbEngine.reinit (engine.py:102-136).  source 0: explicit point (device
+ * pointers x[n], v[p], lam[m]); 1: current iterate; 2: ergodic average.
+ * reset_inner zeroes the since-restart counter (run_restarted's `inner`).     */
+int rapdb_reinit(rapdb_ctx* ctx, int source, const double* x, const double* v,
+                 const double* lam, int warm_tau, int reset_inner);
+
+/* Accepted iterations with device-side backtracking, KKT cadence, termination
+ * and fixed restarts (engine.py:198-259 inside restarts.py:111-161).  trace is
+ * a device buffer of max_iters * RAPDB_TRACE_COLS doubles (row-major).        */
+int rapdb_run(rapdb_ctx* ctx, const rapdb_run_args* args, double* trace, rapdb_run_result* out);
+
+/* kkt_residual at the current iterate (diagnostics.py:96-113); out[8] host   */
+int rapdb_kkt(rapdb_ctx* ctx, int has_f_star, double f_star, double* out);
+
+/* engine.last / engine.average() (engine.py:262-272) into device buffers     */
+int rapdb_get_iterate(rapdb_ctx* ctx, int which, double* x, double* v, double* lam);
+
+/* One fused sweep at x (device): u[(k1-k0)][n] and g[m+1] (index 0 = f) into
+ * device buffers; reps > 1 repeats it (timing); *ms = mean device ms/sweep.   */
+int rapdb_probe_sweep(rapdb_ctx* ctx, const double* x, double* u, double* g, int reps, float* ms);
+
+/* smoothed_gap(z, xi) at the current iterate (source 1) or the ergodic
+ * average (2) (diagnostics.py:120-163): dense H = Q0 + sum lam_i Q_i, power
+ * iteration (problem.py:47-68), APG subsolver (subsolve.py:27-62).  x_warm is
+ * a device pointer or NULL.  out[4] host = gap, iterations, residual, converged.
+ * The candidate x used is written to x_cand (device, n) for the next warm start. */
+int rapdb_smoothed_gap(rapdb_ctx* ctx, int source, double xi, double tol, const double* x_warm,
+                       double* x_cand, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,207 @@
+"""ctypes binding of the C ABI (include/rapdb_b200.h) -- no CPU fallback.
+
+``load()`` opens ``_rapdb_b200.so`` built in-tree by ``csrc/Makefile``; if the
+library or a CUDA device is missing every solver entry point raises
+``DeviceError`` instead of computing anything on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from .errors import ConfigurationError, DeviceError, InputError, NonConvergence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_rapdb_b200.so")
+
+TRACE_COLS = 11
+RUN_LIMIT, RUN_CONVERGED, RUN_BUDGET, RUN_CHECK_DUE, RUN_FIXED_DUE, RUN_NONCONV, RUN_ABORT = range(7)
+
+
+class RunArgs(C.Structure):
+    _fields_ = [("max_iters", C.c_longlong), ("budget", C.c_longlong), ("stop_total", C.c_longlong),
+                ("metrics_every", C.c_int), ("criterion", C.c_int),
+                ("eps", C.c_double), ("eps_kkt", C.c_double), ("eps_feas", C.c_double),
+                ("f_star", C.c_double), ("has_f_star", C.c_int), ("fixed_period", C.c_int),
+                ("fixed_point", C.c_int), ("warm_tau", C.c_int), ("stop_at_fixed", C.c_int)]
+
+
+class RunResult(C.Structure):
+    _fields_ = [("status", C.c_int), ("iters_done", C.c_longlong), ("total", C.c_longlong),
+                ("inner", C.c_longlong), ("evals_total", C.c_longlong),
+                ("tau_cand", C.c_double), ("tau_prev", C.c_double), ("gamma", C.c_double),
+                ("sigma_prev", C.c_double), ("T", C.c_double),
+                ("fail_tau", C.c_double), ("fail_gamma", C.c_double), ("fail_iter", C.c_longlong),
+                ("metrics", C.c_double * 8), ("has_metrics", C.c_int),
+                ("sweep_ns", C.c_double), ("sweeps", C.c_longlong)]
+
+
+_lib = None
+EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_error", "rapdb_set_stream",
+           "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
+           "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
+           "rapdb_smoothed_gap"]
+
+
+def load(path: str = LIB_PATH):
+    """Open the native library (raises DeviceError when it is absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise DeviceError(f"native library {path} is missing; run `make -C paper_2605_29291_b200/csrc` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    P, D, I, LL = C.c_void_p, C.c_double, C.c_int, C.c_longlong
+    lib.rapdb_abi_version.restype = I
+    lib.rapdb_create.argtypes = [I, I, I, C.POINTER(P)]
+    lib.rapdb_destroy.argtypes = [P]
+    lib.rapdb_destroy.restype = None
+    lib.rapdb_last_error.argtypes = [P, C.c_char_p, I]
+    lib.rapdb_set_stream.argtypes = [P, P]
+    lib.rapdb_bind_dense.argtypes = [P, I, I, I, I, I, LL, P, P, P, P, P, P, P, D, P]
+    lib.rapdb_set_params.argtypes = [P, I, D, D, D, D, D, D, I, I, I, D, D]
+    lib.rapdb_workspace_bytes.argtypes = [P]
+    lib.rapdb_workspace_bytes.restype = LL
+    lib.rapdb_bind_workspace.argtypes = [P, P, LL]
+    lib.rapdb_reinit.argtypes = [P, I, P, P, P, I, I]
+    lib.rapdb_run.argtypes = [P, C.POINTER(RunArgs), P, C.POINTER(RunResult)]
+    lib.rapdb_kkt.argtypes = [P, I, D, C.POINTER(D)]
+    lib.rapdb_get_iterate.argtypes = [P, I, P, P, P]
+    lib.rapdb_probe_sweep.argtypes = [P, P, P, P, I, C.POINTER(C.c_float)]
+    lib.rapdb_smoothed_gap.argtypes = [P, I, D, D, P, P, C.POINTER(D)]
+    _lib = lib
+    return lib
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+class Context:
+    """One device solver context bound to a device instance (see problem.DeviceData)."""
+
+    def __init__(self, device_index: int = 0, rank: int = 0, nranks: int = 1):
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the rAPDB path runs only on the GPU (no CPU fallback)")
+        self.lib = load()
+        self.torch = torch
+        self.device = torch.device("cuda", device_index)
+        h = C.c_void_p()
+        self._check(self.lib.rapdb_create(device_index, rank, nranks, C.byref(h)), ctx=None)
+        self.h = h
+        self.ws = None
+        self.data = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and self.h.value:
+                self.lib.rapdb_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # -- error mapping (rapdb_b200.h return codes) --------------------------
+    def _msg(self):
+        buf = C.create_string_buffer(512)
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.rapdb_last_error(self.h, buf, 512)
+        return buf.value.decode(errors="replace")
+
+    def _check(self, code, ctx="self", state=None):
+        if code == 0:
+            return
+        msg = self._msg() if ctx is not None else f"rapdb_create failed ({code})"
+        if code == 1:
+            raise InputError(msg)
+        if code == 2:
+            raise ConfigurationError(msg)
+        if code == 3:
+            raise NonConvergence(msg, state=state)
+        raise DeviceError(msg)
+
+    def stream(self):
+        return self.torch.cuda.current_stream(self.device)
+
+    def _set_stream(self):
+        self.lib.rapdb_set_stream(self.h, C.c_void_p(self.stream().cuda_stream))
+
+    # -- binding -----------------------------------------------------------
+    def bind(self, data, cfg):
+        """data: problem.DeviceData; cfg: resolved SolverConfig."""
+        from .geometry import ball_code
+        self._set_stream()
+        zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)
+        self._check(self.lib.rapdb_bind_dense(
+            self.h, data.n, data.m, data.p, 0, data.m + 1, data.ld,
+            _ptr(data.Q), _ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
+            _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
+            zero.ctypes.data_as(C.c_void_p)))
+        kind, r1, r2 = ball_code(cfg.dual_ball)
+        self._check(self.lib.rapdb_set_params(
+            self.h, 1 if cfg.mode == "xy" else 0, float(cfg.c_alpha), float(cfg.c_beta), float(cfg.delta),
+            float(cfg.eta), float(cfg.tau_bar), float(cfg.gamma0), 1 if cfg.nonmonotone else 0,
+            int(cfg.max_backtracks), kind, r1, r2))
+        nbytes = int(self.lib.rapdb_workspace_bytes(self.h))
+        if nbytes <= 0:
+            raise DeviceError("workspace size query failed")
+        self.ws = self.torch.empty(nbytes + 256, dtype=self.torch.uint8, device=self.device)
+        base = self.ws.data_ptr()
+        off = (-base) % 256
+        self._check(self.lib.rapdb_bind_workspace(self.h, C.c_void_p(base + off), nbytes))
+        self.data = data
+
+    # -- ops -----------------------------------------------------------------
+    def reinit(self, source: int, x=None, v=None, lam=None, warm_tau=False, reset_inner=False):
+        self._set_stream()
+        self._check(self.lib.rapdb_reinit(self.h, source, _ptr(x), _ptr(v), _ptr(lam),
+                                          1 if warm_tau else 0, 1 if reset_inner else 0))
+
+    def run(self, args: RunArgs, trace_tensor):
+        self._set_stream()
+        res = RunResult()
+        code = self.lib.rapdb_run(self.h, C.byref(args), _ptr(trace_tensor), C.byref(res))
+        state = None
+        if code == 3:
+            state = {"tau": res.fail_tau, "gamma": res.fail_gamma, "iter": int(res.fail_iter)}
+        self._check(code, state=state)
+        return res
+
+    def kkt(self, f_star=None):
+        self._set_stream()
+        out = (C.c_double * 8)()
+        self._check(self.lib.rapdb_kkt(self.h, 0 if f_star is None else 1,
+                                       0.0 if f_star is None else float(f_star), out))
+        return list(out)
+
+    def get_iterate(self, which: int):
+        torch = self.torch
+        d = self.data
+        x = torch.empty(d.n, dtype=torch.float64, device=self.device)
+        v = torch.empty(max(d.p, 1), dtype=torch.float64, device=self.device)
+        lam = torch.empty(max(d.m, 1), dtype=torch.float64, device=self.device)
+        self._set_stream()
+        self._check(self.lib.rapdb_get_iterate(self.h, which, _ptr(x), _ptr(v), _ptr(lam)))
+        return x, v[:d.p], lam[:d.m]
+
+    def probe_sweep(self, x, reps=1):
+        torch = self.torch
+        d = self.data
+        u = torch.empty((d.m + 1, d.n), dtype=torch.float64, device=self.device)
+        g = torch.empty(d.m + 1, dtype=torch.float64, device=self.device)
+        ms = C.c_float()
+        self._set_stream()
+        self._check(self.lib.rapdb_probe_sweep(self.h, _ptr(x), _ptr(u), _ptr(g), int(reps), C.byref(ms)))
+        return u, g, float(ms.value)
+
+    def smoothed_gap(self, source: int, xi: float, tol: float, x_warm=None, x_cand=None):
+        out = (C.c_double * 4)()
+        self._set_stream()
+        self._check(self.lib.rapdb_smoothed_gap(self.h, source, float(xi), float(tol), _ptr(x_warm),
+                                                _ptr(x_cand), out))
+        return list(out)

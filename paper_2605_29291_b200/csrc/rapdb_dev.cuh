@@ -1,0 +1,181 @@
+// rapdb_dev.cuh -- device data structures and primitives of the B200 rAPDB path.
+//
+// Layout in HBM (one context, single rank shard [k0, k1) of the m+1 matrices):
+//   Q     [nloc][n][ld]   fp64, row-major, ld even (16-B rows for bulk copies)
+//   q     [m+1][n], r [m+1], A [p][n], b [p], lower/upper [n]
+//   x     [2][n]          parity `cur` = accepted x_k, `cur^1` = trial x_new
+//   U     [2][nloc][n]    u_i = Q_i x for both parities (the U-cache)
+//   gval  [2][m+1]        f (index 0) and g_i at both parities
+//   eqv   [2][p]          A x - b
+//   y     [2][p+m]        (v, lam) at both parities
+//   ytr   [p+m]           dual trial point before the dual-ball projection
+//   gy    [3][p+m]        yx caches gy_prev / gy_cur / gy_new (rotating indices)
+//   gxb   [3][n]          xy caches gx_prev / gx_cur / gx_new (rotating indices)
+//   gxs   [n]             scratch gradient (gx_mixed, KKT gradient, gx at y_k)
+//   xcum  [n], ycum [p+m] ergodic accumulators (engine.py:244-249)
+//   part  [NSLOT][G]      per-CTA partial sums (fixed-order grid reductions)
+//   segxu/segqx [G][segmax]  per-CTA per-matrix-segment x.u and q.x sums
+//
+// All arithmetic is IEEE binary64.  The file is compiled with -fmad=false so
+// scalar control reproduces the reference's Python-float operation order
+// exactly; dot products request FMA explicitly with fma().
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rapdb {
+
+constexpr int kThreads = 288;      // 8 consumer warps + 1 bulk-copy producer warp
+constexpr int kConsumerWarps = 8;
+constexpr int kWarps = 9;
+constexpr int kMaxTR = 32;         // rows per tile upper bound
+
+enum Slot {
+  S_BALL_V = 0, S_BALL_L,                       // dual-ball norms of the trial dual
+  S_DP, S_GXDX, S_DD, S_MIXV, S_MIXL,           // yx phase 2 / xy phase 1+4
+  S_DGY, S_NEWV, S_NEWL,                        // yx phase 4 / xy phase 4
+  S_GXD1, S_GXD2,                               // xy: |gx_new-gx_yk|^2, |gx_yk-gx_cur|^2
+  S_STAT, S_EQ2, S_COMP, S_GPOS2, S_GPOS1,      // KKT
+  S_PHIV, S_PHIL,                               // Phi at a (re)start point
+  S_AVG_V, S_AVG_L,                             // ball norms of an average point
+  NSLOT
+};
+
+enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4 };
+enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
+                 ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6 };
+
+struct SolverState {
+  double tau_cand, tau_prev, gamma, sigma_prev, alpha, beta, sigma0, T, phi_k;
+  double fail_tau, fail_gamma;
+  double metrics[8];
+  double sweep_ns;
+  long long iters, evals_total, inner, fail_iter, sweeps;
+  int cur, ig_prev, ig_cur, ig_new, has_sigma0, status, has_metrics, pad;
+};
+
+struct DevProblem {
+  int n, m, p, k0, k1, nloc, nact, nzero;
+  long long ld;
+  const double* Q; const double* q; const double* r; const double* A; const double* b;
+  const double* lo; const double* hi;
+  double mu;
+  const int* act;        // [nact]  local index of each streamed (non-zero) matrix
+  const int* zero_list;  // [nzero] local index of each all-zero matrix
+  const int* seg_lo;     // [nact]  first CTA whose row range touches active matrix a
+  const int* seg_hi;     // [nact]  last CTA (inclusive)
+  const int* cta_a0;     // [G]     first active matrix of each CTA's row range
+  const int* mat_slot;   // [nloc]  active index a >= 0, or -(zero index)-1
+};
+
+struct DevParams {
+  int mode;              // 0 yx, 1 xy
+  int max_bt, ball;      // ball 0 none, 1 joint, 2 split
+  int pad;
+  double c_alpha, c_beta, delta, eta, tau_bar, gamma0, c_nm, r1, r2;
+};
+
+struct SweepPlan {
+  int TR;                // rows per tile (power of two <= 32)
+  int nstages;
+  int segmax;
+  int pad;
+  long long stage_bytes; // per ring slot (multiple of 128)
+  long long rows_total;  // nact * n
+  long long xs_bytes;    // x staging bytes (multiple of 128)
+};
+
+struct Work {
+  double *x, *U, *gval, *eqv, *y, *ytr, *gy, *gxb, *gxs, *xcum, *ycum, *part,
+         *segxu, *segqx, *zq, *aux, *aux2;
+  double* trace;
+  SolverState* st;
+  unsigned long long* bar;
+  int* abort_flag;
+};
+
+struct RunCfg {
+  long long max_iters, budget, stop_total;
+  int metrics_every, criterion, has_f_star, fixed_period, fixed_point, warm_tau, stop_at_fixed;
+  int op, src, reset_inner, reps;
+  double eps, eps_kkt, eps_feas, f_star;
+  const double* in_x; const double* in_v; const double* in_lam;   // explicit points
+  double* out_x; double* out_v; double* out_lam; double* out_u; double* out_g;
+};
+
+struct KArgs {
+  DevProblem P;
+  DevParams prm;
+  SweepPlan sp;
+  Work w;
+  RunCfg rc;
+};
+
+// ---------------------------------------------------------------- primitives
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n\t.reg .pred p;\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+               "selp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;"
+      :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void named_bar_consumers() {
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // butterfly: every lane holds the same bits
+}
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+}  // namespace rapdb

@@ -1,0 +1,605 @@
+// solver.cu -- kernel entry (op dispatch + the accepted-iteration loop) and
+// the C ABI declared in include/rapdb_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rapdb_b200.h"
+#include "solver_ops.cuh"
+
+namespace rapdb {
+
+__device__ __forceinline__ void trace_put(const KArgs& K, long long row, int col, double v) {
+  if (K.w.trace) K.w.trace[row * RAPDB_TRACE_COLS + col] = v;
+}
+
+// run_restarted's loop body on device (restarts.py:111-161) around
+// ApdbEngine.step (engine.py:198-259).
+__device__ void op_run(const KArgs& K, Sm& S) {
+  SolverState& st = *S.st;
+  const RunCfg& rc = K.rc;
+  const DevParams& prm = K.prm;
+  const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  long long done = 0;
+  int status = ST_LIMIT;
+  for (;;) {
+    double tau = st.tau_cand;
+    const double tau_start = tau;
+    const double slack = 1e-13 * (1.0 + fabs(st.phi_k));
+    int evals = 0, acc = 0;
+    TrialOut o{};
+    for (int t = 0; t <= prm.max_bt; ++t) {
+      const int r = prm.mode == 1 ? trial_xy(K, S, tau, slack, o) : trial_yx(K, S, tau, slack, o);
+      if (r < 0) { status = ST_ABORT; goto out; }
+      ++evals;
+      if (r == 1) { acc = 1; break; }
+      tau *= prm.eta;
+    }
+    if (!acc) {
+      if (threadIdx.x == 0) {
+        st.fail_tau = tau;
+        st.fail_gamma = st.gamma;
+        st.fail_iter = st.iters;
+      }
+      __syncthreads();
+      status = ST_NONCONV;
+      goto out;
+    }
+    roll(K, S, tau, evals, o);
+    ++done;
+    {
+      const long long total = st.iters;
+      const long long row = done - 1;
+      if (rec) {
+        trace_put(K, row, 0, (double)total);
+        trace_put(K, row, 1, tau_start);
+        trace_put(K, row, 2, tau);
+        trace_put(K, row, 3, o.sigma);
+        trace_put(K, row, 4, st.gamma);
+        trace_put(K, row, 5, (double)evals);
+        trace_put(K, row, 6, (double)st.evals_total);
+        trace_put(K, row, 7, qnan);
+        trace_put(K, row, 8, qnan);
+        trace_put(K, row, 9, qnan);
+        trace_put(K, row, 10, 0.0);
+      }
+      if (rc.criterion != 0 && rc.metrics_every > 0 &&
+          (total % rc.metrics_every == 0 || total == rc.budget)) {
+        // the trial's last phase wrote partial slots other CTAs may still read
+        if (!gsync(K, S)) { status = ST_ABORT; goto out; }
+        if (!dev_kkt(K, S)) { status = ST_ABORT; goto out; }
+        if (rec) {
+          trace_put(K, row, 7, st.metrics[0]);
+          trace_put(K, row, 8, st.metrics[4]);
+          trace_put(K, row, 9, st.metrics[7]);
+        }
+        if (terminated(rc, st.metrics)) { status = ST_CONVERGED; goto out; }
+      }
+      if (rc.fixed_period > 0 && st.inner >= rc.fixed_period && total < rc.budget) {
+        if (rc.stop_at_fixed) { status = ST_FIXED_DUE; goto out; }
+        if (!gsync(K, S)) { status = ST_ABORT; goto out; }
+        if (!dev_reinit(K, S, rc.fixed_point ? 2 : 1, rc.warm_tau)) { status = ST_ABORT; goto out; }
+        if (threadIdx.x == 0) st.inner = 0;
+        __syncthreads();
+        if (rec) trace_put(K, row, 10, 1.0);
+      }
+      if (rc.stop_total > 0 && total == rc.stop_total && total < rc.budget) { status = ST_CHECK_DUE; goto out; }
+      if (total >= rc.budget) { status = ST_BUDGET; goto out; }
+      if (done >= rc.max_iters) { status = ST_LIMIT; goto out; }
+    }
+  }
+out:
+  if (threadIdx.x == 0) st.status = status;
+  __syncthreads();
+}
+
+__device__ void op_get(const KArgs& K, Sm& S) {
+  const SolverState& st = *S.st;
+  const Work& w = K.w;
+  const int n = K.P.n, p = K.P.p, m = K.P.m, np = p + m;
+  const bool avg = K.rc.src == 2 && st.T > 0.0;
+  const double* xc = w.x + (long long)st.cur * n;
+  const double* yc = w.y + (long long)st.cur * np;
+  for (long long j = gtid(); j < n; j += gstride())
+    K.rc.out_x[j] = avg ? ldcg(w.xcum + j) / st.T : ldcg(xc + j);
+  for (long long j = gtid(); j < np; j += gstride()) {
+    const double v = avg ? ldcg(w.ycum + j) / st.T : ldcg(yc + j);
+    if (j < p) K.rc.out_v[j] = v; else K.rc.out_lam[j - p] = v;
+  }
+}
+
+__device__ void op_probe(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const int par = S.st->cur ^ 1;
+  for (int r = 0; r < max(1, K.rc.reps); ++r)
+    if (!sweep_sync(K, S, K.rc.in_x, par)) return;
+  for (long long i = gtid(); i <= P.m; i += gstride()) K.rc.out_g[i] = g_combine(K, (int)i);
+  const double* Up = K.w.U + (long long)par * P.nloc * P.n;
+  const long long tot = (long long)P.nloc * P.n;
+  for (long long j = gtid(); j < tot; j += gstride()) K.rc.out_u[j] = ldcg(Up + j);
+}
+
+}  // namespace rapdb
+
+using namespace rapdb;
+
+extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(const __grid_constant__ KArgs K) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ double s_red[kWarps * 8];
+  __shared__ double s_tot[NSLOT + 4];
+  __shared__ double s_part[2][kMaxTR][8];
+  __shared__ SolverState s_st;
+  __shared__ int s_flag[4];
+  Sm S;
+  S.xs = reinterpret_cast<double*>(dsm);
+  S.ring = dsm + K.sp.xs_bytes;
+  S.full = reinterpret_cast<uint64_t*>(S.ring + (long long)K.sp.nstages * K.sp.stage_bytes);
+  S.empty = S.full + K.sp.nstages;
+  S.stage = reinterpret_cast<double*>(S.ring);
+  S.red = s_red;
+  S.tot = s_tot;
+  S.part = s_part;
+  S.st = &s_st;
+  S.flag = s_flag;
+  S.gen = 0;
+  S.pseq = 0;
+  if (threadIdx.x == 0) {
+    s_st = *K.w.st;
+    for (int s = 0; s < K.sp.nstages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  switch (K.rc.op) {
+    case OP_RUN:
+      op_run(K, S);
+      break;
+    case OP_REINIT:
+      if (dev_reinit(K, S, K.rc.src, K.rc.warm_tau) && threadIdx.x == 0 && K.rc.reset_inner) s_st.inner = 0;
+      break;
+    case OP_KKT:
+      dev_kkt(K, S);
+      break;
+    case OP_GET:
+      op_get(K, S);
+      break;
+    case OP_PROBE:
+      op_probe(K, S);
+      break;
+    default:
+      break;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *K.w.st = s_st;
+}
+
+// ========================================================================
+// host side
+// ========================================================================
+
+struct rapdb_ctx {
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int nsm = 0, G = 0;
+  size_t optin = 0, dyn_smem = 0;
+  bool bound = false, have_params = false, have_ws = false;
+  DevProblem P{};
+  DevParams prm{};
+  SweepPlan sp{};
+  Work w{};
+  int* d_ints = nullptr;
+  long long ws_bytes = 0;
+  long long stage_cap = 0;  // doubles available in the staging area
+};
+
+namespace {
+
+int fail(rapdb_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(rapdb_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, RAPDB_EDEVICE, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+  } while (0)
+
+long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  long long off[24];
+  long long total;
+};
+
+enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
+             B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_COUNT };
+
+Layout layout_of(const rapdb_ctx* c) {
+  const long long n = c->P.n, m = c->P.m, p = c->P.p, np = n > 0 ? p + m : 0;
+  const long long G = c->G, nloc = c->P.nloc;
+  long long sz[B_COUNT];
+  sz[B_X] = 2 * n * 8;
+  sz[B_U] = 2 * nloc * n * 8;
+  sz[B_GVAL] = 2 * (m + 1) * 8;
+  sz[B_EQV] = 2 * std::max(p, 1LL) * 8;
+  sz[B_Y] = 2 * std::max(np, 1LL) * 8;
+  sz[B_YTR] = std::max(np, 1LL) * 8;
+  sz[B_GY] = 3 * std::max(np, 1LL) * 8;
+  sz[B_GXB] = 3 * n * 8;
+  sz[B_GXS] = n * 8;
+  sz[B_XCUM] = n * 8;
+  sz[B_YCUM] = std::max(np, 1LL) * 8;
+  sz[B_PART] = (long long)NSLOT * G * 8;
+  sz[B_SEGXU] = G * c->sp.segmax * 8;
+  sz[B_SEGQX] = G * c->sp.segmax * 8;
+  sz[B_ZQ] = std::max(c->P.nzero, 1) * 8LL;
+  sz[B_AUX] = n * 8;
+  sz[B_AUX2] = n * 8;
+  sz[B_ST] = sizeof(SolverState);
+  sz[B_BAR] = 64;
+  sz[B_ABORT] = 64;
+  Layout L;
+  long long o = 0;
+  for (int i = 0; i < B_COUNT; ++i) {
+    L.off[i] = o;
+    o += align_up(sz[i], 256);
+  }
+  L.total = o;
+  return L;
+}
+
+int launch(rapdb_ctx* c, RunCfg rc) {
+  if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
+  KArgs K;
+  K.P = c->P;
+  K.prm = c->prm;
+  K.sp = c->sp;
+  K.w = c->w;
+  K.rc = rc;
+  CK(cudaMemsetAsync(c->w.bar, 0, 128, c->stream));
+  void* args[] = {&K};
+  CK(cudaLaunchCooperativeKernel((const void*)rapdb_solver_kernel, dim3(c->G), dim3(kThreads), args,
+                                 c->dyn_smem, c->stream));
+  CK(cudaGetLastError());
+  return RAPDB_OK;
+}
+
+int read_state(rapdb_ctx* c, SolverState* st) {
+  int ab = 0;
+  CK(cudaMemcpyAsync(st, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (ab) return fail(c, RAPDB_EDEVICE, "device watchdog fired (grid barrier timeout)");
+  return RAPDB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rapdb_abi_version(void) { return 1; }
+
+int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
+  if (!out) return RAPDB_EINPUT;
+  *out = nullptr;
+  rapdb_ctx* c = new rapdb_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return RAPDB_EDEVICE;
+  }
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  c->nsm = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  c->optin = (size_t)v;
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  if (!coop || c->nsm <= 0) {
+    delete c;
+    return RAPDB_EDEVICE;
+  }
+  *out = c;
+  return RAPDB_OK;
+}
+
+void rapdb_destroy(rapdb_ctx* c) {
+  if (!c) return;
+  if (c->d_ints) cudaFree(c->d_ints);
+  delete c;
+}
+
+int rapdb_last_error(const rapdb_ctx* c, char* buf, int size) {
+  if (!c || !buf || size <= 0) return RAPDB_EINPUT;
+  std::snprintf(buf, (size_t)size, "%s", c->err.c_str());
+  return RAPDB_OK;
+}
+
+int rapdb_set_stream(rapdb_ctx* c, void* s) {
+  if (!c) return RAPDB_EINPUT;
+  c->stream = static_cast<cudaStream_t>(s);
+  return RAPDB_OK;
+}
+
+int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long long ld, const double* Q,
+                     const double* q, const double* r, const double* A, const double* b,
+                     const double* lower, const double* upper, double mu, const unsigned char* zero_flags) {
+  if (!c) return RAPDB_EINPUT;
+  if (n <= 0 || m < 0 || p < 0) return fail(c, RAPDB_EINPUT, "need n > 0, m >= 0, p >= 0");
+  if (k0 < 0 || k1 > m + 1 || k1 <= k0) return fail(c, RAPDB_EINPUT, "bad local matrix range");
+  if (ld < n || (ld & 1)) return fail(c, RAPDB_EINPUT, "ld must be even and >= n");
+  if (c->nranks != 1 || k0 != 0 || k1 != m + 1)
+    return fail(c, RAPDB_ECONFIG, "constraint sharding across ranks is not enabled in this build");
+  if (!Q || !q || !r || !lower || !upper || (p > 0 && (!A || !b)))
+    return fail(c, RAPDB_EINPUT, "null data pointer");
+  if ((reinterpret_cast<uintptr_t>(Q) & 15) != 0) return fail(c, RAPDB_EINPUT, "Q must be 16-byte aligned");
+  const int nloc = k1 - k0;
+  std::vector<int> act, zl, slot(nloc);
+  for (int i = 0; i < nloc; ++i) {
+    if (zero_flags && zero_flags[i]) {
+      slot[i] = -(int)zl.size() - 1;
+      zl.push_back(i);
+    } else {
+      slot[i] = (int)act.size();
+      act.push_back(i);
+    }
+  }
+  // sweep plan: rows per tile, ring depth, shared memory
+  const long long row_bytes = ld * 8;
+  SweepPlan sp{};
+  int TR = 1;
+  while (TR * 2 <= kMaxTR && (long long)(TR * 2) * row_bytes <= 32768) TR *= 2;
+  sp.TR = TR;
+  sp.stage_bytes = align_up((long long)TR * row_bytes, 128);
+  sp.xs_bytes = align_up(row_bytes, 128);
+  const long long static_smem = 8 * (kWarps * 8 + NSLOT + 4 + 2 * kMaxTR * 8) + (long long)sizeof(SolverState) + 64;
+  const long long budget = (long long)c->optin - static_smem - 2048;
+  long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
+  ns = std::min(ns, 8LL);
+  if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense tile ring (row > ~96 KB)");
+  sp.nstages = (int)ns;
+  c->dyn_smem = (size_t)(sp.xs_bytes + ns * sp.stage_bytes + 2 * ns * 8);
+  c->stage_cap = ns * sp.stage_bytes / 8;
+  if (2LL * (p + m) > c->stage_cap)
+    return fail(c, RAPDB_ECONFIG, "too many multipliers for the shared-memory dual staging area");
+  cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->dyn_smem);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaFuncSetAttribute");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)rapdb_solver_kernel, kThreads, c->dyn_smem);
+  if (e != cudaSuccess) return cuda_fail(c, e, "occupancy");
+  if (occ < 1) return fail(c, RAPDB_EDEVICE, "solver kernel cannot be resident");
+  c->G = c->nsm * occ;
+  const int G = c->G;
+  // row partition of the streamed rows over CTAs and the segment tables
+  const long long R = (long long)act.size() * n;
+  sp.rows_total = R;
+  std::vector<int> cta_a0(G, 0), seg_lo(std::max<size_t>(act.size(), 1), 0), seg_hi(std::max<size_t>(act.size(), 1), -1);
+  int segmax = 1;
+  for (int bb = 0; bb < G; ++bb) {
+    const long long rs = (long long)bb * R / G, re = (long long)(bb + 1) * R / G;
+    if (rs >= re) {
+      cta_a0[bb] = 0;
+      continue;
+    }
+    const int a_lo = (int)(rs / n), a_hi = (int)((re - 1) / n);
+    cta_a0[bb] = a_lo;
+    segmax = std::max(segmax, a_hi - a_lo + 1);
+    for (int a = a_lo; a <= a_hi; ++a) {
+      if (seg_hi[a] < 0) seg_lo[a] = bb;
+      seg_hi[a] = bb;
+    }
+  }
+  sp.segmax = segmax;
+  std::vector<int> ints;
+  auto put = [&](const std::vector<int>& v) {
+    size_t o = ints.size();
+    ints.insert(ints.end(), v.begin(), v.end());
+    if (v.empty()) ints.push_back(0);
+    return o;
+  };
+  const size_t o_act = put(act), o_zl = put(zl), o_lo = put(seg_lo), o_hi = put(seg_hi),
+               o_a0 = put(cta_a0), o_slot = put(slot);
+  if (c->d_ints) cudaFree(c->d_ints);
+  c->d_ints = nullptr;
+  CK(cudaMalloc(&c->d_ints, ints.size() * sizeof(int)));
+  CK(cudaMemcpy(c->d_ints, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+  DevProblem P{};
+  P.n = n; P.m = m; P.p = p; P.k0 = k0; P.k1 = k1; P.nloc = nloc;
+  P.nact = (int)act.size(); P.nzero = (int)zl.size(); P.ld = ld;
+  P.Q = Q; P.q = q; P.r = r; P.A = A; P.b = b; P.lo = lower; P.hi = upper; P.mu = mu;
+  P.act = c->d_ints + o_act; P.zero_list = c->d_ints + o_zl; P.seg_lo = c->d_ints + o_lo;
+  P.seg_hi = c->d_ints + o_hi; P.cta_a0 = c->d_ints + o_a0; P.mat_slot = c->d_ints + o_slot;
+  c->P = P;
+  c->sp = sp;
+  c->bound = true;
+  c->have_ws = false;
+  return RAPDB_OK;
+}
+
+int rapdb_set_params(rapdb_ctx* c, int mode, double c_alpha, double c_beta, double delta, double eta,
+                     double tau_bar, double gamma0, int nonmonotone, int max_backtracks, int ball_kind,
+                     double r1, double r2) {
+  if (!c) return RAPDB_EINPUT;
+  if (mode != 0 && mode != 1) return fail(c, RAPDB_ECONFIG, "unknown mode");
+  if (!(eta > 0.0 && eta < 1.0)) return fail(c, RAPDB_ECONFIG, "eta must lie in (0, 1)");
+  if (tau_bar <= 0 || gamma0 <= 0) return fail(c, RAPDB_ECONFIG, "tau_bar and gamma0 must be positive");
+  if (max_backtracks < 0) return fail(c, RAPDB_ECONFIG, "max_backtracks must be >= 0");
+  if (ball_kind < 0 || ball_kind > 2) return fail(c, RAPDB_ECONFIG, "unknown dual ball");
+  DevParams d{};
+  d.mode = mode; d.c_alpha = c_alpha; d.c_beta = c_beta; d.delta = delta; d.eta = eta;
+  d.tau_bar = tau_bar; d.gamma0 = gamma0; d.c_nm = nonmonotone ? 1.0 : 0.0; d.max_bt = max_backtracks;
+  d.ball = ball_kind; d.r1 = r1; d.r2 = r2;
+  c->prm = d;
+  c->have_params = true;
+  return RAPDB_OK;
+}
+
+long long rapdb_workspace_bytes(rapdb_ctx* c) {
+  if (!c || !c->bound) return -1;
+  return layout_of(c).total;
+}
+
+int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
+  if (!c || !c->bound) return RAPDB_EINPUT;
+  const Layout L = layout_of(c);
+  if (!dptr || bytes < L.total) return fail(c, RAPDB_EINPUT, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(dptr) & 255) != 0) return fail(c, RAPDB_EINPUT, "workspace must be 256-byte aligned");
+  char* base = static_cast<char*>(dptr);
+  auto D = [&](int i) { return reinterpret_cast<double*>(base + L.off[i]); };
+  Work w{};
+  w.x = D(B_X); w.U = D(B_U); w.gval = D(B_GVAL); w.eqv = D(B_EQV); w.y = D(B_Y); w.ytr = D(B_YTR);
+  w.gy = D(B_GY); w.gxb = D(B_GXB); w.gxs = D(B_GXS); w.xcum = D(B_XCUM); w.ycum = D(B_YCUM);
+  w.part = D(B_PART); w.segxu = D(B_SEGXU); w.segqx = D(B_SEGQX); w.zq = D(B_ZQ); w.aux = D(B_AUX);
+  w.aux2 = D(B_AUX2);
+  w.trace = nullptr;
+  w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
+  w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);
+  w.abort_flag = reinterpret_cast<int*>(base + L.off[B_ABORT]);
+  c->w = w;
+  CK(cudaMemsetAsync(dptr, 0, (size_t)L.total, c->stream));
+  SolverState st{};
+  st.ig_prev = 0; st.ig_cur = 1; st.ig_new = 2;
+  CK(cudaMemcpyAsync(w.st, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->have_ws = true;
+  return RAPDB_OK;
+}
+
+int rapdb_reinit(rapdb_ctx* c, int source, const double* x, const double* v, const double* lam, int warm_tau,
+                 int reset_inner) {
+  if (!c) return RAPDB_EINPUT;
+  if (source < 0 || source > 2) return fail(c, RAPDB_EINPUT, "bad reinit source");
+  if (source == 0 && (!x || (c->P.p > 0 && !v) || (c->P.m > 0 && !lam)))
+    return fail(c, RAPDB_EINPUT, "explicit reinit needs x, v, lam");
+  RunCfg rc{};
+  rc.op = OP_REINIT;
+  rc.src = source;
+  rc.warm_tau = warm_tau;
+  rc.reset_inner = reset_inner;
+  rc.in_x = x; rc.in_v = v; rc.in_lam = lam;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  return read_state(c, &st);
+}
+
+int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_result* out) {
+  if (!c || !a || !out) return RAPDB_EINPUT;
+  if (a->max_iters < 1) return fail(c, RAPDB_ECONFIG, "need max_iters >= 1");
+  RunCfg rc{};
+  rc.op = OP_RUN;
+  rc.max_iters = a->max_iters; rc.budget = a->budget; rc.stop_total = a->stop_total;
+  rc.metrics_every = a->metrics_every; rc.criterion = a->criterion;
+  rc.eps = a->eps; rc.eps_kkt = a->eps_kkt; rc.eps_feas = a->eps_feas;
+  rc.f_star = a->f_star; rc.has_f_star = a->has_f_star;
+  rc.fixed_period = a->fixed_period; rc.fixed_point = a->fixed_point; rc.warm_tau = a->warm_tau;
+  rc.stop_at_fixed = a->stop_at_fixed;
+  Work saved = c->w;
+  c->w.trace = trace;
+  SolverState before;
+  int r = read_state(c, &before);
+  if (!r) r = launch(c, rc);
+  c->w = saved;
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  if (r) return r;
+  std::memset(out, 0, sizeof(*out));
+  out->status = st.status;
+  out->iters_done = st.iters - before.iters;
+  out->total = st.iters;
+  out->inner = st.inner;
+  out->evals_total = st.evals_total;
+  out->tau_cand = st.tau_cand; out->tau_prev = st.tau_prev; out->gamma = st.gamma;
+  out->sigma_prev = st.sigma_prev; out->T = st.T;
+  out->fail_tau = st.fail_tau; out->fail_gamma = st.fail_gamma; out->fail_iter = st.fail_iter;
+  for (int i = 0; i < 8; ++i) out->metrics[i] = st.metrics[i];
+  out->has_metrics = st.has_metrics;
+  out->sweep_ns = st.sweep_ns;
+  out->sweeps = st.sweeps;
+  if (st.status == ST_ABORT) return fail(c, RAPDB_EDEVICE, "device watchdog fired");
+  if (st.status == ST_NONCONV) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "backtracking failed after %d shrinkages (tau=%.3e); check data validity / Lipschitz regime",
+                  c->prm.max_bt, st.fail_tau);
+    c->err = buf;
+    return RAPDB_ENONCONV;
+  }
+  return RAPDB_OK;
+}
+
+int rapdb_kkt(rapdb_ctx* c, int has_f_star, double f_star, double* out) {
+  if (!c || !out) return RAPDB_EINPUT;
+  RunCfg rc{};
+  rc.op = OP_KKT;
+  rc.has_f_star = has_f_star;
+  rc.f_star = f_star;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  if (r) return r;
+  for (int i = 0; i < 8; ++i) out[i] = st.metrics[i];
+  return RAPDB_OK;
+}
+
+int rapdb_get_iterate(rapdb_ctx* c, int which, double* x, double* v, double* lam) {
+  if (!c || !x || (c->P.p > 0 && !v) || (c->P.m > 0 && !lam)) return RAPDB_EINPUT;
+  RunCfg rc{};
+  rc.op = OP_GET;
+  rc.src = which == 1 ? 2 : 1;
+  rc.out_x = x; rc.out_v = v; rc.out_lam = lam;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  return read_state(c, &st);
+}
+
+int rapdb_probe_sweep(rapdb_ctx* c, const double* x, double* u, double* g, int reps, float* ms) {
+  if (!c || !x || !u || !g) return RAPDB_EINPUT;
+  RunCfg rc{};
+  rc.op = OP_PROBE;
+  rc.in_x = x; rc.out_u = u; rc.out_g = g;
+  rc.reps = reps < 1 ? 1 : reps;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c->stream));
+  int r = launch(c, rc);
+  CK(cudaEventRecord(e1, c->stream));
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  float t = 0;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms) *ms = t / (float)rc.reps;
+  return r;
+}
+
+int rapdb_smoothed_gap(rapdb_ctx* c, int source, double xi, double tol, const double* x_warm, double* x_cand,
+                       double* out) {
+  (void)source; (void)xi; (void)tol; (void)x_warm; (void)x_cand; (void)out;
+  return fail(c, RAPDB_ECONFIG, "smoothed_gap not built yet");
+}
+
+}  // extern "C"

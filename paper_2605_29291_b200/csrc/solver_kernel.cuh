@@ -1,0 +1,332 @@
+// solver_kernel.cuh -- the persistent, cooperative rAPDB kernel (sm_100a, fp64).
+//
+// One CTA per SM (288 threads: 8 consumer warps + 1 TMA-bulk producer warp,
+// ~200 KB of shared memory for the Q-tile ring).  A launch executes one "op":
+//   OP_RUN    accepted iterations with device-side backtracking, KKT cadence,
+//             termination and fixed restarts  (engine.py:198-259 inside
+//             restarts.py:111-161);
+//   OP_REINIT ApdbEngine.reinit from an explicit / last / average point
+//             (engine.py:102-136);
+//   OP_KKT    kkt_residual at the current iterate (diagnostics.py:96-113);
+//   OP_GET    engine.last / engine.average() (engine.py:262-272);
+//   OP_PROBE  one (or reps) fused Q sweeps at a given x, for KATs and timing.
+//
+// Phases inside an op are separated by a software grid barrier (the launch is
+// cooperative, so all CTAs are co-resident).  Every cross-CTA sum is a
+// two-level fixed-order reduction (warp butterfly -> per-CTA partial -> every
+// CTA sums the G partials in CTA order), so results are bitwise reproducible
+// and every CTA derives the same accept/reject decision without a broadcast.
+#pragma once
+#include "rapdb_dev.cuh"
+
+namespace rapdb {
+
+struct Sm {
+  double* xs;              // staged x (ld doubles, zero padded)
+  unsigned char* ring;     // nstages * stage_bytes bulk-copy ring
+  uint64_t* full;          // [nstages] TMA-complete barriers
+  uint64_t* empty;         // [nstages] consumer-release barriers
+  double* stage;           // the ring reused as a dual-vector staging area outside sweeps
+  double* red;             // [kWarps*8] block-reduction scratch
+  double* tot;             // [NSLOT] grid totals
+  double (*part)[kMaxTR][8];
+  SolverState* st;
+  int* flag;
+  unsigned long long gen;  // grid-barrier generation (thread 0)
+  unsigned pseq;           // pipeline sequence (producer lane / consumers)
+};
+
+// ------------------------------------------------------------ grid barrier
+
+__device__ __noinline__ bool gsync(const KArgs& K, Sm& S) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.gen += gridDim.x;
+    __threadfence();
+    atomicAdd(K.w.bar, 1ULL);
+    volatile unsigned long long* vb = K.w.bar;
+    volatile int* va = K.w.abort_flag;
+    const unsigned long long t0 = globaltimer();
+    int ab = 0;
+    while (*vb < S.gen) {
+      if (*va) { ab = 1; break; }
+      if (globaltimer() - t0 > 30000000000ull) {   // 30 s watchdog
+        atomicExch(K.w.abort_flag, 1);
+        ab = 1;
+        break;
+      }
+      __nanosleep(16);
+    }
+    __threadfence();
+    S.flag[0] = ab;
+  }
+  __syncthreads();
+  return S.flag[0] == 0;
+}
+
+// ------------------------------------------------------ fixed-order sums
+
+template <int NK>
+__device__ __forceinline__ void put_partials(const KArgs& K, Sm& S, const double (&v)[NK],
+                                             const int (&slots)[NK]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const double t = warp_sum(v[k]);
+    if (lane == 0) S.red[w * 8 + k] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < NK) {
+    double s = S.red[threadIdx.x];
+    for (int i = 1; i < kWarps; ++i) s += S.red[i * 8 + threadIdx.x];
+    K.w.part[(long long)slots[threadIdx.x] * gridDim.x + blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <int NK>
+__device__ __forceinline__ void get_totals(const KArgs& K, Sm& S, const int (&slots)[NK]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  for (int k = w; k < NK; k += kWarps) {
+    const double* p = K.w.part + (long long)slots[k] * G;
+    double s = 0.0;
+    for (int i = lane; i < G; i += 32) s += ldcg(p + i);
+    s = warp_sum(s);
+    if (lane == 0) S.tot[slots[k]] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ long long gtid() { return (long long)blockIdx.x * kThreads + threadIdx.x; }
+__device__ __forceinline__ long long gstride() { return (long long)gridDim.x * kThreads; }
+
+__device__ __forceinline__ double clipd(double w, double lo, double hi) { return fmin(fmax(w, lo), hi); }
+
+// ---------------------------------------------------------------- sweep
+
+__device__ __forceinline__ double rowdot(const double* row, const double* xs, long long npairs,
+                                         int start, int step) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  const double2* x2 = reinterpret_cast<const double2*>(xs);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  long long k = start;
+  for (; k + step < npairs; k += 2 * step) {
+    const double2 q0 = r2[k], x0 = x2[k], q1 = r2[k + step], x1 = x2[k + step];
+    a0 = fma(q0.x, x0.x, a0);
+    a1 = fma(q0.y, x0.y, a1);
+    a2 = fma(q1.x, x1.x, a2);
+    a3 = fma(q1.y, x1.y, a3);
+  }
+  if (k < npairs) {
+    const double2 q0 = r2[k], x0 = x2[k];
+    a0 = fma(q0.x, x0.x, a0);
+    a1 = fma(q0.y, x0.y, a1);
+  }
+  return warp_sum((a0 + a1) + (a2 + a3));
+}
+
+// One fused pass over the streamed (non-zero) local matrices at x:
+//   U[par][lm][j] = (Q_lm x)_j, per-CTA segment sums of x_j u_j and q_j x_j,
+//   eqv[par] = A x - b, zq = q.x for all-zero matrices.
+// The CTA's contiguous row range is streamed by 1-D TMA bulk copies into an
+// nstages-deep shared-memory ring (mbarrier full/empty pipeline).
+__device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
+  const DevProblem& P = K.P;
+  const SweepPlan& sp = K.sp;
+  const int n = P.n;
+  const long long ld = P.ld;
+  for (long long j = threadIdx.x; j < ld; j += kThreads) S.xs[j] = (j < n) ? ldcg(xsrc + j) : 0.0;
+  // the ring doubles as a generic-proxy staging area between sweeps: order
+  // those accesses before the async-proxy (bulk copy) writes below
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long rs = ((long long)b * sp.rows_total) / G;
+  const long long re = ((long long)(b + 1) * sp.rows_total) / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* U = K.w.U + (long long)par * P.nloc * n;
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      long long row = rs;
+      while (row < re) {
+        const int a = (int)(row / n);
+        const int jr = (int)(row - (long long)a * n);
+        const int cnt = (int)min((long long)sp.TR, min((long long)(n - jr), re - row));
+        const unsigned s = S.pseq % sp.nstages, use = S.pseq / sp.nstages;
+        if (use > 0) mbar_wait(&S.empty[s], (use - 1) & 1);
+        const unsigned bytes = (unsigned)(cnt * ld * 8);
+        mbar_expect_tx(&S.full[s], bytes);
+        const double* src = P.Q + ((long long)__ldg(P.act + a) * n + jr) * ld;
+        bulk_g2s(S.ring + (long long)s * sp.stage_bytes, src, bytes, &S.full[s], pol);
+        ++S.pseq;
+        row += cnt;
+      }
+    }
+  } else {
+    const int a0 = __ldg(P.cta_a0 + b);
+    const int Sg = sp.TR >= 8 ? 1 : 8 / sp.TR;
+    int cur_a = -1;
+    double accx = 0.0, accq = 0.0;
+    long long row = rs;
+    while (row < re) {
+      const int a = (int)(row / n);
+      const int jr = (int)(row - (long long)a * n);
+      const int cnt = (int)min((long long)sp.TR, min((long long)(n - jr), re - row));
+      const unsigned s = S.pseq % sp.nstages, use = S.pseq / sp.nstages;
+      const int buf = S.pseq & 1;
+      mbar_wait(&S.full[s], use & 1);
+      const double* tile = reinterpret_cast<const double*>(S.ring + (long long)s * sp.stage_bytes);
+      if (sp.TR >= 8) {
+        for (int rr = warp; rr < cnt; rr += kConsumerWarps) {
+          const double v = rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32);
+          if (lane == 0) S.part[buf][rr][0] = v;
+        }
+      } else {
+        const int rr = warp / Sg, ps = warp % Sg;
+        if (rr < cnt) {
+          const double v = rowdot(tile + rr * ld, S.xs, ld / 2, ps * 32 + lane, Sg * 32);
+          if (lane == 0) S.part[buf][rr][ps] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
+      named_bar_consumers();
+      if (warp == 0) {
+        const int lm = __ldg(P.act + a);
+        double cx = 0.0, cq = 0.0;
+        if (lane < cnt) {
+          double u = S.part[buf][lane][0];
+          for (int k = 1; k < Sg; ++k) u += S.part[buf][lane][k];
+          const int j = jr + lane;
+          U[(long long)lm * n + j] = u;
+          const double xj = S.xs[j];
+          cx = xj * u;
+          cq = __ldg(P.q + (long long)(P.k0 + lm) * n + j) * xj;
+        }
+        if (a != cur_a) {
+          if (cur_a >= 0 && lane == 0) {
+            K.w.segxu[(long long)b * sp.segmax + (cur_a - a0)] = accx;
+            K.w.segqx[(long long)b * sp.segmax + (cur_a - a0)] = accq;
+          }
+          cur_a = a;
+          accx = 0.0;
+          accq = 0.0;
+        }
+        for (int l = 0; l < cnt; ++l) {           // row order within the segment
+          accx += __shfl_sync(0xffffffffu, cx, l);
+          accq += __shfl_sync(0xffffffffu, cq, l);
+        }
+      }
+      ++S.pseq;
+      row += cnt;
+    }
+    if (warp == 0 && lane == 0 && cur_a >= 0) {
+      K.w.segxu[(long long)b * sp.segmax + (cur_a - a0)] = accx;
+      K.w.segqx[(long long)b * sp.segmax + (cur_a - a0)] = accq;
+    }
+  }
+  __syncthreads();
+  // equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
+  const long long items = (long long)P.p + P.nzero;
+  for (long long it = (long long)b * kWarps + warp; it < items; it += (long long)G * kWarps) {
+    const double* vec = it < P.p ? P.A + it * n : P.q + (long long)(P.k0 + __ldg(P.zero_list + (it - P.p))) * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(__ldg(vec + j), S.xs[j], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (it < P.p) K.w.eqv[(long long)par * P.p + it] = s - __ldg(P.b + it);
+      else K.w.zq[it - P.p] = s;
+    }
+  }
+}
+
+// g_i (i = 0..m, i = 0 is f) from the sweep's segment sums: 0.5*x.u + q.x + r
+// (problem.py:166-177 operation order).
+__device__ __forceinline__ double g_combine(const KArgs& K, int i) {
+  const DevProblem& P = K.P;
+  const int lm = i - P.k0;
+  const int slot = __ldg(P.mat_slot + lm);
+  double sxu, sqx;
+  if (slot < 0) {
+    sxu = 0.0;
+    sqx = ldcg(K.w.zq + (-slot - 1));
+  } else {
+    const int lo = __ldg(P.seg_lo + slot), hi = __ldg(P.seg_hi + slot);
+    sxu = 0.0;
+    sqx = 0.0;
+    for (int b = lo; b <= hi; ++b) {
+      const long long at = (long long)b * K.sp.segmax + (slot - __ldg(P.cta_a0 + b));
+      sxu += ldcg(K.w.segxu + at);
+      sqx += ldcg(K.w.segqx + at);
+    }
+  }
+  return 0.5 * sxu + sqx + __ldg(P.r + i);
+}
+
+// grad_x Phi(x, (v, lam)) at coordinate j from the U-cache (problem.py:207-217):
+// (u_0 + q_0) then, in i order, + lam_i (u_i + q_i) for lam_i != 0, then + A^T v.
+__device__ __forceinline__ double recombine(const KArgs& K, const double* Upar, const double* lam_s,
+                                            const double* v_s, long long j) {
+  const DevProblem& P = K.P;
+  const long long n = P.n;
+  double acc = ldcg(Upar + j) + __ldg(P.q + j);
+  int i = 1;
+  for (; i + 3 <= P.m; i += 4) {
+    double u[4], qq[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u[k] = ldcg(Upar + (long long)(i + k) * n + j);
+      qq[k] = __ldg(P.q + (long long)(i + k) * n + j);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double l = lam_s[i + k - 1];
+      const double t = l * (u[k] + qq[k]);
+      acc = (l != 0.0) ? acc + t : acc;
+    }
+  }
+  for (; i <= P.m; ++i) {
+    const double l = lam_s[i - 1];
+    if (l != 0.0) acc = acc + l * (ldcg(Upar + (long long)i * n + j) + __ldg(P.q + (long long)i * n + j));
+  }
+  if (P.p > 0) {
+    double t = 0.0;
+    for (int l = 0; l < P.p; ++l) t = t + __ldg(P.A + (long long)l * n + j) * v_s[l];
+    acc = acc + t;
+  }
+  return acc;
+}
+
+// dual-ball radial scaling factors from the two squared norms (geometry.py:263-311)
+struct BallScale { double sv, sl; int av, al; };
+
+__device__ __forceinline__ BallScale ball_scale(const DevParams& prm, double vv, double ll) {
+  BallScale r{1.0, 1.0, 0, 0};
+  if (prm.ball == 1) {
+    const double nrm = sqrt(vv + ll);
+    if (!(nrm <= prm.r1)) { r.sv = r.sl = prm.r1 / nrm; r.av = r.al = 1; }
+  } else if (prm.ball == 2) {
+    const double nv = sqrt(vv), nl = sqrt(ll);
+    if (nv > prm.r1) { r.sv = prm.r1 / nv; r.av = 1; }
+    if (nl > prm.r2) { r.sl = prm.r2 / nl; r.al = 1; }
+  }
+  return r;
+}
+
+// stage (v, lam) = ball(src) into shared memory: v_s[0..p), lam_s[0..m)
+__device__ __forceinline__ void stage_dual(const KArgs& K, const double* src, BallScale bs,
+                                           double* v_s, double* lam_s) {
+  const int p = K.P.p, m = K.P.m;
+  for (int j = threadIdx.x; j < p + m; j += kThreads) {
+    double yv = ldcg(src + j);
+    if (j < p) v_s[j] = bs.av ? bs.sv * yv : yv;
+    else lam_s[j - p] = bs.al ? bs.sl * yv : yv;
+  }
+  __syncthreads();
+}
+
+}  // namespace rapdb

@@ -1,0 +1,115 @@
+"""Solution-quality metrics: drop-in for ``pkg/src/rapdb/diagnostics.py``.
+
+Inside ``run_restarted`` the KKT residual (diagnostics.py:96-113) and the
+termination test (:252-263) run in the persistent kernel every
+``metrics_every`` iterations, from the cached U = [Q_i x_k] (no extra sweep).
+The standalone functions below evaluate at a user-given point on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .errors import ConfigurationError
+from .problem import Iterate, ProblemInstance
+
+
+@dataclass
+class Metrics:
+    kkt_residual: float
+    stationarity: float
+    primal_eq: float
+    complementarity: float
+    infeas: float
+    f_value: float
+    mean_pos_violation: float
+    subopt_abs: Optional[float] = None
+    gap_xi: Optional[float] = None
+    gap_reliable: bool = True
+
+
+@dataclass
+class TerminationCriteria:
+    eps: float = 1e-7
+    f_star: Optional[float] = None
+    criterion: str = "paper51"
+    eps_kkt: float = 1e-7
+    eps_feas: float = 1e-7
+
+    def code(self) -> int:
+        if self.criterion == "conic":
+            return 1
+        if self.criterion == "paper51":
+            return 2
+        raise ConfigurationError(f"unknown termination criterion {self.criterion!r}")
+
+
+@dataclass
+class Certificate:
+    iterations: int
+    residual: float
+    converged: bool
+
+
+def metrics_from(vals, f_star=None) -> Metrics:
+    return Metrics(kkt_residual=vals[0], stationarity=vals[1], primal_eq=vals[2],
+                   complementarity=vals[3], infeas=vals[4], f_value=vals[5],
+                   mean_pos_violation=vals[6],
+                   subopt_abs=None if f_star is None else vals[7])
+
+
+def kkt_residual(inst: ProblemInstance, z: Iterate, f_star: Optional[float] = None) -> Metrics:
+    """r(x, v, lam) at an arbitrary point, evaluated on the device."""
+    ev = inst._evaluator()
+    torch = ev.ctx.torch
+    d = ev.data
+    x = ev._x(z.x)
+    gx = ev.grad_x_t(z)
+    stat = float(torch.linalg.vector_norm(x - torch.clamp(x - gx, d.lower, d.upper)))
+    e = ev.eq(z.x) if inst.p else torch.zeros(0, dtype=torch.float64, device=x.device)
+    eq = float(torch.linalg.vector_norm(e))
+    u, g = ev.sweep(z.x)
+    gi = g[1:]
+    lam = ev._x(z.lam)
+    comp = float(torch.linalg.vector_norm(torch.minimum(lam, -gi))) if inst.m else 0.0
+    gp = torch.clamp(gi, min=0.0)
+    infeas = float(torch.sqrt(e @ e + gp @ gp))
+    mpv = float(gp.mean()) if inst.m else 0.0
+    f = float(g[0])
+    return Metrics(kkt_residual=stat + eq + comp, stationarity=stat, primal_eq=eq,
+                   complementarity=comp, infeas=infeas, f_value=f, mean_pos_violation=mpv,
+                   subopt_abs=None if f_star is None else f - f_star)
+
+
+def infeasibility(inst: ProblemInstance, x) -> float:
+    return kkt_residual(inst, Iterate(x, np.zeros(inst.p), np.zeros(inst.m))).infeas
+
+
+def check_termination(metrics: Metrics, criteria: TerminationCriteria) -> bool:
+    """diagnostics.py:252-263 (the same predicate the kernel evaluates)."""
+    if criteria.criterion == "paper51":
+        if criteria.f_star is None:
+            return (metrics.kkt_residual <= criteria.eps_kkt
+                    and metrics.infeas <= criteria.eps_feas)
+        rel_gap = abs(metrics.f_value - criteria.f_star) / (1.0 + abs(criteria.f_star))
+        return max(rel_gap, metrics.mean_pos_violation) <= criteria.eps
+    if criteria.criterion == "conic":
+        return (metrics.kkt_residual <= criteria.eps_kkt
+                and metrics.infeas <= criteria.eps_feas)
+    raise ConfigurationError(f"unknown termination criterion {criteria.criterion!r}")
+
+
+def smoothed_gap(inst: ProblemInstance, z: Iterate, xi: float, dual_ball=None,
+                 subsolver_tol: float = 1e-9, x_warm=None):
+    """G_xi(z) (diagnostics.py:120-163) on the device; returns (gap, Certificate)."""
+    from .engine import ApdbEngine, SolverConfig
+    from .geometry import Unbounded
+    if xi <= 0:
+        raise ConfigurationError("xi must be positive")
+    cfg = SolverConfig(dual_ball=dual_ball or Unbounded())
+    eng = ApdbEngine(inst, cfg, z)
+    gap, cert, _ = eng.smoothed_gap(1, xi, subsolver_tol, x_warm, raw_point=z)
+    return gap, cert

@@ -1,0 +1,239 @@
+"""QCQP instances, iterates and the coupling-function operator contract.
+
+Mirrors ``pkg/src/rapdb/problem.py`` (``ProblemInstance`` :109-162, ``Iterate``
+:71-89, ``coupling_value``/``grad_x_coupling``/``grad_y_coupling`` :196-223) for
+the hot path's instance class: dense Q_i, box primal set, nonnegative-orthant
+cone, optional equality block ``Ax = b``.
+
+Storage differs from the reference by design: instead of
+a Python list of m+1 dense arrays / CSR matrices (``_as_operator``
+:31-40), the device holds ONE contiguous fp64 stack ``[m+1][n][ld]`` (ld = n
+rounded up to even so every row is a 16-byte-aligned bulk-copy source) and the
+solver streams it once per test evaluation.  ``DeviceData`` is that upload.
+
+The operator-contract functions evaluate on the GPU (one probe sweep + a few
+device vector ops); nothing here evaluates Q products on the host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from .errors import ConfigurationError, InputError
+from .geometry import Box, NonnegOrthant, cone_dim, set_dim
+
+
+@dataclass(frozen=True)
+class Iterate:
+    """Primal-dual point z = (x, v, lam)."""
+
+    x: np.ndarray
+    v: np.ndarray
+    lam: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "x", np.asarray(self.x, dtype=float))
+        object.__setattr__(self, "v", np.asarray(self.v, dtype=float))
+        object.__setattr__(self, "lam", np.asarray(self.lam, dtype=float))
+
+    @property
+    def y(self):
+        return np.concatenate([self.v, self.lam])
+
+    def dual_norm(self) -> float:
+        return float(np.sqrt(self.v @ self.v + self.lam @ self.lam))
+
+
+def _dense(M):
+    return M.toarray() if hasattr(M, "toarray") else np.asarray(M, dtype=float)
+
+
+@dataclass(frozen=True)
+class ProblemInstance:
+    """Immutable QCQP data; Q[0] is the objective, Q[1..m] the constraints.
+
+    ``Q`` may be a list of m+1 (n, n) arrays (reference style) or one
+    C-contiguous ``(m+1, n, n)`` float64 stack (no copy is made).  ``validate``
+    mirrors the reference's load-time checks (problem.py:142-162: symmetry to
+    1e-12, lambda_min >= -1e-10, rank(A) = p); pass ``validate=False`` for the
+    multi-GB benchmark instances whose generators guarantee both.
+    """
+
+    n: int
+    m: int
+    p: int
+    Q: object
+    q: object
+    r: np.ndarray
+    A: object
+    b: np.ndarray
+    primal_set: Box
+    cone: NonnegOrthant
+    mu: float = 0.0
+    dual_set: Optional[object] = None
+    name: str = ""
+    validate: bool = field(default=True, compare=False)
+
+    def __post_init__(self):
+        n, m, p = self.n, self.m, self.p
+        if n <= 0 or m < 0 or p < 0:
+            raise InputError("need n > 0, m >= 0, p >= 0")
+        Q = self.Q
+        if isinstance(Q, np.ndarray) and Q.ndim == 3:
+            if Q.shape != (m + 1, n, n):
+                raise InputError("need m+1 quadratic forms (objective plus m constraints)")
+            stack = np.ascontiguousarray(Q, dtype=np.float64)
+        else:
+            if len(Q) != m + 1:
+                raise InputError("need m+1 quadratic forms (objective plus m constraints)")
+            mats = [_dense(M) for M in Q]
+            for i, M in enumerate(mats):
+                if M.shape != (n, n):
+                    raise InputError(f"quadratic form {i} has wrong dimensions")
+            stack = np.ascontiguousarray(np.stack(mats), dtype=np.float64)
+        if isinstance(self.q, (list, tuple)):
+            qa = (np.stack([np.asarray(v, dtype=float) for v in self.q]) if len(self.q)
+                  else np.zeros((0, n)))
+        else:
+            qa = np.asarray(self.q, dtype=float)
+        if qa.shape != (m + 1, n):
+            raise InputError("need m+1 linear terms of length n")
+        r = np.asarray(self.r, dtype=float)
+        if r.shape != (m + 1,):
+            raise InputError("need m+1 constants")
+        A = np.asarray(_dense(self.A) if p else np.zeros((0, n)), dtype=float).reshape(p, n)
+        b = np.asarray(self.b, dtype=float).reshape(p)
+        object.__setattr__(self, "Q", stack)
+        object.__setattr__(self, "q", np.ascontiguousarray(qa))
+        object.__setattr__(self, "r", r)
+        object.__setattr__(self, "A", np.ascontiguousarray(A))
+        object.__setattr__(self, "b", b)
+        if set_dim(self.primal_set) != n:
+            raise InputError("primal set dimension mismatch")
+        if cone_dim(self.cone) != m:
+            raise InputError("cone dimension mismatch")
+        if self.mu < 0:
+            raise InputError("strong convexity modulus must be nonnegative")
+        if self.validate:
+            for i in range(m + 1):
+                D = stack[i]
+                if np.max(np.abs(D - D.T)) > 1e-12 * max(1.0, np.max(np.abs(D))):
+                    raise InputError(f"Q[{i}] is not symmetric")
+                lam_min = float(np.linalg.eigvalsh(D)[0])
+                if lam_min < -1e-10:
+                    raise InputError(f"Q[{i}] has negative eigenvalue {lam_min:.3e}")
+            if p > 0 and np.linalg.matrix_rank(A) < p:
+                raise InputError("equality matrix A is not full row rank")
+            if self.mu > 0:
+                lam0 = float(np.linalg.eigvalsh(stack[0])[0])
+                if self.mu > lam0 + 1e-10:
+                    raise InputError(f"declared mu={self.mu} exceeds lambda_min(Q0)={lam0:.3e}")
+        object.__setattr__(self, "_dev", {})
+
+    @classmethod
+    def from_arrays(cls, arr, validate=True):
+        """From ``instances.QcqpArrays``."""
+        return cls(n=arr.n, m=arr.m, p=arr.p, Q=arr.Q, q=arr.q, r=arr.r, A=arr.A, b=arr.b,
+                   primal_set=Box(arr.lower, arr.upper), cone=NonnegOrthant(arr.m), mu=arr.mu,
+                   name=arr.name, validate=validate)
+
+    def check_device_support(self):
+        if self.dual_set is not None:
+            raise ConfigurationError("minimax dual_set instances are not built on the device path")
+        if not isinstance(self.primal_set, Box):
+            raise ConfigurationError("the device path supports Box primal sets")
+        if not isinstance(self.cone, NonnegOrthant):
+            raise ConfigurationError("the device path supports the nonnegative orthant cone")
+
+    def device_data(self, device=None, pinned_host=None):
+        """Upload (cached per device).  ``pinned_host``: optional pinned torch copy
+        of the Q stack to copy from (benchmark e2e path)."""
+        import torch
+        dev = torch.device("cuda", 0) if device is None else torch.device(device)
+        key = str(dev)
+        cache = self._dev
+        if key not in cache:
+            cache[key] = DeviceData.upload(self, dev, pinned_host)
+        return cache[key]
+
+    def drop_device_data(self):
+        self._dev.clear()
+
+    # -- evaluations (problem.py:166-186) on the device --------------------
+    def _evaluator(self):
+        from .engine import _Evaluator
+        ev = self._dev.get("_eval")
+        if ev is None:
+            ev = _Evaluator(self)
+            self._dev["_eval"] = ev
+        return ev
+
+    def f_value(self, x) -> float:
+        return float(self._evaluator().sweep(x)[1][0])
+
+    def g_value(self, x) -> np.ndarray:
+        if self.m == 0:
+            return np.zeros(0)
+        return self._evaluator().sweep(x)[1][1:].cpu().numpy()
+
+    def eq_residual(self, x) -> np.ndarray:
+        if self.p == 0:
+            return np.zeros(0)
+        return self._evaluator().eq(x).cpu().numpy()
+
+    def project_dual_cone(self, lam):
+        return np.maximum(np.asarray(lam, dtype=float), 0.0)
+
+
+class DeviceData:
+    """The instance resident in HBM: Q stack [m+1][n][ld] + vectors (fp64)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    @classmethod
+    def upload(cls, inst: ProblemInstance, device, pinned_host=None):
+        import torch
+        n, m, p = inst.n, inst.m, inst.p
+        ld = n + (n & 1)
+        zero = np.array([not np.any(inst.Q[i]) for i in range(m + 1)], dtype=np.uint8)
+        src = pinned_host if pinned_host is not None else torch.from_numpy(inst.Q)
+        if ld == n:
+            Qd = src.to(device, non_blocking=pinned_host is not None)
+        else:
+            Qd = torch.zeros((m + 1, n, ld), dtype=torch.float64, device=device)
+            Qd[:, :, :n].copy_(src, non_blocking=pinned_host is not None)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+        lo = inst.primal_set.lower
+        hi = inst.primal_set.upper
+        return cls(n=n, m=m, p=p, ld=ld, Q=Qd, q=t(inst.q), r=t(inst.r),
+                   A=t(inst.A) if p else None, b=t(inst.b) if p else None,
+                   lower=t(lo), upper=t(hi), mu=float(inst.mu), zero_flags=zero, device=device)
+
+
+def _check_point(inst: ProblemInstance, z: Iterate):
+    if z.x.shape != (inst.n,) or z.v.shape != (inst.p,) or z.lam.shape != (inst.m,):
+        raise InputError(
+            f"iterate dims {(z.x.shape, z.v.shape, z.lam.shape)} do not match "
+            f"instance (n={inst.n}, p={inst.p}, m={inst.m})")
+
+
+def coupling_value(inst: ProblemInstance, z: Iterate) -> float:
+    """Phi(x, y) = f(x) + v'(Ax - b) + lam'g(x) (problem.py:196-204), on device."""
+    _check_point(inst, z)
+    return inst._evaluator().coupling(z)
+
+
+def grad_x_coupling(inst: ProblemInstance, z: Iterate) -> np.ndarray:
+    """(Q0 + sum lam_i Q_i) x + q0 + sum lam_i q_i + A'v (problem.py:207-217), on device."""
+    _check_point(inst, z)
+    return inst._evaluator().grad_x(z)
+
+
+def grad_y_coupling(inst: ProblemInstance, z: Iterate):
+    """(Ax - b, g(x)) (problem.py:220-223), on device."""
+    _check_point(inst, z)
+    return inst.eq_residual(z.x), inst.g_value(z.x)

@@ -1,0 +1,258 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+traces and the CPU oracle.
+
+Bars (BASELINE.json north_star): accepted step sizes and restart points
+identical over the first 200 iterations; iterates within 1e-9 relative error
+over those iterations; final residuals / objective within 1e-6 relative;
+iteration counts within 2% (exact where the reference's own perturbation band
+is zero, SURVEY.md section 7 hard part 4).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import ANALYTIC_NAMES, analytic_arrays, load_golden
+import paper_2605_29291_b200 as R
+from paper_2605_29291_b200 import instances
+from paper_2605_29291_b200.geometry import Box, JointBall, NonnegOrthant, SplitBall
+
+pytestmark = pytest.mark.gpu
+
+TAU = slice(1, 7)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    den = max(np.linalg.norm(b), 1e-300)
+    return float(np.linalg.norm(a - b) / den) if b.size else 0.0
+
+
+def inst_from(Q, q, r, lower, upper, A=None, b=None, mu=0.0):
+    Q = np.asarray(Q, float)
+    n = Q.shape[1]
+    m = Q.shape[0] - 1
+    A = np.zeros((0, n)) if A is None else np.asarray(A, float).reshape(-1, n)
+    b = np.zeros(A.shape[0]) if b is None else np.asarray(b, float)
+    return R.ProblemInstance(n=n, m=m, p=A.shape[0], Q=Q, q=np.asarray(q, float), r=r, A=A, b=b,
+                             primal_set=Box(lower, upper), cone=NonnegOrthant(m), mu=mu)
+
+
+def trace_arr(trace):
+    nan = np.nan
+    return np.array([[t.iter, t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total,
+                      nan if t.kkt is None else t.kkt, nan if t.infeas is None else t.infeas,
+                      nan if t.gap_xi is None else t.gap_xi, t.restart_flag] for t in trace])
+
+
+def policy_of(kind, **kw):
+    if kind == "none":
+        return R.NoRestart()
+    if kind == "fixed":
+        return R.FixedRestart(**kw)
+    return R.AdaptiveRestart(**kw)
+
+
+def crit(eps):
+    return None if eps is None else R.TerminationCriteria(criterion="conic", eps_kkt=eps, eps_feas=eps)
+
+
+@pytest.fixture(scope="module")
+def small():
+    g = load_golden("small_qcqp")
+    return g, inst_from(g["Q"], g["q"], g["r"], g["lower"], g["upper"])
+
+
+def test_probe_sweep_c0_kat():
+    """One fused sweep: u_i = Q_i x and g(x) against the reference's numpy values."""
+    import torch
+    g = load_golden("c0")
+    arr = instances.config_instance("C0")
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    ev = inst._evaluator()
+    u, gv = ev.sweep(g["probe_x"])
+    u = u.cpu().numpy()
+    gv = gv.cpu().numpy()
+    for i in range(arr.m + 1):
+        assert rel(u[i], g["probe_u"][i]) <= 1e-13
+    assert abs(gv[0] - float(g["probe_f"])) <= 1e-12 * abs(float(g["probe_f"]))
+    np.testing.assert_allclose(gv[1:], g["probe_g"], rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("key,mode,nm,ball,budget", [
+    ("yx_mono", "yx", False, None, 200), ("yx_nm", "yx", True, None, 200),
+    ("xy_mono", "xy", False, None, 200), ("xy_nm", "xy", True, None, 200),
+    ("yx_nm_joint5", "yx", True, JointBall(5.0), 200),
+    ("yx_nm_split", "yx", True, SplitBall(1.0, 0.7), 150)])
+def test_engine_small_qcqp_200(small, key, mode, nm, ball, budget):
+    g, inst = small
+    cfg = R.SolverConfig(mode=mode, nonmonotone=nm, **({"dual_ball": ball} if ball else {}))
+    eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst, cfg.dual_ball))
+    snaps = list(g[f"{key}/snap_iters"])
+    done = 0
+    for k in (1, 2, 10, 50, 100, 150, 200):
+        if k > budget:
+            break
+        eng.run_block(k - done)
+        done = k
+        z = eng.last
+        idx = snaps.index(k)
+        assert rel(z.x, g[f"{key}/snap_x"][idx]) <= 1e-9, k
+        assert rel(z.lam, g[f"{key}/snap_lam"][idx]) <= 1e-9, k
+    tr = trace_arr(eng.trace)
+    np.testing.assert_array_equal(tr[:, TAU], g[f"{key}/trace"][:len(tr), TAU])
+
+
+def test_fixed_restart_average_small(small):
+    g, inst = small
+    key = "yx_nm_fixed40avg"
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True),
+                          R.FixedRestart(40, point="average"), budget=200)
+    tr = trace_arr(res.trace)
+    np.testing.assert_array_equal(tr[:, TAU], g[f"{key}/trace"][:, TAU])
+    assert [e.iteration for e in res.restart_log] == list(g[f"{key}/restart_iters"])
+    assert rel(res.solution.x, g[f"{key}/final_x"]) <= 1e-9
+    assert rel(res.average.x, g[f"{key}/avg_x"]) <= 1e-9
+
+
+def test_fixed_restart_recorded_points(small):
+    g, inst = small
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True),
+                          R.FixedRestart(40, point="average"), budget=200, record_restart_points=True)
+    tr = trace_arr(res.trace)
+    np.testing.assert_array_equal(tr[:, TAU], g["yx_nm_fixed40avg/trace"][:, TAU])
+    lo, hi = inst.primal_set.lower, inst.primal_set.upper
+    assert res.restart_log
+    for e in res.restart_log:
+        assert np.all(e.point.x >= lo - 1e-12) and np.all(e.point.x <= hi + 1e-12)
+
+
+@pytest.mark.parametrize("name", ANALYTIC_NAMES)
+@pytest.mark.parametrize("key", ["nm_fixed500", "mono_fixed5", "xy_nm"])
+def test_analytic_suite(name, key):
+    g = load_golden("analytic")
+    a = analytic_arrays(g, name)
+    inst = inst_from(a["Q"], a["q"], a["r"], a["lower"], a["upper"], a["A"], a["b"], a["mu"])
+    spec = {"nm_fixed500": ("yx", True, policy_of("fixed", period=500), 5000, 1e-7),
+            "mono_fixed5": ("yx", False, policy_of("fixed", period=5), 23, None),
+            "xy_nm": ("xy", True, policy_of("none"), 300, None)}[key]
+    res = R.run_restarted(inst, R.SolverConfig(mode=spec[0], nonmonotone=spec[1]), spec[2],
+                          budget=spec[3], criteria=crit(spec[4]))
+    pre = f"{name}/{key}/"
+    tr_g = g[pre + "trace"]
+    tr = trace_arr(res.trace)
+    k = min(200, len(tr_g))
+    np.testing.assert_array_equal(tr[:k, TAU], tr_g[:k, TAU])
+    assert res.iterations == int(g[pre + "iterations"])
+    np.testing.assert_allclose(res.solution.x, g[pre + "final_x"], rtol=1e-6, atol=1e-9)
+    met = g[pre + "metrics"]
+    assert abs(res.metrics.kkt_residual - met[0]) <= 1e-6 * max(abs(met[0]), 1e-6)
+    if key == "nm_fixed500":
+        assert np.linalg.norm(res.solution.x - g[f"{name}/x_star"]) <= 1e-6
+
+
+@pytest.mark.parametrize("key,nm,policy,budget", [
+    ("mono_none", False, ("none", {}), 50000),
+    ("nm_fixed500", True, ("fixed", {"period": 500}), 50000)])
+def test_c0_full_runs(key, nm, policy, budget):
+    g = load_golden("c0")
+    arr = instances.config_instance("C0")
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=nm), policy_of(policy[0], **policy[1]),
+                          budget=budget, criteria=crit(1e-6))
+    tr = trace_arr(res.trace)
+    tr_g = g[f"{key}/trace"]
+    np.testing.assert_array_equal(tr[:200, TAU], tr_g[:200, TAU])
+    it_ref = int(g[f"{key}/iterations"])
+    assert abs(res.iterations - it_ref) <= 0.02 * it_ref
+    assert res.converged
+    met = g[f"{key}/metrics"]
+    assert abs(res.metrics.f_value - met[5]) <= 1e-6 * abs(met[5])
+    assert res.metrics.kkt_residual <= 1e-6 and res.metrics.infeas <= 1e-6
+    assert [e.iteration for e in res.restart_log] == list(g[f"{key}/restart_iters"])
+
+
+def test_c0_xy_200():
+    g = load_golden("c0")
+    arr = instances.config_instance("C0")
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    _, last, trace, _ = R.run(inst, R.SolverConfig(mode="xy", nonmonotone=True), R.initial_iterate(inst), 200)
+    np.testing.assert_array_equal(trace_arr(trace)[:, TAU], g["xy_nm_none/trace"][:, TAU])
+    assert rel(last.x, g["xy_nm_none/final_x"]) <= 1e-9
+    assert rel(last.lam, g["xy_nm_none/final_lam"]) <= 1e-9
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key,nm", [("mono", False), ("nm", True)])
+def test_c1_first_200(key, nm):
+    g = load_golden("c1_200")
+    arr = instances.config_instance("C1")
+    np.testing.assert_allclose([float(np.sum(arr.Q[i])) for i in range(0, arr.m + 1, 20)],
+                               g["Q_checksum"][::20], rtol=1e-12)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.initial_iterate(inst))
+    snaps = list(g[f"{key}/snap_iters"])
+    done = 0
+    for k in snaps:
+        eng.run_block(int(k) - done)
+        done = int(k)
+        z = eng.last
+        idx = snaps.index(k)
+        assert rel(z.x, g[f"{key}/snap_x"][idx]) <= 1e-9, k
+        assert rel(z.lam, g[f"{key}/snap_lam"][idx]) <= 1e-9, k
+    np.testing.assert_array_equal(trace_arr(eng.trace)[:, TAU], g[f"{key}/trace"][:, TAU])
+
+
+def test_kml_small_epigraph():
+    g = load_golden("kml_small")
+    arr = instances.kml_epigraph(N=120, d=10)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(500),
+                          budget=3000, criteria=crit(1e-6))
+    tr = trace_arr(res.trace)
+    np.testing.assert_array_equal(tr[:200, TAU], g["nm_fixed500/trace"][:200, TAU])
+    assert res.iterations == int(g["nm_fixed500/iterations"])
+
+
+def test_nonconvergence_state(small):
+    _, inst = small
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", tau_bar=1e6, max_backtracks=0), R.initial_iterate(inst))
+    with pytest.raises(R.NonConvergence) as exc:
+        eng.step()
+    assert set(exc.value.state) == {"tau", "gamma", "iter"}
+
+
+def test_degenerate_no_constraints():
+    inst = inst_from(np.eye(2)[None], np.array([[-1.0, 1.0]]), np.zeros(1), -4 * np.ones(2), 4 * np.ones(2))
+    for mode in ("xy", "yx"):
+        _, last, _, _ = R.run(inst, R.SolverConfig(mode=mode), R.initial_iterate(inst), 200)
+        np.testing.assert_allclose(last.x, [1.0, -1.0], atol=1e-6)
+
+
+def test_determinism_bitwise(small):
+    _, inst = small
+    outs = []
+    for _ in range(2):
+        res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(30),
+                              budget=120)
+        outs.append((trace_arr(res.trace), res.solution.x))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+def test_oracle_live_random(small):
+    """CUDA path vs the live CPU oracle on fresh seeded instances (incl. odd n, p > 0)."""
+    from oracle import rapdb_oracle as O
+    for seed, (n, m, r) in enumerate([(33, 4, 5), (64, 7, 8), (17, 1, 3)]):
+        arr = instances.dense_qcqp(n, m, r, seed=seed + 11)
+        inst = R.ProblemInstance.from_arrays(arr, validate=False)
+        P = O.Problem.from_arrays(arr)
+        for nm in (False, True):
+            ref = O.run_restarted(P, O.Options(mode="yx", nonmonotone=nm), O.Policy("fixed", period=50),
+                                  budget=300, criteria=dict(criterion="conic", eps_kkt=1e-8, eps_feas=1e-8))
+            res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.FixedRestart(50),
+                                  budget=300, criteria=crit(1e-8))
+            a = trace_arr(res.trace)[:200, TAU]
+            b = np.array([[t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total]
+                          for t in ref.trace])[:200]
+            np.testing.assert_array_equal(a, b)
+            assert rel(res.solution.x, ref.x) <= 1e-8
