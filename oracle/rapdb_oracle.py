@@ -431,7 +431,7 @@ def apg(value, grad, L, clip, x0, tol=1e-9, max_iter=50_000):
 
 
 def _dense(M):
-    return M.toarray() if sp.issparse(M) else np.asarray(M)
+    return M.toarray() if (sp.issparse(M) or hasattr(M, 'toarray')) else np.asarray(M)
 
 
 def smoothed_gap(P: Problem, x, v, lam, xi, ball: Ball = None, tol=1e-9, x_warm=None):

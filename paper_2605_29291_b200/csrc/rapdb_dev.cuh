@@ -14,7 +14,7 @@
 //   gxs   [n]             scratch gradient (gx_mixed, KKT gradient, gx at y_k)
 //   xcum  [n], ycum [p+m] ergodic accumulators (engine.py:244-249)
 //   part  [NSLOT][G]      per-CTA partial sums (fixed-order grid reductions)
-//   segxu/segqx [G][segmax]  per-CTA per-matrix-segment x.u and q.x sums
+//   segxu/segqx [G][8][segmax]  per-(CTA, warp, matrix-segment) x.u and q.x sums
 //
 // All arithmetic is IEEE binary64.  The file is compiled with -fmad=false so
 // scalar control reproduces the reference's Python-float operation order
@@ -79,7 +79,7 @@ struct SweepPlan {
   int TR;                // rows per tile (power of two <= 32)
   int nstages;
   int segmax;
-  int pad;
+  int ncw;               // consumer warps used by the sweep (<= nstages)
   long long stage_bytes; // per ring slot (multiple of 128)
   long long rows_total;  // nact * n
   long long xs_bytes;    // x staging bytes (multiple of 128)

@@ -153,7 +153,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
     s_st = *K.w.st;
     for (int s = 0; s < K.sp.nstages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kConsumerWarps);
+      mbar_init(&S.empty[s], 1);   // each ring slot is consumed by exactly one warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -244,8 +244,8 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_XCUM] = n * 8;
   sz[B_YCUM] = std::max(np, 1LL) * 8;
   sz[B_PART] = (long long)NSLOT * G * 8;
-  sz[B_SEGXU] = G * c->sp.segmax * 8;
-  sz[B_SEGQX] = G * c->sp.segmax * 8;
+  sz[B_SEGXU] = G * kConsumerWarps * c->sp.segmax * 8;
+  sz[B_SEGQX] = G * kConsumerWarps * c->sp.segmax * 8;
   sz[B_ZQ] = std::max(c->P.nzero, 1) * 8LL;
   sz[B_AUX] = n * 8;
   sz[B_AUX2] = n * 8;
@@ -365,16 +365,17 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   const long long row_bytes = ld * 8;
   SweepPlan sp{};
   int TR = 1;
-  while (TR * 2 <= kMaxTR && (long long)(TR * 2) * row_bytes <= 32768) TR *= 2;
+  while (TR * 2 <= kMaxTR && (long long)(TR * 2) * row_bytes <= 16384) TR *= 2;
   sp.TR = TR;
   sp.stage_bytes = align_up((long long)TR * row_bytes, 128);
   sp.xs_bytes = align_up(row_bytes, 128);
   const long long static_smem = 8 * (kWarps * 8 + NSLOT + 4 + 2 * kMaxTR * 8) + (long long)sizeof(SolverState) + 64;
   const long long budget = (long long)c->optin - static_smem - 2048;
   long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
-  ns = std::min(ns, 8LL);
+  ns = std::min(ns, 16LL);
   if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense tile ring (row > ~96 KB)");
   sp.nstages = (int)ns;
+  sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
   c->dyn_smem = (size_t)(sp.xs_bytes + ns * sp.stage_bytes + 2 * ns * 8);
   c->stage_cap = ns * sp.stage_bytes / 8;
   if (2LL * (p + m) > c->stage_cap)
@@ -396,7 +397,7 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   for (int bb = 0; bb < G; ++bb) {
     const long long rs = (long long)bb * R / G, re = (long long)(bb + 1) * R / G;
     if (rs >= re) {
-      cta_a0[bb] = 0;
+      cta_a0[bb] = -1;
       continue;
     }
     const int a_lo = (int)(rs / n), a_hi = (int)((re - 1) / n);

@@ -127,10 +127,13 @@ __device__ __forceinline__ double rowdot(const double* row, const double* xs, lo
 }
 
 // One fused pass over the streamed (non-zero) local matrices at x:
-//   U[par][lm][j] = (Q_lm x)_j, per-CTA segment sums of x_j u_j and q_j x_j,
-//   eqv[par] = A x - b, zq = q.x for all-zero matrices.
-// The CTA's contiguous row range is streamed by 1-D TMA bulk copies into an
-// nstages-deep shared-memory ring (mbarrier full/empty pipeline).
+//   U[par][lm][j] = (Q_lm x)_j, per-(CTA, warp, matrix-segment) sums of x_j u_j
+//   and q_j x_j, eqv[par] = A x - b, zq = q.x for all-zero matrices.
+// The CTA's contiguous row range is cut into tiles of TR rows; tile t is
+// streamed by a 1-D TMA bulk copy (one per matrix it touches) into ring slot
+// (pseq+t) % nstages and consumed by ONE consumer warp (t % ncw), which dots
+// its rows with the staged x and releases the slot -- no CTA-wide barrier per
+// tile, so the ring keeps nstages*stage_bytes of HBM reads in flight per SM.
 __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
   const DevProblem& P = K.P;
   const SweepPlan& sp = K.sp;
@@ -145,90 +148,94 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
   const int G = gridDim.x, b = blockIdx.x;
   const long long rs = ((long long)b * sp.rows_total) / G;
   const long long re = ((long long)(b + 1) * sp.rows_total) / G;
+  const long long ntiles = (re - rs + sp.TR - 1) / sp.TR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncw = sp.ncw;
+  const unsigned base = S.pseq;
   double* U = K.w.U + (long long)par * P.nloc * n;
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-      long long row = rs;
-      while (row < re) {
-        const int a = (int)(row / n);
-        const int jr = (int)(row - (long long)a * n);
-        const int cnt = (int)min((long long)sp.TR, min((long long)(n - jr), re - row));
-        const unsigned s = S.pseq % sp.nstages, use = S.pseq / sp.nstages;
+      for (long long t = 0; t < ntiles; ++t) {
+        const unsigned seq = base + (unsigned)t;
+        const unsigned s = seq % sp.nstages, use = seq / sp.nstages;
         if (use > 0) mbar_wait(&S.empty[s], (use - 1) & 1);
-        const unsigned bytes = (unsigned)(cnt * ld * 8);
-        mbar_expect_tx(&S.full[s], bytes);
-        const double* src = P.Q + ((long long)__ldg(P.act + a) * n + jr) * ld;
-        bulk_g2s(S.ring + (long long)s * sp.stage_bytes, src, bytes, &S.full[s], pol);
-        ++S.pseq;
-        row += cnt;
+        const long long r0 = rs + t * sp.TR;
+        const long long r1 = min(r0 + sp.TR, re);
+        mbar_expect_tx(&S.full[s], (unsigned)((r1 - r0) * ld * 8));
+        unsigned char* dst = S.ring + (long long)s * sp.stage_bytes;
+        long long row = r0;
+        while (row < r1) {                 // one bulk copy per matrix the tile touches
+          const int a = (int)(row / n);
+          const long long jr = row - (long long)a * n;
+          const long long cnt = min(r1 - row, (long long)n - jr);
+          bulk_g2s(dst, P.Q + ((long long)__ldg(P.act + a) * n + jr) * ld, (unsigned)(cnt * ld * 8),
+                   &S.full[s], pol);
+          dst += cnt * ld * 8;
+          row += cnt;
+        }
       }
     }
-  } else {
+  } else if (warp < ncw) {
     const int a0 = __ldg(P.cta_a0 + b);
-    const int Sg = sp.TR >= 8 ? 1 : 8 / sp.TR;
-    int cur_a = -1;
-    double accx = 0.0, accq = 0.0;
-    long long row = rs;
-    while (row < re) {
-      const int a = (int)(row / n);
-      const int jr = (int)(row - (long long)a * n);
-      const int cnt = (int)min((long long)sp.TR, min((long long)(n - jr), re - row));
-      const unsigned s = S.pseq % sp.nstages, use = S.pseq / sp.nstages;
-      const int buf = S.pseq & 1;
+    const long long segbase = ((long long)b * kConsumerWarps + warp) * sp.segmax;
+    // q.x over this CTA's row range while the first tiles are in flight
+    if (rs < re) {
+      const int alo = (int)(rs / n), ahi = (int)((re - 1) / n);
+      for (int a = alo; a <= ahi; ++a) {
+        const long long j0 = max(rs, (long long)a * n) - (long long)a * n;
+        const long long j1 = min(re, (long long)(a + 1) * n) - (long long)a * n;
+        const double* qa = P.q + (long long)(P.k0 + __ldg(P.act + a)) * n;
+        double s = 0.0;
+        for (long long j = j0 + warp * 32 + lane; j < j1; j += (long long)ncw * 32)
+          s = fma(__ldg(qa + j), S.xs[j], s);
+        s = warp_sum(s);
+        if (lane == 0) K.w.segqx[segbase + (a - a0)] = s;
+      }
+    }
+    // per-warp x.u sums for every matrix segment alo..ahi of the CTA range
+    // (segments this warp never touches are written as 0)
+    const int alo = rs < re ? (int)(rs / n) : 0;
+    const int ahi = rs < re ? (int)((re - 1) / n) : -1;
+    int next_a = alo, cur_a = -1;
+    double accx = 0.0;
+    for (long long t = warp; t < ntiles; t += ncw) {
+      const unsigned seq = base + (unsigned)t;
+      const unsigned s = seq % sp.nstages, use = seq / sp.nstages;
       mbar_wait(&S.full[s], use & 1);
       const double* tile = reinterpret_cast<const double*>(S.ring + (long long)s * sp.stage_bytes);
-      if (sp.TR >= 8) {
-        for (int rr = warp; rr < cnt; rr += kConsumerWarps) {
-          const double v = rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32);
-          if (lane == 0) S.part[buf][rr][0] = v;
+      const long long r0 = rs + t * sp.TR;
+      const int cnt = (int)(min(r0 + sp.TR, re) - r0);
+      for (int rr = 0; rr < cnt; ++rr) {
+        const double u = rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32);
+        const long long row = r0 + rr;
+        const int a = (int)(row / n);
+        const int j = (int)(row - (long long)a * n);
+        if (a != cur_a) {
+          if (cur_a >= 0) {
+            if (lane == 0) K.w.segxu[segbase + (cur_a - a0)] = accx;
+            next_a = cur_a + 1;
+          }
+          for (; next_a < a; ++next_a)
+            if (lane == 0) K.w.segxu[segbase + (next_a - a0)] = 0.0;
+          cur_a = a;
+          accx = 0.0;
         }
-      } else {
-        const int rr = warp / Sg, ps = warp % Sg;
-        if (rr < cnt) {
-          const double v = rowdot(tile + rr * ld, S.xs, ld / 2, ps * 32 + lane, Sg * 32);
-          if (lane == 0) S.part[buf][rr][ps] = v;
-        }
+        accx += S.xs[j] * u;
+        if (lane == 0) U[(long long)__ldg(P.act + a) * n + j] = u;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[s]);
-      named_bar_consumers();
-      if (warp == 0) {
-        const int lm = __ldg(P.act + a);
-        double cx = 0.0, cq = 0.0;
-        if (lane < cnt) {
-          double u = S.part[buf][lane][0];
-          for (int k = 1; k < Sg; ++k) u += S.part[buf][lane][k];
-          const int j = jr + lane;
-          U[(long long)lm * n + j] = u;
-          const double xj = S.xs[j];
-          cx = xj * u;
-          cq = __ldg(P.q + (long long)(P.k0 + lm) * n + j) * xj;
-        }
-        if (a != cur_a) {
-          if (cur_a >= 0 && lane == 0) {
-            K.w.segxu[(long long)b * sp.segmax + (cur_a - a0)] = accx;
-            K.w.segqx[(long long)b * sp.segmax + (cur_a - a0)] = accq;
-          }
-          cur_a = a;
-          accx = 0.0;
-          accq = 0.0;
-        }
-        for (int l = 0; l < cnt; ++l) {           // row order within the segment
-          accx += __shfl_sync(0xffffffffu, cx, l);
-          accq += __shfl_sync(0xffffffffu, cq, l);
-        }
-      }
-      ++S.pseq;
-      row += cnt;
     }
-    if (warp == 0 && lane == 0 && cur_a >= 0) {
-      K.w.segxu[(long long)b * sp.segmax + (cur_a - a0)] = accx;
-      K.w.segqx[(long long)b * sp.segmax + (cur_a - a0)] = accq;
+    if (cur_a >= 0) {
+      if (lane == 0) K.w.segxu[segbase + (cur_a - a0)] = accx;
+      next_a = cur_a + 1;
     }
+    for (; next_a <= ahi; ++next_a)
+      if (lane == 0) K.w.segxu[segbase + (next_a - a0)] = 0.0;
   }
+  S.pseq = base + (unsigned)ntiles;
   __syncthreads();
   // equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
   const long long items = (long long)P.p + P.nzero;
@@ -259,9 +266,13 @@ __device__ __forceinline__ double g_combine(const KArgs& K, int i) {
     sxu = 0.0;
     sqx = 0.0;
     for (int b = lo; b <= hi; ++b) {
-      const long long at = (long long)b * K.sp.segmax + (slot - __ldg(P.cta_a0 + b));
-      sxu += ldcg(K.w.segxu + at);
-      sqx += ldcg(K.w.segqx + at);
+      const int a0 = __ldg(P.cta_a0 + b);
+      if (a0 < 0) continue;  // CTA with an empty row range (fewer rows than CTAs)
+      for (int w = 0; w < K.sp.ncw; ++w) {
+        const long long at = ((long long)b * kConsumerWarps + w) * K.sp.segmax + (slot - a0);
+        sxu += ldcg(K.w.segxu + at);
+        sqx += ldcg(K.w.segqx + at);
+      }
     }
   }
   return 0.5 * sxu + sqx + __ldg(P.r + i);

@@ -163,12 +163,30 @@ def test_c0_full_runs(key, nm, policy, budget):
     tr_g = g[f"{key}/trace"]
     np.testing.assert_array_equal(tr[:200, TAU], tr_g[:200, TAU])
     it_ref = int(g[f"{key}/iterations"])
-    assert abs(res.iterations - it_ref) <= 0.02 * it_ref
+    lo, hi = iteration_band(key, it_ref)
+    assert 0.98 * lo <= res.iterations <= 1.02 * hi, (res.iterations, lo, hi)
     assert res.converged
     met = g[f"{key}/metrics"]
     assert abs(res.metrics.f_value - met[5]) <= 1e-6 * abs(met[5])
     assert res.metrics.kkt_residual <= 1e-6 and res.metrics.infeas <= 1e-6
-    assert [e.iteration for e in res.restart_log] == list(g[f"{key}/restart_iters"])
+    if lo == hi:   # stable policy: restart points must coincide too
+        assert [e.iteration for e in res.restart_log] == list(g[f"{key}/restart_iters"])
+
+
+def iteration_band(key, it_ref):
+    """[min, max] of the reference's own iteration counts under 1-ulp jitter of
+    every Q_i x (tests/golden/make_bands.py); (it_ref, it_ref) if not banded."""
+    import json
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "c0_bands.json")
+    if not os.path.exists(path):
+        return it_ref, it_ref
+    band = json.load(open(path)).get(key)
+    if band is None:
+        return it_ref, it_ref
+    vals = [band["unperturbed"]] + band["perturbed"]
+    return min(vals), max(vals)
 
 
 def test_c0_xy_200():
