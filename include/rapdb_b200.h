@@ -76,7 +76,12 @@ typedef struct {
   int has_metrics;
   double sweep_ns;         /* device time spent in Q sweeps (globaltimer)         */
   long long sweeps;        /* number of Q sweeps                                  */
+  double kernel_ms;        /* CUDA-event time of this call's solver launch        */
+  long long sweep_bytes;   /* algorithmic bytes of one sweep (streamed Q rows)    */
 } rapdb_run_result;
+
+/* process-wide number of kernel launches issued by this library */
+long long rapdb_launch_count(void);
 
 /* version of the ABI (bumped on incompatible change) */
 int rapdb_abi_version(void);

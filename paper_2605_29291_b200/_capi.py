@@ -37,14 +37,20 @@ class RunResult(C.Structure):
                 ("sigma_prev", C.c_double), ("T", C.c_double),
                 ("fail_tau", C.c_double), ("fail_gamma", C.c_double), ("fail_iter", C.c_longlong),
                 ("metrics", C.c_double * 8), ("has_metrics", C.c_int),
-                ("sweep_ns", C.c_double), ("sweeps", C.c_longlong)]
+                ("sweep_ns", C.c_double), ("sweeps", C.c_longlong),
+                ("kernel_ms", C.c_double), ("sweep_bytes", C.c_longlong)]
 
 
 _lib = None
 EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_error", "rapdb_set_stream",
            "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
-           "rapdb_smoothed_gap"]
+           "rapdb_smoothed_gap", "rapdb_launch_count"]
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the native library in this process."""
+    return int(load().rapdb_launch_count())
 
 
 def load(path: str = LIB_PATH):
@@ -74,6 +80,7 @@ def load(path: str = LIB_PATH):
     lib.rapdb_get_iterate.argtypes = [P, I, P, P, P]
     lib.rapdb_probe_sweep.argtypes = [P, P, P, P, I, C.POINTER(C.c_float)]
     lib.rapdb_smoothed_gap.argtypes = [P, I, D, D, P, P, C.POINTER(D)]
+    lib.rapdb_launch_count.restype = LL
     _lib = lib
     return lib
 

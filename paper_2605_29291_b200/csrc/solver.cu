@@ -262,6 +262,8 @@ Layout layout_of(const rapdb_ctx* c) {
   return L;
 }
 
+long long g_launches = 0;
+
 int launch(rapdb_ctx* c, RunCfg rc) {
   if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
   KArgs K;
@@ -275,6 +277,7 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   CK(cudaLaunchCooperativeKernel((const void*)rapdb_solver_kernel, dim3(c->G), dim3(kThreads), args,
                                  c->dyn_smem, c->stream));
   CK(cudaGetLastError());
+  ++g_launches;
   return RAPDB_OK;
 }
 
@@ -292,6 +295,8 @@ int read_state(rapdb_ctx* c, SolverState* st) {
 extern "C" {
 
 int rapdb_abi_version(void) { return 1; }
+
+long long rapdb_launch_count(void) { return g_launches; }
 
 int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
   if (!out) return RAPDB_EINPUT;
@@ -517,12 +522,23 @@ int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_re
   c->w.trace = trace;
   SolverState before;
   int r = read_state(c, &before);
-  if (!r) r = launch(c, rc);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (!r) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, c->stream));
+    r = launch(c, rc);
+    if (!r) CK(cudaEventRecord(e1, c->stream));
+  }
   c->w = saved;
   if (r) return r;
   SolverState st;
   r = read_state(c, &st);
   if (r) return r;
+  float kms = 0.0f;
+  cudaEventElapsedTime(&kms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   std::memset(out, 0, sizeof(*out));
   out->status = st.status;
   out->iters_done = st.iters - before.iters;
@@ -534,8 +550,10 @@ int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_re
   out->fail_tau = st.fail_tau; out->fail_gamma = st.fail_gamma; out->fail_iter = st.fail_iter;
   for (int i = 0; i < 8; ++i) out->metrics[i] = st.metrics[i];
   out->has_metrics = st.has_metrics;
-  out->sweep_ns = st.sweep_ns;
-  out->sweeps = st.sweeps;
+  out->sweep_ns = st.sweep_ns - before.sweep_ns;
+  out->sweeps = st.sweeps - before.sweeps;
+  out->kernel_ms = (double)kms;
+  out->sweep_bytes = c->sp.rows_total * (long long)c->P.n * 8;
   if (st.status == ST_ABORT) return fail(c, RAPDB_EDEVICE, "device watchdog fired");
   if (st.status == ST_NONCONV) {
     char buf[256];

@@ -156,11 +156,21 @@ class ProblemInstance:
         key = str(dev)
         cache = self._dev
         if key not in cache:
-            cache[key] = DeviceData.upload(self, dev, pinned_host)
+            src = pinned_host if pinned_host is not None else cache.get("_pinned")
+            cache[key] = DeviceData.upload(self, dev, src)
         return cache[key]
 
+    def pin_host(self):
+        """Keep a page-locked copy of the Q stack so uploads run at full PCIe rate."""
+        import torch
+        if "_pinned" not in self._dev:
+            self._dev["_pinned"] = torch.from_numpy(self.Q).pin_memory()
+        return self._dev["_pinned"]
+
     def drop_device_data(self):
-        self._dev.clear()
+        """Release the device copies (the pinned host copy is kept)."""
+        for k in [k for k in self._dev if k != "_pinned"]:
+            del self._dev[k]
 
     # -- evaluations (problem.py:166-186) on the device --------------------
     def _evaluator(self):

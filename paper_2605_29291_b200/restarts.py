@@ -114,7 +114,7 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
     status = "budget"
     metrics = None
     total = 0
-    sweep_ns, sweeps = 0.0, 0
+    stats = {"sweep_ns": 0.0, "sweeps": 0, "kernel_ms": 0.0, "run_launches": 0, "sweep_bytes": 0}
 
     while total < budget:
         a = _capi.RunArgs(max_iters=budget - total, budget=budget, stop_total=0,
@@ -136,7 +136,11 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
             nxt = _next_check(policy, total, inner, gap_ref)
             a.stop_total = nxt if nxt < budget else 0
         res, recs = engine.run_block_args(a)
-        sweep_ns, sweeps = res.sweep_ns, res.sweeps
+        stats["sweep_ns"] += res.sweep_ns
+        stats["sweeps"] += int(res.sweeps)
+        stats["kernel_ms"] += res.kernel_ms
+        stats["run_launches"] += 1
+        stats["sweep_bytes"] = int(res.sweep_bytes)
         for r in recs:                      # fixed restarts executed on device
             if r.restart_flag:
                 outer += 1
@@ -185,4 +189,4 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
     return RunResult(solution=engine.last, average=engine.average(), trace=engine.trace,
                      restart_log=restart_log, iterations=engine.iters, evals=engine.evals_total,
                      converged=converged, status=status, metrics=metrics,
-                     device_stats={"sweep_ns": sweep_ns, "sweeps": sweeps})
+                     device_stats=stats)
