@@ -80,6 +80,8 @@ struct SweepPlan {
   int nstages;
   int segmax;
   int ncw;               // consumer warps used by the sweep (<= nstages)
+  int cpr;               // column chunks per row (> 1: rows wider than a stage)
+  int chunk;             // doubles per chunk (== ld when cpr == 1)
   long long stage_bytes; // per ring slot (multiple of 128)
   long long rows_total;  // nact * n
   long long xs_bytes;    // x staging bytes (multiple of 128)
@@ -145,8 +147,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
   return ok != 0;
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  while (!mbar_try_wait(bar, parity)) {
+// spin on an mbarrier phase; after ~10 s raise the device abort flag and give
+// up (a protocol bug then surfaces as RAPDB_EDEVICE instead of a hung GPU)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, int* abort_flag) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = globaltimer();
+  for (unsigned spins = 1;; ++spins) {
+    if (mbar_try_wait(bar, parity)) return;
+    if ((spins & 1023u) == 0) {
+      if (*(volatile int*)abort_flag) return;
+      if (globaltimer() - t0 > 10000000000ull) {
+        atomicExch(abort_flag, 1);
+        return;
+      }
+    }
   }
 }
 

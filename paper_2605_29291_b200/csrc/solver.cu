@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -368,17 +369,40 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   }
   // sweep plan: rows per tile, ring depth, shared memory
   const long long row_bytes = ld * 8;
+  // ~16 KB bulk copies (whole rows up to 48 KB), 12-16-deep ring: measured at
+  // ~6.9 TB/s for the C1 sweep on B200 (tools/profile_sweep.py); env knobs
+  // RAPDB_TILE_BYTES / RAPDB_STAGES / RAPDB_ROW_TILE_MAX exist for tuning runs.
+  const char* env_tile = std::getenv("RAPDB_TILE_BYTES");
+  const char* env_st = std::getenv("RAPDB_STAGES");
+  const char* env_rt = std::getenv("RAPDB_ROW_TILE_MAX");
+  const long long tile_target = env_tile ? std::max(1024LL, std::atoll(env_tile)) : 16384;
+  const long long max_stages = env_st ? std::max(2LL, std::atoll(env_st)) : 16;
+  const long long row_tile_max = env_rt ? std::atoll(env_rt) : 49152;
   SweepPlan sp{};
-  int TR = 1;
-  while (TR * 2 <= kMaxTR && (long long)(TR * 2) * row_bytes <= 16384) TR *= 2;
-  sp.TR = TR;
-  sp.stage_bytes = align_up((long long)TR * row_bytes, 128);
+  if (row_bytes > tile_target && row_bytes <= row_tile_max) {   // one whole row per tile
+    sp.TR = 1;
+    sp.cpr = 1;
+    sp.chunk = (int)ld;
+    sp.stage_bytes = align_up(row_bytes, 128);
+  } else if (row_bytes <= tile_target) {
+    int TR = 1;
+    while (TR * 2 <= kMaxTR && (long long)(TR * 2) * row_bytes <= tile_target) TR *= 2;
+    sp.TR = TR;
+    sp.cpr = 1;
+    sp.chunk = (int)ld;
+    sp.stage_bytes = align_up((long long)TR * row_bytes, 128);
+  } else {
+    sp.TR = 1;
+    sp.chunk = (int)(tile_target / 16 * 2);          // even number of doubles
+    sp.cpr = (int)((ld + sp.chunk - 1) / sp.chunk);
+    sp.stage_bytes = align_up((long long)sp.chunk * 8, 128);
+  }
   sp.xs_bytes = align_up(row_bytes, 128);
   const long long static_smem = 8 * (kWarps * 8 + NSLOT + 4 + 2 * kMaxTR * 8) + (long long)sizeof(SolverState) + 64;
   const long long budget = (long long)c->optin - static_smem - 2048;
   long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
-  ns = std::min(ns, 16LL);
-  if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense tile ring (row > ~96 KB)");
+  ns = std::min(ns, max_stages);
+  if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense path (x does not fit in shared memory)");
   sp.nstages = (int)ns;
   sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
   c->dyn_smem = (size_t)(sp.xs_bytes + ns * sp.stage_bytes + 2 * ns * 8);

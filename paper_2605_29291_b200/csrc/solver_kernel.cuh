@@ -129,11 +129,13 @@ __device__ __forceinline__ double rowdot(const double* row, const double* xs, lo
 // One fused pass over the streamed (non-zero) local matrices at x:
 //   U[par][lm][j] = (Q_lm x)_j, per-(CTA, warp, matrix-segment) sums of x_j u_j
 //   and q_j x_j, eqv[par] = A x - b, zq = q.x for all-zero matrices.
-// The CTA's contiguous row range is cut into tiles of TR rows; tile t is
-// streamed by a 1-D TMA bulk copy (one per matrix it touches) into ring slot
-// (pseq+t) % nstages and consumed by ONE consumer warp (t % ncw), which dots
-// its rows with the staged x and releases the slot -- no CTA-wide barrier per
-// tile, so the ring keeps nstages*stage_bytes of HBM reads in flight per SM.
+// The CTA's contiguous row range is cut into ~8 KB tiles: TR whole rows when a
+// row fits (small n), else one column chunk of one row (cpr chunks per row).
+// Tile t is streamed by a 1-D TMA bulk copy into ring slot (pseq+t) % nstages
+// and consumed by ONE consumer warp -- the warp that owns its row unit -- which
+// dots it with the staged x and releases the slot.  There is no CTA-wide
+// barrier per tile, so the ring keeps nstages*stage_bytes of HBM reads in
+// flight per SM; chunk partials of a row are summed in chunk order.
 __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
   const DevProblem& P = K.P;
   const SweepPlan& sp = K.sp;
@@ -148,7 +150,9 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
   const int G = gridDim.x, b = blockIdx.x;
   const long long rs = ((long long)b * sp.rows_total) / G;
   const long long re = ((long long)(b + 1) * sp.rows_total) / G;
-  const long long ntiles = (re - rs + sp.TR - 1) / sp.TR;
+  const bool chunked = sp.cpr > 1;
+  const long long nunits = chunked ? (re - rs) : (re - rs + sp.TR - 1) / sp.TR;
+  const long long ntiles = chunked ? nunits * sp.cpr : nunits;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncw = sp.ncw;
   const unsigned base = S.pseq;
@@ -156,24 +160,72 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
+      // Single issuing thread: all tile addressing is incremental (no 64-bit
+      // divisions on the issue path -- they capped the issue rate at ~1 tile
+      // per 0.5 us).  Ring slot / phase advance as counters.
       const uint64_t pol = evict_first_policy();
-      for (long long t = 0; t < ntiles; ++t) {
-        const unsigned seq = base + (unsigned)t;
-        const unsigned s = seq % sp.nstages, use = seq / sp.nstages;
-        if (use > 0) mbar_wait(&S.empty[s], (use - 1) & 1);
-        const long long r0 = rs + t * sp.TR;
-        const long long r1 = min(r0 + sp.TR, re);
-        mbar_expect_tx(&S.full[s], (unsigned)((r1 - r0) * ld * 8));
+      const int ns = sp.nstages;
+      unsigned s = base % ns, use = base / ns;
+      auto next_slot = [&](unsigned bytes) -> unsigned char* {
+        if (use > 0) mbar_wait(&S.empty[s], (use - 1) & 1, K.w.abort_flag);
         unsigned char* dst = S.ring + (long long)s * sp.stage_bytes;
-        long long row = r0;
-        while (row < r1) {                 // one bulk copy per matrix the tile touches
-          const int a = (int)(row / n);
-          const long long jr = row - (long long)a * n;
-          const long long cnt = min(r1 - row, (long long)n - jr);
-          bulk_g2s(dst, P.Q + ((long long)__ldg(P.act + a) * n + jr) * ld, (unsigned)(cnt * ld * 8),
-                   &S.full[s], pol);
-          dst += cnt * ld * 8;
-          row += cnt;
+        mbar_expect_tx(&S.full[s], bytes);
+        return dst;
+      };
+      auto advance = [&]() { if (++s == (unsigned)ns) { s = 0; ++use; } };
+      if (rs < re) {
+        int a = (int)(rs / n);
+        long long jr = rs - (long long)a * n;
+        const double* qa = P.Q + (long long)__ldg(P.act + a) * n * ld;
+        if (chunked) {
+          // stream order: groups of ncw rows, chunk-major inside a group, so
+          // every consumer warp's consecutive tiles are exactly ncw apart (a
+          // wider gap than nstages would alias the slot's mbarrier parity)
+          for (long long g0 = 0; g0 < nunits; g0 += ncw) {
+            const int width = (int)min((long long)ncw, nunits - g0);
+            for (int c = 0; c < sp.cpr; ++c) {
+              const long long c0 = (long long)c * sp.chunk;
+              const unsigned bytes = (unsigned)(min((long long)sp.chunk, ld - c0) * 8);
+              int ar = a;
+              long long jj = jr;
+              const double* qr = qa;
+              for (int rr = 0; rr < width; ++rr) {
+                unsigned char* dst = next_slot(bytes);
+                bulk_g2s(dst, qr + jj * ld + c0, bytes, &S.full[s], pol);
+                advance();
+                if (++jj == n && rr + 1 < width) {
+                  jj = 0;
+                  ++ar;
+                  qr = P.Q + (long long)__ldg(P.act + ar) * n * ld;
+                }
+              }
+            }
+            jr += width;
+            while (jr >= n && g0 + width < nunits) {
+              jr -= n;
+              ++a;
+              qa = P.Q + (long long)__ldg(P.act + a) * n * ld;
+            }
+          }
+        } else {
+          for (long long r0 = rs; r0 < re; r0 += sp.TR) {
+            const long long r1 = min(r0 + sp.TR, re);
+            unsigned char* dst = next_slot((unsigned)((r1 - r0) * ld * 8));
+            long long row = r0;
+            while (row < r1) {             // one bulk copy per matrix the tile touches
+              const long long cnt = min(r1 - row, (long long)n - jr);
+              bulk_g2s(dst, qa + jr * ld, (unsigned)(cnt * ld * 8), &S.full[s], pol);
+              dst += cnt * ld * 8;
+              row += cnt;
+              jr += cnt;
+              if (jr == n && row < re) {
+                jr = 0;
+                ++a;
+                qa = P.Q + (long long)__ldg(P.act + a) * n * ld;
+              }
+            }
+            advance();
+          }
         }
       }
     }
@@ -200,33 +252,77 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
     const int ahi = rs < re ? (int)((re - 1) / n) : -1;
     int next_a = alo, cur_a = -1;
     double accx = 0.0;
-    for (long long t = warp; t < ntiles; t += ncw) {
-      const unsigned seq = base + (unsigned)t;
-      const unsigned s = seq % sp.nstages, use = seq / sp.nstages;
-      mbar_wait(&S.full[s], use & 1);
-      const double* tile = reinterpret_cast<const double*>(S.ring + (long long)s * sp.stage_bytes);
-      const long long r0 = rs + t * sp.TR;
-      const int cnt = (int)(min(r0 + sp.TR, re) - r0);
-      for (int rr = 0; rr < cnt; ++rr) {
-        const double u = rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32);
-        const long long row = r0 + rr;
-        const int a = (int)(row / n);
-        const int j = (int)(row - (long long)a * n);
-        if (a != cur_a) {
-          if (cur_a >= 0) {
-            if (lane == 0) K.w.segxu[segbase + (cur_a - a0)] = accx;
-            next_a = cur_a + 1;
-          }
-          for (; next_a < a; ++next_a)
-            if (lane == 0) K.w.segxu[segbase + (next_a - a0)] = 0.0;
-          cur_a = a;
-          accx = 0.0;
+    // The warp's current row (active matrix ra, row rj) and ring position
+    // (slot rs_s, phase use) advance incrementally: no divisions per tile.
+    int ra = 0;
+    long long rj = 0;
+    const unsigned ns = (unsigned)sp.nstages;
+    unsigned slot = 0, use = 0;
+    auto seek = [&](long long row, unsigned seq) {
+      ra = (int)(row / n);
+      rj = row - (long long)ra * n;
+      slot = seq % ns;
+      use = seq / ns;
+    };
+    auto step_rows = [&](long long d) {
+      rj += d;
+      while (rj >= n) { rj -= n; ++ra; }
+    };
+    auto step_seq = [&](unsigned d) {    // d <= nstages
+      slot += d;
+      if (slot >= ns) { slot -= ns; ++use; }
+    };
+    auto emit = [&](double u) {          // u = (Q x)_row: U-cache + segment sum
+      const int j = (int)rj;
+      if (ra != cur_a) {
+        if (cur_a >= 0) {
+          if (lane == 0) K.w.segxu[segbase + (cur_a - a0)] = accx;
+          next_a = cur_a + 1;
         }
-        accx += S.xs[j] * u;
-        if (lane == 0) U[(long long)__ldg(P.act + a) * n + j] = u;
+        for (; next_a < ra; ++next_a)
+          if (lane == 0) K.w.segxu[segbase + (next_a - a0)] = 0.0;
+        cur_a = ra;
+        accx = 0.0;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
+      accx += S.xs[j] * u;
+      if (lane == 0) U[(long long)__ldg(P.act + ra) * n + j] = u;
+    };
+    if (chunked) {
+      const long long full = nunits / ncw, rem = nunits - full * ncw;
+      if (warp < nunits) seek(rs + warp, base + (unsigned)warp);
+      for (long long k = warp; k < nunits; k += ncw) {
+        const unsigned width = (unsigned)(k / ncw < full ? ncw : rem);   // rows in this group
+        double u = 0.0;
+        for (int c = 0; c < sp.cpr; ++c) {
+          if (c > 0) step_seq(width);
+          mbar_wait(&S.full[slot], use & 1, K.w.abort_flag);
+          const double* tile = reinterpret_cast<const double*>(S.ring + (long long)slot * sp.stage_bytes);
+          const long long c0 = (long long)c * sp.chunk;
+          const long long len = min((long long)sp.chunk, ld - c0);
+          u += rowdot(tile, S.xs + c0, len / 2, lane, 32);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.empty[slot]);
+        }
+        emit(u);
+        step_rows(ncw);
+        step_seq((unsigned)ncw);
+      }
+    } else {
+      if (warp < nunits) seek(rs + (long long)warp * sp.TR, base + (unsigned)warp);
+      for (long long k = warp; k < nunits; k += ncw) {
+        mbar_wait(&S.full[slot], use & 1, K.w.abort_flag);
+        const double* tile = reinterpret_cast<const double*>(S.ring + (long long)slot * sp.stage_bytes);
+        const long long r0 = rs + k * sp.TR;
+        const int cnt = (int)(min(r0 + sp.TR, re) - r0);
+        for (int rr = 0; rr < cnt; ++rr) {
+          emit(rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32));
+          step_rows(1);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[slot]);
+        step_rows((long long)ncw * sp.TR - cnt);
+        step_seq((unsigned)ncw);
+      }
     }
     if (cur_a >= 0) {
       if (lane == 0) K.w.segxu[segbase + (cur_a - a0)] = accx;

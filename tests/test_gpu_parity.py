@@ -274,3 +274,30 @@ def test_oracle_live_random(small):
                           for t in ref.trace])[:200]
             np.testing.assert_array_equal(a, b)
             assert rel(res.solution.x, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("tile,stages,n", [(1024, 8, 300), (1024, 6, 300), (2048, 16, 1001), (4096, 3, 700)])
+def test_chunked_sweep_and_solver(monkeypatch, tile, stages, n):
+    """Rows wider than a ring slot stream as column chunks (C1/C2/C4 shapes in
+    production); exercise that path at oracle-checkable sizes."""
+    from oracle import rapdb_oracle as O
+    import torch
+    monkeypatch.setenv("RAPDB_TILE_BYTES", str(tile))
+    monkeypatch.setenv("RAPDB_STAGES", str(stages))
+    monkeypatch.setenv("RAPDB_ROW_TILE_MAX", "0")       # force column chunks
+    arr = instances.dense_qcqp(n, 7, 9, seed=21)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    ev = inst._evaluator()
+    x = np.random.default_rng(1).uniform(-1, 1, n)
+    u, g, _ = ev.ctx.probe_sweep(torch.from_numpy(x).cuda(), reps=2)
+    u = u.cpu().numpy()
+    for i in range(arr.m + 1):
+        assert rel(u[i], arr.Q[i] @ x) <= 1e-13
+    P = O.Problem.from_arrays(arr)
+    np.testing.assert_allclose(g.cpu().numpy()[1:], P.g(x), rtol=1e-12, atol=1e-12)
+    ref = O.run_restarted(P, O.Options(mode="yx", nonmonotone=True), O.Policy("fixed", period=40), budget=80)
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(40), budget=80)
+    a = trace_arr(res.trace)[:, TAU]
+    b = np.array([[t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total] for t in ref.trace])
+    np.testing.assert_array_equal(a, b)
+    assert rel(res.solution.x, ref.x) <= 1e-9
