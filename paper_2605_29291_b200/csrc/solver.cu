@@ -273,7 +273,8 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   K.sp = c->sp;
   K.w = c->w;
   K.rc = rc;
-  CK(cudaMemsetAsync(c->w.bar, 0, 128, c->stream));
+  CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
+  CK(cudaMemsetAsync(c->w.abort_flag, 0, 64, c->stream));
   void* args[] = {&K};
   CK(cudaLaunchCooperativeKernel((const void*)rapdb_solver_kernel, dim3(c->G), dim3(kThreads), args,
                                  c->dyn_smem, c->stream));
