@@ -149,16 +149,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
 
 // spin on an mbarrier phase; after ~10 s raise the device abort flag and give
 // up (a protocol bug then surfaces as RAPDB_EDEVICE instead of a hung GPU)
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, int* abort_flag) {
-  if (mbar_try_wait(bar, parity)) return;
-  const unsigned long long t0 = globaltimer();
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, unsigned parity, int* abort_flag) {
+  if (mbar_try_wait(bar, parity)) return true;
+  // SM cycle counter, not %globaltimer: the driver re-synchronises globaltimer
+  // with host time and it can jump (a backward jump wrapped the unsigned delta
+  // and fired this watchdog spuriously)
+  const long long t0 = clock64();
   for (unsigned spins = 1;; ++spins) {
-    if (mbar_try_wait(bar, parity)) return;
+    if (mbar_try_wait(bar, parity)) return true;
     if ((spins & 1023u) == 0) {
-      if (*(volatile int*)abort_flag) return;
-      if (globaltimer() - t0 > 10000000000ull) {
-        atomicExch(abort_flag, 1);
-        return;
+      if (*(volatile int*)abort_flag) return false;
+      const long long el = (clock64() - t0) / 2;   // ~ns at ~2 GHz
+      if (el > 20000000000ll) {
+        if (atomicExch(abort_flag, 2) == 0) {   // 2: mbarrier (bulk-copy pipeline) timeout
+          abort_flag[1] = blockIdx.x;
+          abort_flag[2] = threadIdx.x;
+          abort_flag[3] = (int)parity;
+          abort_flag[4] = (int)(el / 1000000ll);
+          abort_flag[5] = (int)(smem_u32(bar) & 0x3ffff);
+        }
+        return false;
       }
     }
   }

@@ -137,7 +137,13 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
   __shared__ double s_part[2][kMaxTR][8];
   __shared__ SolverState s_st;
   __shared__ int s_flag[4];
+  __shared__ unsigned s_prog[kConsumerWarps];
+  __shared__ unsigned s_tag[32], s_rel[32];
   Sm S;
+  S.prog = s_prog;
+  S.tag = s_tag;
+  S.rel = s_rel;
+  if (threadIdx.x < kConsumerWarps) s_prog[threadIdx.x] = 0;
   S.xs = reinterpret_cast<double*>(dsm);
   S.ring = dsm + K.sp.xs_bytes;
   S.full = reinterpret_cast<uint64_t*>(S.ring + (long long)K.sp.nstages * K.sp.stage_bytes);
@@ -252,7 +258,7 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_AUX2] = n * 8;
   sz[B_ST] = sizeof(SolverState);
   sz[B_BAR] = 64;
-  sz[B_ABORT] = 64;
+  sz[B_ABORT] = 128;
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -274,7 +280,7 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   K.w = c->w;
   K.rc = rc;
   CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
-  CK(cudaMemsetAsync(c->w.abort_flag, 0, 64, c->stream));
+  CK(cudaMemsetAsync(c->w.abort_flag, 0, 128, c->stream));
   void* args[] = {&K};
   CK(cudaLaunchCooperativeKernel((const void*)rapdb_solver_kernel, dim3(c->G), dim3(kThreads), args,
                                  c->dyn_smem, c->stream));
@@ -288,7 +294,19 @@ int read_state(rapdb_ctx* c, SolverState* st) {
   CK(cudaMemcpyAsync(st, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (ab) return fail(c, RAPDB_EDEVICE, "device watchdog fired (grid barrier timeout)");
+  if (ab) {
+    int info[20] = {0};
+    cudaMemcpy(info, c->w.abort_flag, sizeof(info), cudaMemcpyDeviceToHost);
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "device watchdog fired (%s): cta=%d thread=%d parity=%d waited_ms=%d bar=0x%x "
+                  "issued=%d slot=%d use=%d ntiles=%d base=%d prog=[%d %d %d %d %d %d %d %d]",
+                  ab == 2 ? "bulk-copy pipeline timeout" : ab == 1 ? "grid barrier timeout" :
+                  ab == 3 ? "ring slot holds another tile (seq/slot/tag/use/base in issued..base)" :
+                  ab == 4 ? "ring slot released by another tile (seq/slot/rel in issued..use)" : "abort flag corrupted",
+                  info[1], info[2], info[3], info[4], info[5], info[6], info[7], info[8], info[9], info[10],
+                  info[11], info[12], info[13], info[14], info[15], info[16], info[17], info[18]);
+    return fail(c, RAPDB_EDEVICE, buf);
+  }
   return RAPDB_OK;
 }
 
@@ -377,7 +395,7 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   const char* env_st = std::getenv("RAPDB_STAGES");
   const char* env_rt = std::getenv("RAPDB_ROW_TILE_MAX");
   const long long tile_target = env_tile ? std::max(1024LL, std::atoll(env_tile)) : 16384;
-  const long long max_stages = env_st ? std::max(2LL, std::atoll(env_st)) : 16;
+  const long long max_stages = std::min(32LL, env_st ? std::max(2LL, std::atoll(env_st)) : 16LL);
   const long long row_tile_max = env_rt ? std::atoll(env_rt) : 49152;
   SweepPlan sp{};
   if (row_bytes > tile_target && row_bytes <= row_tile_max) {   // one whole row per tile

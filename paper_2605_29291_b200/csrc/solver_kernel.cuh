@@ -32,6 +32,9 @@ struct Sm {
   double (*part)[kMaxTR][8];
   SolverState* st;
   int* flag;
+  volatile unsigned* prog; // [8] units consumed per consumer warp in the current sweep
+  volatile unsigned* tag;  // [32] sequence number of the tile last issued into each slot
+  volatile unsigned* rel;  // [32] sequence number of the tile last released from each slot
   unsigned long long gen;  // grid-barrier generation (thread 0)
   unsigned pseq;           // pipeline sequence (producer lane / consumers)
 };
@@ -46,12 +49,12 @@ __device__ __noinline__ bool gsync(const KArgs& K, Sm& S) {
     atomicAdd(K.w.bar, 1ULL);
     volatile unsigned long long* vb = K.w.bar;
     volatile int* va = K.w.abort_flag;
-    const unsigned long long t0 = globaltimer();
+    const long long t0 = clock64();   // monotonic per SM (see mbar_wait)
     int ab = 0;
     while (*vb < S.gen) {
       if (*va) { ab = 1; break; }
-      if (globaltimer() - t0 > 30000000000ull) {   // 30 s watchdog
-        atomicExch(K.w.abort_flag, 1);
+      if (clock64() - t0 > 60000000000ll) {   // ~30 s watchdog
+        atomicExch(K.w.abort_flag, 1);   // 1: grid-barrier timeout
         ab = 1;
         break;
       }
@@ -166,8 +169,25 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
       const uint64_t pol = evict_first_policy();
       const int ns = sp.nstages;
       unsigned s = base % ns, use = base / ns;
+      unsigned issued = 0;
       auto next_slot = [&](unsigned bytes) -> unsigned char* {
-        if (use > 0) mbar_wait(&S.empty[s], (use - 1) & 1, K.w.abort_flag);
+        const unsigned seq = base + issued;
+        if (use > 0 && !mbar_wait(&S.empty[s], (use - 1) & 1, K.w.abort_flag)) {
+          int* f = K.w.abort_flag;   // diagnostics of a stalled ring (host prints them)
+          f[6] = (int)issued;
+          f[7] = (int)s;
+          f[8] = (int)use;
+          f[9] = (int)ntiles;
+          f[10] = (int)base;
+          for (int w = 0; w < kConsumerWarps; ++w) f[11 + w] = (int)S.prog[w];
+        } else if (use > 0 && S.rel[s] != seq - (unsigned)ns) {
+          int* f = K.w.abort_flag;   // protocol check: slot released by the wrong tile
+          if (atomicExch(f, 4) == 0) {
+            f[1] = blockIdx.x; f[2] = threadIdx.x; f[6] = (int)seq; f[7] = (int)s; f[8] = (int)S.rel[s];
+          }
+        }
+        ++issued;
+        S.tag[s] = seq;
         unsigned char* dst = S.ring + (long long)s * sp.stage_bytes;
         mbar_expect_tx(&S.full[s], bytes);
         return dst;
@@ -300,6 +320,7 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
           const long long c0 = (long long)c * sp.chunk;
           const long long len = min((long long)sp.chunk, ld - c0);
           u += rowdot(tile, S.xs + c0, len / 2, lane, 32);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.empty[slot]);
         }
@@ -310,7 +331,14 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
     } else {
       if (warp < nunits) seek(rs + (long long)warp * sp.TR, base + (unsigned)warp);
       for (long long k = warp; k < nunits; k += ncw) {
-        mbar_wait(&S.full[slot], use & 1, K.w.abort_flag);
+        const unsigned expect = base + (unsigned)k;
+        if (mbar_wait(&S.full[slot], use & 1, K.w.abort_flag) && S.tag[slot] != expect) {
+          int* f = K.w.abort_flag;   // protocol check: slot holds another tile
+          if (lane == 0 && atomicExch(f, 3) == 0) {
+            f[1] = blockIdx.x; f[2] = threadIdx.x; f[6] = (int)expect; f[7] = (int)slot;
+            f[8] = (int)S.tag[slot]; f[9] = (int)use; f[10] = (int)base;
+          }
+        }
         const double* tile = reinterpret_cast<const double*>(S.ring + (long long)slot * sp.stage_bytes);
         const long long r0 = rs + k * sp.TR;
         const int cnt = (int)(min(r0 + sp.TR, re) - r0);
@@ -318,8 +346,15 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
           emit(rowdot(tile + rr * ld, S.xs, ld / 2, lane, 32));
           step_rows(1);
         }
+        // generic-proxy reads of the slot must be ordered before the producer's
+        // next async-proxy (bulk copy) write into it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[slot]);
+        if (lane == 0) {
+          S.rel[slot] = expect;
+          mbar_arrive(&S.empty[slot]);
+          S.prog[warp] = (unsigned)(k + 1);
+        }
         step_rows((long long)ncw * sp.TR - cnt);
         step_seq((unsigned)ncw);
       }
