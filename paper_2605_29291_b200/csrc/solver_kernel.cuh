@@ -313,16 +313,27 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
       for (long long k = warp; k < nunits; k += ncw) {
         const unsigned width = (unsigned)(k / ncw < full ? ncw : rem);   // rows in this group
         double u = 0.0;
+        const unsigned gseq = base + (unsigned)((k / ncw) * sp.cpr * ncw) + (unsigned)warp;
         for (int c = 0; c < sp.cpr; ++c) {
           if (c > 0) step_seq(width);
-          mbar_wait(&S.full[slot], use & 1, K.w.abort_flag);
+          const unsigned expect = gseq + (unsigned)c * width;
+          if (mbar_wait(&S.full[slot], use & 1, K.w.abort_flag) && S.tag[slot] != expect) {
+            int* f = K.w.abort_flag;
+            if (lane == 0 && atomicExch(f, 3) == 0) {
+              f[1] = blockIdx.x; f[2] = threadIdx.x; f[6] = (int)expect; f[7] = (int)slot;
+              f[8] = (int)S.tag[slot]; f[9] = (int)use; f[10] = (int)base;
+            }
+          }
           const double* tile = reinterpret_cast<const double*>(S.ring + (long long)slot * sp.stage_bytes);
           const long long c0 = (long long)c * sp.chunk;
           const long long len = min((long long)sp.chunk, ld - c0);
           u += rowdot(tile, S.xs + c0, len / 2, lane, 32);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) mbar_arrive(&S.empty[slot]);
+          if (lane == 0) {
+            S.rel[slot] = expect;
+            mbar_arrive(&S.empty[slot]);
+          }
         }
         emit(u);
         step_rows(ncw);
