@@ -135,13 +135,17 @@ int rapdb_get_iterate(rapdb_ctx* ctx, int which, double* x, double* v, double* l
  * device buffers; reps > 1 repeats it (timing); *ms = mean device ms/sweep.   */
 int rapdb_probe_sweep(rapdb_ctx* ctx, const double* x, double* u, double* g, int reps, float* ms);
 
-/* smoothed_gap(z, xi) at the current iterate (source 1) or the ergodic
- * average (2) (diagnostics.py:120-163): dense H = Q0 + sum lam_i Q_i, power
- * iteration (problem.py:47-68), APG subsolver (subsolve.py:27-62).  x_warm is
- * a device pointer or NULL.  out[4] host = gap, iterations, residual, converged.
- * The candidate x used is written to x_cand (device, n) for the next warm start. */
-int rapdb_smoothed_gap(rapdb_ctx* ctx, int source, double xi, double tol, const double* x_warm,
-                       double* x_cand, double* out);
+/* smoothed_gap(z, xi) (diagnostics.py:120-163) at an explicit point (source 0:
+ * device x[n], v[p], lam[m], used as given -- no projection), the current
+ * iterate (1) or the ergodic average (2): closed-form dual step, dense
+ * H = Q0 + sum lam_i Q_i built in one pass over the stack, power iteration for
+ * ||H|| (problem.py:47-68), accelerated projected gradient with function-value
+ * restart on Phi(., y) + xi |. - x|^2 (subsolve.py:27-62), all in one device
+ * launch.  x_warm: device pointer or NULL.  x_cand (device, n) receives the
+ * candidate's x for the next warm start (restarts.py:148).
+ * out[6] host = gap, subsolver iterations, residual, converged, L, dual_term. */
+int rapdb_smoothed_gap(rapdb_ctx* ctx, int source, const double* x, const double* v, const double* lam,
+                       double xi, double tol, const double* x_warm, double* x_cand, double* out);
 
 #ifdef __cplusplus
 }

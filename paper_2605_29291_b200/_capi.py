@@ -79,7 +79,7 @@ def load(path: str = LIB_PATH):
     lib.rapdb_kkt.argtypes = [P, I, D, C.POINTER(D)]
     lib.rapdb_get_iterate.argtypes = [P, I, P, P, P]
     lib.rapdb_probe_sweep.argtypes = [P, P, P, P, I, C.POINTER(C.c_float)]
-    lib.rapdb_smoothed_gap.argtypes = [P, I, D, D, P, P, C.POINTER(D)]
+    lib.rapdb_smoothed_gap.argtypes = [P, I, P, P, P, D, D, P, P, C.POINTER(D)]
     lib.rapdb_launch_count.restype = LL
     _lib = lib
     return lib
@@ -206,9 +206,11 @@ class Context:
         self._check(self.lib.rapdb_probe_sweep(self.h, _ptr(x), _ptr(u), _ptr(g), int(reps), C.byref(ms)))
         return u, g, float(ms.value)
 
-    def smoothed_gap(self, source: int, xi: float, tol: float, x_warm=None, x_cand=None):
-        out = (C.c_double * 4)()
+    def smoothed_gap(self, source: int, xi: float, tol: float, x_warm=None, x_cand=None, point=None):
+        """point = (x, v, lam) device tensors for source 0."""
+        out = (C.c_double * 6)()
+        x, v, lam = point if point is not None else (None, None, None)
         self._set_stream()
-        self._check(self.lib.rapdb_smoothed_gap(self.h, source, float(xi), float(tol), _ptr(x_warm),
-                                                _ptr(x_cand), out))
+        self._check(self.lib.rapdb_smoothed_gap(self.h, source, _ptr(x), _ptr(v), _ptr(lam), float(xi),
+                                                float(tol), _ptr(x_warm), _ptr(x_cand), out))
         return list(out)

@@ -38,10 +38,11 @@ enum Slot {
   S_STAT, S_EQ2, S_COMP, S_GPOS2, S_GPOS1,      // KKT
   S_PHIV, S_PHIL,                               // Phi at a (re)start point
   S_AVG_V, S_AVG_L,                             // ball norms of an average point
+  S_GAPQ,                                       // z'Hz in the smoothed-gap subsolver
   NSLOT
 };
 
-enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4 };
+enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5 };
 enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
                  ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6 };
 
@@ -49,6 +50,7 @@ struct SolverState {
   double tau_cand, tau_prev, gamma, sigma_prev, alpha, beta, sigma0, T, phi_k;
   double fail_tau, fail_gamma;
   double metrics[8];
+  double gap[6];           // gap, subsolver iterations, residual, converged, L, dual term
   double sweep_ns;
   long long iters, evals_total, inner, fail_iter, sweeps;
   int cur, ig_prev, ig_cur, ig_new, has_sigma0, status, has_metrics, pad;
@@ -90,6 +92,7 @@ struct SweepPlan {
 struct Work {
   double *x, *U, *gval, *eqv, *y, *ytr, *gy, *gxb, *gxs, *xcum, *ycum, *part,
          *segxu, *segqx, *zq, *aux, *aux2;
+  double *H, *hx, *hxn, *hy;   // smoothed gap: dense H (n x n) and H-products
   double* trace;
   SolverState* st;
   unsigned long long* bar;
@@ -101,6 +104,8 @@ struct RunCfg {
   int metrics_every, criterion, has_f_star, fixed_period, fixed_point, warm_tau, stop_at_fixed;
   int op, src, reset_inner, reps;
   double eps, eps_kkt, eps_feas, f_star;
+  double xi, tol;                  // smoothed gap
+  const double* warm;              // smoothed gap subsolver warm start (or null)
   const double* in_x; const double* in_v; const double* in_lam;   // explicit points
   double* out_x; double* out_v; double* out_lam; double* out_u; double* out_g;
 };

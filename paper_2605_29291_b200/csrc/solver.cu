@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "gap.cuh"
 #include "rapdb_b200.h"
 #include "solver_ops.cuh"
 
@@ -181,6 +182,9 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
     case OP_PROBE:
       op_probe(K, S);
       break;
+    case OP_GAP:
+      dev_gap(K, S);
+      break;
     default:
       break;
   }
@@ -206,6 +210,7 @@ struct rapdb_ctx {
   int* d_ints = nullptr;
   long long ws_bytes = 0;
   long long stage_cap = 0;  // doubles available in the staging area
+  bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
 };
 
 namespace {
@@ -233,7 +238,8 @@ struct Layout {
 };
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
-             B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_COUNT };
+             B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
+             B_COUNT };
 
 Layout layout_of(const rapdb_ctx* c) {
   const long long n = c->P.n, m = c->P.m, p = c->P.p, np = n > 0 ? p + m : 0;
@@ -256,6 +262,10 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_ZQ] = std::max(c->P.nzero, 1) * 8LL;
   sz[B_AUX] = n * 8;
   sz[B_AUX2] = n * 8;
+  sz[B_H] = c->gap_ok ? n * n * 8 : 8;
+  sz[B_HX] = n * 8;
+  sz[B_HXN] = n * 8;
+  sz[B_HY] = n * 8;
   sz[B_ST] = sizeof(SolverState);
   sz[B_BAR] = 64;
   sz[B_ABORT] = 128;
@@ -426,6 +436,9 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
   c->dyn_smem = (size_t)(sp.xs_bytes + ns * sp.stage_bytes + 2 * ns * 8);
   c->stage_cap = ns * sp.stage_bytes / 8;
+  // smoothed gap: five shared n-vectors + staged multipliers in xs+ring, and a
+  // dense n x n H in the workspace (skipped for very large n)
+  c->gap_ok = (5LL * n + m + p + m + 64) * 8 <= sp.xs_bytes + ns * sp.stage_bytes && n <= 16384;
   if (2LL * (p + m) > c->stage_cap)
     return fail(c, RAPDB_ECONFIG, "too many multipliers for the shared-memory dual staging area");
   cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
@@ -518,6 +531,10 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.gy = D(B_GY); w.gxb = D(B_GXB); w.gxs = D(B_GXS); w.xcum = D(B_XCUM); w.ycum = D(B_YCUM);
   w.part = D(B_PART); w.segxu = D(B_SEGXU); w.segqx = D(B_SEGQX); w.zq = D(B_ZQ); w.aux = D(B_AUX);
   w.aux2 = D(B_AUX2);
+  w.H = D(B_H);
+  w.hx = D(B_HX);
+  w.hxn = D(B_HXN);
+  w.hy = D(B_HY);
   w.trace = nullptr;
   w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);
@@ -658,10 +675,31 @@ int rapdb_probe_sweep(rapdb_ctx* c, const double* x, double* u, double* g, int r
   return r;
 }
 
-int rapdb_smoothed_gap(rapdb_ctx* c, int source, double xi, double tol, const double* x_warm, double* x_cand,
-                       double* out) {
-  (void)source; (void)xi; (void)tol; (void)x_warm; (void)x_cand; (void)out;
-  return fail(c, RAPDB_ECONFIG, "smoothed_gap not built yet");
+int rapdb_smoothed_gap(rapdb_ctx* c, int source, const double* x, const double* v, const double* lam,
+                       double xi, double tol, const double* x_warm, double* x_cand, double* out) {
+  if (!c || !out) return RAPDB_EINPUT;
+  if (!(xi > 0.0)) return fail(c, RAPDB_ECONFIG, "xi must be positive");
+  if (!(tol > 0.0)) return fail(c, RAPDB_ECONFIG, "need tol > 0");
+  if (source < 0 || source > 2) return fail(c, RAPDB_EINPUT, "bad smoothed_gap source");
+  if (source == 0 && (!x || (c->P.p > 0 && !v) || (c->P.m > 0 && !lam)))
+    return fail(c, RAPDB_EINPUT, "explicit smoothed_gap point needs x, v, lam");
+  if (!c->gap_ok)
+    return fail(c, RAPDB_ECONFIG, "smoothed gap needs the dense H (n too large for this instance layout)");
+  RunCfg rc{};
+  rc.op = OP_GAP;
+  rc.src = source;
+  rc.in_x = x; rc.in_v = v; rc.in_lam = lam;
+  rc.xi = xi;
+  rc.tol = tol;
+  rc.warm = x_warm;
+  rc.out_x = x_cand;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  if (r) return r;
+  for (int i = 0; i < 6; ++i) out[i] = st.gap[i];
+  return RAPDB_OK;
 }
 
 }  // extern "C"

@@ -184,7 +184,15 @@ class ApdbEngine:
         from .diagnostics import Certificate
         torch = self._ctx.torch
         x_cand = torch.empty(self.inst.n, dtype=torch.float64, device=self._ctx.device)
-        out = self._ctx.smoothed_gap(source, xi, tol, x_warm, x_cand)
+        point = None
+        if raw_point is not None:
+            source = 0
+            point = (self._tensor(raw_point.x, self.inst.n), self._tensor(raw_point.v, self.inst.p),
+                     self._tensor(raw_point.lam, self.inst.m))
+        if x_warm is not None and not hasattr(x_warm, "data_ptr"):
+            x_warm = self._tensor(x_warm, self.inst.n)
+        out = self._ctx.smoothed_gap(source, xi, tol, x_warm, x_cand, point)
+        self.last_gap = out
         return out[0], Certificate(int(out[1]), out[2], bool(out[3])), x_cand
 
     def step(self) -> TraceRecord:

@@ -301,3 +301,89 @@ def test_chunked_sweep_and_solver(monkeypatch, tile, stages, n):
     b = np.array([[t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total] for t in ref.trace])
     np.testing.assert_array_equal(a, b)
     assert rel(res.solution.x, ref.x) <= 1e-9
+
+
+# ----------------------------------------------------------------- adaptive restart
+
+def _gap_rows(trace_like):
+    t = trace_like
+    return t[~np.isnan(t[:, 9])][:, [0, 9]]
+
+
+def test_adaptive_small_qcqp(small):
+    g, inst = small
+    key = "yx_nm_ada"
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True),
+                          R.AdaptiveRestart(warmup=50, check_period=100), budget=1500,
+                          criteria=crit(1e-8))
+    tr = trace_arr(res.trace)
+    tr_g = g[f"{key}/trace"]
+    np.testing.assert_array_equal(tr[:200, TAU], tr_g[:200, TAU])
+    # restart decisions must coincide while the compared gaps are above the
+    # subsolver-tolerance floor (~1e-9 here); below it both are rounding noise
+    ref_it = list(g[f"{key}/restart_iters"])
+    ref_gaps = g[f"{key}/restart_gaps"]
+    meaningful = [it for it, (gn, gr) in zip(ref_it, ref_gaps) if gr > 1e-8]
+    assert [e.iteration for e in res.restart_log][:len(meaningful)] == meaningful
+    ours, ref = _gap_rows(tr), _gap_rows(tr_g)
+    k = min(len(ours), len(ref))
+    np.testing.assert_array_equal(ours[:k, 0][ref[:k, 1] > 1e-8], ref[:k, 0][ref[:k, 1] > 1e-8])
+    ours, ref = ours[:k], ref[:k]
+    big = np.abs(ref[:, 1]) > 1e-7          # above the subsolver-tolerance floor
+    np.testing.assert_allclose(ours[big, 1], ref[big, 1], rtol=1e-5)
+    for e in res.restart_log:
+        assert e.gap_new <= 0.5 * e.gap_ref + 1e-9
+
+
+@pytest.mark.parametrize("key,nm", [("mono_ada", False), ("nm_ada", True)])
+def test_c0_adaptive(key, nm):
+    g = load_golden("c0")
+    arr = instances.config_instance("C0")
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.AdaptiveRestart(),
+                          budget=50000, criteria=crit(1e-6))
+    tr = trace_arr(res.trace)
+    tr_g = g[f"{key}/trace"]
+    np.testing.assert_array_equal(tr[:200, TAU], tr_g[:200, TAU])
+    it_ref = int(g[f"{key}/iterations"])
+    lo, hi = iteration_band(key, it_ref)
+    assert 0.98 * lo <= res.iterations <= 1.02 * hi, (res.iterations, lo, hi)
+    assert res.converged and res.metrics.kkt_residual <= 1e-6
+    met = g[f"{key}/metrics"]
+    assert abs(res.metrics.f_value - met[5]) <= 1e-6 * abs(met[5])
+    if lo == hi:
+        assert [e.iteration for e in res.restart_log] == list(g[f"{key}/restart_iters"])
+        ours, ref = _gap_rows(tr), _gap_rows(tr_g)
+        np.testing.assert_array_equal(ours[:, 0], ref[:, 0])
+        big = np.abs(ref[:, 1]) > 1e-7
+        np.testing.assert_allclose(ours[big, 1], ref[big, 1], rtol=1e-5)
+
+
+def test_smoothed_gap_kats():
+    """Gap ~ 0 at the analytic saddle points, > 1 off-optimum on the ball
+    instance (test_diagnostics.py:19-37); equal to the oracle at random points."""
+    from paper_2605_29291_b200.diagnostics import smoothed_gap
+    from oracle import rapdb_oracle as O
+    g = load_golden("analytic")
+    rng = np.random.default_rng(13)
+    for name in ANALYTIC_NAMES:
+        a = analytic_arrays(g, name)
+        inst = inst_from(a["Q"], a["q"], a["r"], a["lower"], a["upper"], a["A"], a["b"], a["mu"])
+        zs = R.Iterate(g[f"{name}/x_star"], g[f"{name}/v_star"], g[f"{name}/lam_star"])
+        gap, cert = smoothed_gap(inst, zs, 0.04, subsolver_tol=1e-11)
+        assert cert.converged and abs(gap) <= 1e-7, (name, gap)
+        P = O.Problem(list(a["Q"]), list(a["q"]), a["r"], a["A"], a["b"], a["lower"], a["upper"], a["mu"])
+        lo = np.maximum(a["lower"], -10)
+        hi = np.minimum(a["upper"], 10)
+        for _ in range(5):
+            x = rng.uniform(lo, hi)
+            lam = np.abs(rng.normal(size=inst.m))
+            v = rng.normal(size=inst.p)
+            ours, _ = smoothed_gap(inst, R.Iterate(x, v, lam), 0.04, subsolver_tol=1e-10)
+            ref, _ = O.smoothed_gap(P, x, v, lam, 0.04, tol=1e-10)
+            assert ours >= -1e-9
+            assert abs(ours - ref) <= 1e-7 * max(1.0, abs(ref)), (name, ours, ref)
+    a = analytic_arrays(g, "ball")
+    inst = inst_from(a["Q"], a["q"], a["r"], a["lower"], a["upper"])
+    gap, _ = smoothed_gap(inst, R.Iterate(np.zeros(2), np.zeros(0), np.zeros(1)), 0.04, subsolver_tol=1e-11)
+    assert gap > 1.0
