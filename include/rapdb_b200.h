@@ -83,6 +83,23 @@ typedef struct {
 /* process-wide number of kernel launches issued by this library */
 long long rapdb_launch_count(void);
 
+/* ---- constraint sharding ---------------------------
+ * Rank r binds only its matrices [k0, k1) of the m+1 stack (rapdb_bind_dense);
+ * x, (v, lam), q, r, A, b and the bounds are replicated.  A sharded context
+ * ("split", set automatically when nranks > 1, or forced for testing) stops at
+ * every exchange point and calls `fn(user, kind)`; the callback must sum the
+ * buffer(s) returned by rapdb_exchange_buffers(kind) across all ranks
+ * (all-reduce, identical result on every rank) and return 0; the op then
+ * resumes.  Exchange kinds: 1 partial grad_x Phi (n), 2 constraint values
+ * g (m+1, exact: disjoint supports), 3 two gradients (n + n, APDB-xy),
+ * 4 H (n*n, smoothed gap).  Per yx trial: one n-vector and one (m+1)-vector. */
+typedef int (*rapdb_exchange_fn)(void* user, int kind);
+int rapdb_set_exchange(rapdb_ctx* ctx, rapdb_exchange_fn fn, void* user, int force_split);
+int rapdb_exchange_buffers(rapdb_ctx* ctx, int kind, double** buf0, long long* count0,
+                           double** buf1, long long* count1);
+/* number of exchanges performed by this context so far */
+long long rapdb_exchange_count(const rapdb_ctx* ctx);
+
 /* version of the ABI (bumped on incompatible change) */
 int rapdb_abi_version(void);
 

@@ -45,7 +45,11 @@ _lib = None
 EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_error", "rapdb_set_stream",
            "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
-           "rapdb_smoothed_gap", "rapdb_launch_count"]
+           "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
+           "rapdb_exchange_count"]
+
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
+X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
 
 
 def launch_count() -> int:
@@ -81,6 +85,11 @@ def load(path: str = LIB_PATH):
     lib.rapdb_probe_sweep.argtypes = [P, P, P, P, I, C.POINTER(C.c_float)]
     lib.rapdb_smoothed_gap.argtypes = [P, I, P, P, P, D, D, P, P, C.POINTER(D)]
     lib.rapdb_launch_count.restype = LL
+    lib.rapdb_set_exchange.argtypes = [P, EXCHANGE_FN, P, I]
+    lib.rapdb_exchange_buffers.argtypes = [P, I, C.POINTER(C.c_void_p), C.POINTER(LL),
+                                           C.POINTER(C.c_void_p), C.POINTER(LL)]
+    lib.rapdb_exchange_count.argtypes = [P]
+    lib.rapdb_exchange_count.restype = LL
     _lib = lib
     return lib
 
@@ -138,14 +147,46 @@ class Context:
     def _set_stream(self):
         self.lib.rapdb_set_stream(self.h, C.c_void_p(self.stream().cuda_stream))
 
+    # -- sharding ----------------------------------------------------------
+    def set_exchange(self, fn, force_split=False):
+        """fn(kind) -> None must all-reduce (sum) self.exchange_views(kind) across
+        ranks.  Must be called before bind()."""
+        def _cb(user, kind):
+            try:
+                fn(int(kind))
+                return 0
+            except Exception as exc:  # surfaced as DeviceError by the C side
+                self._cb_error = exc
+                return 1
+        self._cb = EXCHANGE_FN(_cb)      # keep the thunk alive
+        self._check(self.lib.rapdb_set_exchange(self.h, self._cb, None, 1 if force_split else 0))
+
+    def exchange_views(self, kind):
+        """float64 views into the workspace of the buffer(s) to all-reduce."""
+        b0, b1 = C.c_void_p(), C.c_void_p()
+        n0, n1 = C.c_longlong(), C.c_longlong()
+        self._check(self.lib.rapdb_exchange_buffers(self.h, kind, C.byref(b0), C.byref(n0),
+                                                    C.byref(b1), C.byref(n1)))
+        base = self.ws.data_ptr()
+        out = []
+        for b, cnt in ((b0, n0), (b1, n1)):
+            if b.value and cnt.value > 0:
+                off = b.value - base
+                out.append(self.ws[off:off + 8 * cnt.value].view(self.torch.float64))
+        return out
+
+    def exchange_count(self):
+        return int(self.lib.rapdb_exchange_count(self.h))
+
     # -- binding -----------------------------------------------------------
-    def bind(self, data, cfg):
-        """data: problem.DeviceData; cfg: resolved SolverConfig."""
+    def bind(self, data, cfg, k0=0, k1=None):
+        """data: problem.DeviceData (data.Q holds matrices k0..k1-1); cfg: resolved SolverConfig."""
         from .geometry import ball_code
         self._set_stream()
+        k1 = data.m + 1 if k1 is None else k1
         zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)
         self._check(self.lib.rapdb_bind_dense(
-            self.h, data.n, data.m, data.p, 0, data.m + 1, data.ld,
+            self.h, data.n, data.m, data.p, k0, k1, data.ld,
             _ptr(data.Q), _ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
             _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
             zero.ctypes.data_as(C.c_void_p)))

@@ -103,29 +103,37 @@ __device__ __forceinline__ void gap_pgrad(const KArgs& K, const GapScratch& g, c
   }
 }
 
-__device__ bool dev_gap(const KArgs& K, Sm& S) {
+// G_CAND: choose the candidate parity (st.pad); a point that is not the current
+// iterate gets one sweep (its g is then exchanged at G_GLOCAL)
+__device__ int g_cand(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const int n = P.n, p = P.p, np = p + P.m;
+  const int nxt = st.cur ^ 1;
+  const bool fresh = K.rc.src != 1 && !(K.rc.src == 2 && !(st.T > 0.0));
+  if (threadIdx.x == 0) st.pad = fresh ? nxt : st.cur;
+  __syncthreads();
+  if (!fresh) return G_HPART;
+  const bool avg = K.rc.src == 2;
+  for (long long j = gtid(); j < n; j += gstride())
+    w.x[(long long)nxt * n + j] = avg ? ldcg(w.xcum + j) / st.T : ldcg(K.rc.in_x + j);
+  for (long long j = gtid(); j < np; j += gstride())
+    w.y[(long long)nxt * np + j] = avg ? ldcg(w.ycum + j) / st.T
+                                        : (j < p ? ldcg(K.rc.in_v + j) : ldcg(K.rc.in_lam + (j - p)));
+  if (!gsync(K, S)) return kAbort;
+  return sweep_sync(K, S, w.x + (long long)nxt * n, nxt) ? G_GLOCAL : kAbort;
+}
+
+// G_HPART: dual term (needs the full g) and this rank's share of H      [X_H]
+__device__ int g_hpart(const KArgs& K, Sm& S, int& xk) {
   const DevProblem& P = K.P;
   const DevParams& prm = K.prm;
   const Work& w = K.w;
   SolverState& st = *S.st;
   const int n = P.n, p = P.p, m = P.m, np = p + m;
   const double xi = K.rc.xi;
-  const int cur = st.cur, nxt = cur ^ 1;
-  // ---- 1. candidate point (x_c, y_c) and its (Ax-b, g): parity cur or nxt
-  int cp = cur;
-  if (K.rc.src != 1 && !(K.rc.src == 2 && !(st.T > 0.0))) {
-    cp = nxt;
-    const bool avg = K.rc.src == 2;
-    for (long long j = gtid(); j < n; j += gstride())
-      w.x[(long long)nxt * n + j] = avg ? ldcg(w.xcum + j) / st.T : ldcg(K.rc.in_x + j);
-    for (long long j = gtid(); j < np; j += gstride())
-      w.y[(long long)nxt * np + j] = avg ? ldcg(w.ycum + j) / st.T
-                                          : (j < p ? ldcg(K.rc.in_v + j) : ldcg(K.rc.in_lam + (j - p)));
-    if (!gsync(K, S)) return false;
-    if (!sweep_sync(K, S, w.x + (long long)nxt * n, nxt)) return false;
-    for (long long i = gtid(); i <= m; i += gstride()) w.gval[(long long)nxt * (m + 1) + i] = g_combine(K, (int)i);
-    if (!gsync(K, S)) return false;
-  }
+  const int cp = st.pad;
   const double* xcand = w.x + (long long)cp * n;
   const double* ycand = w.y + (long long)cp * np;
   const double* gvc = w.gval + (long long)cp * (m + 1);
@@ -172,7 +180,9 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
     const long long gw = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * kWarps;
     constexpr int KC = 16;                  // columns per lane per pass: 16 loads in flight
-    const bool q0 = __ldg(P.mat_slot) >= 0; // an all-zero Q0 is not read
+    // this rank's share: Q0 if held (and not all-zero), then its local Q_i
+    const bool q0 = P.k0 == 0 && __ldg(P.mat_slot) >= 0;
+    const int i_lo = P.k0 == 0 ? 1 : P.k0;
     for (long long r = gw; r < n; r += nw) {
       for (int cb = 0; cb < n; cb += 32 * KC) {
         double h[KC];
@@ -181,10 +191,10 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
           const int c = cb + lane + 32 * k;
           h[k] = (q0 && c < n) ? __ldg(P.Q + r * ld + c) : 0.0;
         }
-        for (int i = 1; i <= m; ++i) {
+        for (int i = i_lo; i < P.k1; ++i) {
           const double l = lam_s[i - 1];
-          if (l == 0.0 || __ldg(P.mat_slot + i) < 0) continue;   // diagnostics.py:146
-          const double* qi = P.Q + ((long long)i * n + r) * ld;
+          if (l == 0.0 || __ldg(P.mat_slot + (i - P.k0)) < 0) continue;   // diagnostics.py:146
+          const double* qi = P.Q + ((long long)(i - P.k0) * n + r) * ld;
           double qv[KC];
 #pragma unroll
           for (int k = 0; k < KC; ++k) {
@@ -203,7 +213,25 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
     }
     __syncthreads();
   }
-  // c_bar + A'v (shared), r_bar - v'b (scalar)
+  if (threadIdx.x == 0) st.gap[5] = dual_term;
+  __syncthreads();
+  xk = X_H;
+  return G_SOLVE;
+}
+
+// G_SOLVE: ||H|| by power iteration, then the APG subsolver; writes st.gap
+__device__ int g_solve(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const int n = P.n, p = P.p, m = P.m;
+  const double xi = K.rc.xi;
+  const int cp = st.pad;
+  const double* xcand = w.x + (long long)cp * n;
+  const double* ycand = w.y + (long long)cp * (p + m);
+  const double dual_term = st.gap[5];
+  double* H = w.H;
+  // c_bar + A'v (shared), r_bar - v'b (scalar); q, r are replicated on every rank
   double* V = reinterpret_cast<double*>(S.xs);   // xs + ring: >= 5n doubles (checked at bind)
   GapScratch g{V, V + n, V + 2 * n, V + 3 * n, V + 4 * n};
   double* lam_s = S.stage + 5 * n;               // after the five vectors
@@ -234,7 +262,6 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
     cst = cst - vb;
   }
   __syncthreads();
-  if (!gsync(K, S)) return false;   // H complete
 
   // ---- 4. power iteration on H'H (H symmetric): L = 1.01 * sqrt(|H H v|)
   double* T = w.hx;      // scratch n-vectors in global memory
@@ -254,10 +281,10 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
     __syncthreads();
     for (int it = 0; it < 200; ++it) {
       double q;
-      if (!gap_matvec(K, S, H, pv, T, q)) return false;
+      if (!gap_matvec(K, S, H, pv, T, q)) return kAbort;
       for (int j = threadIdx.x; j < n; j += kThreads) tv2[j] = ldcg(T + j);
       __syncthreads();
-      if (!gap_matvec(K, S, H, tv2, W2, q)) return false;
+      if (!gap_matvec(K, S, H, tv2, W2, q)) return kAbort;
       double s2 = 0.0;
       for (int j = threadIdx.x; j < n; j += kThreads) {
         const double wj = ldcg(W2 + j);
@@ -290,7 +317,7 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
   }
   __syncthreads();
   double quad;
-  if (!gap_matvec(K, S, H, g.xa, hx, quad)) return false;
+  if (!gap_matvec(K, S, H, g.xa, hx, quad)) return kAbort;
   double fx = gap_value(K, S, g, g.xa, quad, cst, xi);
   const double* hyk = hx;   // yk == x at the start
   double t = 1.0, residual = 0.0;
@@ -299,12 +326,12 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
   for (int it = 1; it <= max_iter; ++it) {
     gap_pgrad(K, g, g.yk, hyk, step, xi, g.xn);
     __syncthreads();
-    if (!gap_matvec(K, S, H, g.xn, hxn, quad)) return false;
+    if (!gap_matvec(K, S, H, g.xn, hxn, quad)) return kAbort;
     double fn = gap_value(K, S, g, g.xn, quad, cst, xi);
     if (fn > fx + 1e-12 * (1.0 + fabs(fx))) {
       gap_pgrad(K, g, g.xa, hx, step, xi, g.xn);
       __syncthreads();
-      if (!gap_matvec(K, S, H, g.xn, hxn, quad)) return false;
+      if (!gap_matvec(K, S, H, g.xn, hxn, quad)) return kAbort;
       fn = gap_value(K, S, g, g.xn, quad, cst, xi);
       t = 1.0;
     }
@@ -336,7 +363,7 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
         break;
       }
     }
-    if (!gap_matvec(K, S, H, g.yk, hy, quad)) return false;
+    if (!gap_matvec(K, S, H, g.yk, hy, quad)) return kAbort;
     hyk = hy;
   }
   if (!finished) {
@@ -353,7 +380,7 @@ __device__ bool dev_gap(const KArgs& K, Sm& S) {
     st.gap[5] = dual_term;
   }
   __syncthreads();
-  return true;
+  return DONE;
 }
 
 }  // namespace rapdb

@@ -44,7 +44,7 @@ enum Slot {
 
 enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5 };
 enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
-                 ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6 };
+                 ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6, ST_EXCHANGE = 7, ST_RUNNING = 8 };
 
 struct SolverState {
   double tau_cand, tau_prev, gamma, sigma_prev, alpha, beta, sigma0, T, phi_k;
@@ -54,7 +54,25 @@ struct SolverState {
   double sweep_ns;
   long long iters, evals_total, inner, fail_iter, sweeps;
   int cur, ig_prev, ig_cur, ig_new, has_sigma0, status, has_metrics, pad;
+  // resumable control (the kernel may exit at an exchange point and resume)
+  double tau, tau_start, slack, sigma, alpha_n, beta_n, phi_new, theta;
+  long long call_done;     // accepted iterations in the current rapdb_run call
+  int step, ret, kret, xkind, evals, rsrc, rwarm, pad2;
 };
+
+// steps of the resumable op state machine
+enum Step {
+  T_BEGIN = 0,
+  TY_DUAL, TY_GXPART, TY_PRIMAL, TY_SWEEP, TY_GLOCAL, TY_GY, TY_DECIDE,
+  TX_PRIMAL, TX_SWEEP, TX_GLOCAL, TX_DUAL, TX_GXPART, TX_NORMS, TX_DECIDE,
+  A_POST, K_GXPART, K_FINISH, A_RESTART, A_END,
+  R_POINT, R_SWEEP, R_GLOCAL, R_CACHE, R_GXPART, R_GXCACHE, R_FINISH,
+  G_CAND, G_GLOCAL, G_HPART, G_SOLVE,
+  P_SWEEP, P_OUT,
+  DONE
+};
+// exchange kinds: what the host must all-reduce (sum) across ranks before resuming
+enum Xkind { X_NONE = 0, X_GX = 1, X_G = 2, X_GX2 = 3, X_H = 4 };
 
 struct DevProblem {
   int n, m, p, k0, k1, nloc, nact, nzero;
@@ -103,6 +121,9 @@ struct RunCfg {
   long long max_iters, budget, stop_total;
   int metrics_every, criterion, has_f_star, fixed_period, fixed_point, warm_tau, stop_at_fixed;
   int op, src, reset_inner, reps;
+  int split;               // exit at exchange points (sharded runs) instead of continuing
+  int resume;              // continue the saved op at st.step
+
   double eps, eps_kkt, eps_feas, f_star;
   double xi, tol;                  // smoothed gap
   const double* warm;              // smoothed gap subsolver warm start (or null)

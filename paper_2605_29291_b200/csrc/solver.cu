@@ -20,85 +20,159 @@ __device__ __forceinline__ void trace_put(const KArgs& K, long long row, int col
   if (K.w.trace) K.w.trace[row * RAPDB_TRACE_COLS + col] = v;
 }
 
-// run_restarted's loop body on device (restarts.py:111-161) around
-// ApdbEngine.step (engine.py:198-259).
-__device__ void op_run(const KArgs& K, Sm& S) {
+// One step of the resumable op state machine (see solver_ops.cuh).  Returns the
+// next step; `xk` is set at exchange points.
+__device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
   SolverState& st = *S.st;
   const RunCfg& rc = K.rc;
-  const DevParams& prm = K.prm;
-  const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
-  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  long long done = 0;
-  int status = ST_LIMIT;
-  for (;;) {
-    double tau = st.tau_cand;
-    const double tau_start = tau;
-    const double slack = 1e-13 * (1.0 + fabs(st.phi_k));
-    int evals = 0, acc = 0;
-    TrialOut o{};
-    for (int t = 0; t <= prm.max_bt; ++t) {
-      const int r = prm.mode == 1 ? trial_xy(K, S, tau, slack, o) : trial_yx(K, S, tau, slack, o);
-      if (r < 0) { status = ST_ABORT; goto out; }
-      ++evals;
-      if (r == 1) { acc = 1; break; }
-      tau *= prm.eta;
-    }
-    if (!acc) {
+  switch (step) {
+    case T_BEGIN:   // ApdbEngine.step entry (engine.py:199-204)
       if (threadIdx.x == 0) {
-        st.fail_tau = tau;
-        st.fail_gamma = st.gamma;
-        st.fail_iter = st.iters;
+        st.tau = st.tau_cand;
+        st.tau_start = st.tau;
+        st.slack = 1e-13 * (1.0 + fabs(st.phi_k));
+        st.evals = 0;
       }
       __syncthreads();
-      status = ST_NONCONV;
-      goto out;
-    }
-    roll(K, S, tau, evals, o);
-    ++done;
-    {
-      const long long total = st.iters;
-      const long long row = done - 1;
-      if (rec) {
-        trace_put(K, row, 0, (double)total);
-        trace_put(K, row, 1, tau_start);
-        trace_put(K, row, 2, tau);
-        trace_put(K, row, 3, o.sigma);
-        trace_put(K, row, 4, st.gamma);
-        trace_put(K, row, 5, (double)evals);
-        trace_put(K, row, 6, (double)st.evals_total);
-        trace_put(K, row, 7, qnan);
-        trace_put(K, row, 8, qnan);
-        trace_put(K, row, 9, qnan);
-        trace_put(K, row, 10, 0.0);
+      return K.prm.mode == 1 ? TX_PRIMAL : TY_DUAL;
+    case TY_DUAL: return ty_dual(K, S);
+    case TY_GXPART: return ty_gxpart(K, S, xk);
+    case TY_PRIMAL: return ty_primal(K, S);
+    case TY_SWEEP: return sweep_sync(K, S, K.w.x + (long long)(st.cur ^ 1) * K.P.n, st.cur ^ 1) ? TY_GLOCAL : kAbort;
+    case TY_GLOCAL: g_local(K, st.cur ^ 1); xk = X_G; return TY_GY;
+    case TY_GY: return ty_gy(K, S);
+    case TY_DECIDE: return ty_decide(K, S);
+    case TX_PRIMAL: return tx_primal(K, S);
+    case TX_SWEEP: return sweep_sync(K, S, K.w.x + (long long)(st.cur ^ 1) * K.P.n, st.cur ^ 1) ? TX_GLOCAL : kAbort;
+    case TX_GLOCAL: g_local(K, st.cur ^ 1); xk = X_G; return TX_DUAL;
+    case TX_DUAL: return tx_dual(K, S);
+    case TX_GXPART: return tx_gxpart(K, S, xk);
+    case TX_NORMS: return tx_norms(K, S);
+    case TX_DECIDE: return tx_decide(K, S);
+    case A_POST: {  // trace row; KKT cadence (restarts.py:115-124)
+      const long long total = st.iters, row = st.call_done - 1;
+      if (blockIdx.x == 0 && threadIdx.x == 0 && K.w.trace) {
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        double* tr = K.w.trace + row * RAPDB_TRACE_COLS;
+        tr[0] = (double)total; tr[1] = st.tau_start; tr[2] = st.tau; tr[3] = st.sigma; tr[4] = st.gamma;
+        tr[5] = (double)st.evals; tr[6] = (double)st.evals_total; tr[7] = qnan; tr[8] = qnan; tr[9] = qnan;
+        tr[10] = 0.0;
       }
-      if (rc.criterion != 0 && rc.metrics_every > 0 &&
-          (total % rc.metrics_every == 0 || total == rc.budget)) {
-        // the trial's last phase wrote partial slots other CTAs may still read
-        if (!gsync(K, S)) { status = ST_ABORT; goto out; }
-        if (!dev_kkt(K, S)) { status = ST_ABORT; goto out; }
-        if (rec) {
-          trace_put(K, row, 7, st.metrics[0]);
-          trace_put(K, row, 8, st.metrics[4]);
-          trace_put(K, row, 9, st.metrics[7]);
-        }
-        if (terminated(rc, st.metrics)) { status = ST_CONVERGED; goto out; }
-      }
-      if (rc.fixed_period > 0 && st.inner >= rc.fixed_period && total < rc.budget) {
-        if (rc.stop_at_fixed) { status = ST_FIXED_DUE; goto out; }
-        if (!gsync(K, S)) { status = ST_ABORT; goto out; }
-        if (!dev_reinit(K, S, rc.fixed_point ? 2 : 1, rc.warm_tau)) { status = ST_ABORT; goto out; }
-        if (threadIdx.x == 0) st.inner = 0;
+      if (rc.criterion != 0 && rc.metrics_every > 0 && (total % rc.metrics_every == 0 || total == rc.budget)) {
+        if (threadIdx.x == 0) st.kret = A_RESTART;
         __syncthreads();
-        if (rec) trace_put(K, row, 10, 1.0);
+        return K_GXPART;
       }
-      if (rc.stop_total > 0 && total == rc.stop_total && total < rc.budget) { status = ST_CHECK_DUE; goto out; }
-      if (total >= rc.budget) { status = ST_BUDGET; goto out; }
-      if (done >= rc.max_iters) { status = ST_LIMIT; goto out; }
+      return A_RESTART;
+    }
+    case K_GXPART: return k_gxpart(K, S, xk);
+    case K_FINISH: {
+      const int nx = k_finish(K, S);
+      if (nx == A_RESTART) {   // inside a run: record and test termination
+        const long long row = st.call_done - 1;
+        if (blockIdx.x == 0 && threadIdx.x == 0 && K.w.trace) {
+          double* tr = K.w.trace + row * RAPDB_TRACE_COLS;
+          tr[7] = st.metrics[0]; tr[8] = st.metrics[4]; tr[9] = st.metrics[7];
+        }
+        if (terminated(rc, st.metrics)) {
+          if (threadIdx.x == 0) st.status = ST_CONVERGED;
+          __syncthreads();
+          return DONE;
+        }
+      }
+      return nx;
+    }
+    case A_RESTART: {   // FixedRestart (restarts.py:126-135)
+      const long long total = st.iters;
+      if (rc.fixed_period > 0 && st.inner >= rc.fixed_period && total < rc.budget) {
+        if (rc.stop_at_fixed) {
+          if (threadIdx.x == 0) st.status = ST_FIXED_DUE;
+          __syncthreads();
+          return DONE;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && K.w.trace)
+          K.w.trace[(st.call_done - 1) * RAPDB_TRACE_COLS + 10] = 1.0;
+        if (threadIdx.x == 0) {
+          st.rsrc = rc.fixed_point ? 2 : 1;
+          st.rwarm = rc.warm_tau;
+          st.ret = A_END;
+          st.inner = 0;
+        }
+        __syncthreads();
+        return gsync(K, S) ? R_POINT : kAbort;
+      }
+      return A_END;
+    }
+    case A_END: {
+      const long long total = st.iters;
+      int status = -1;
+      if (rc.stop_total > 0 && total == rc.stop_total && total < rc.budget) status = ST_CHECK_DUE;
+      else if (total >= rc.budget) status = ST_BUDGET;
+      else if (st.call_done >= rc.max_iters) status = ST_LIMIT;
+      if (status < 0) return T_BEGIN;
+      if (threadIdx.x == 0) st.status = status;
+      __syncthreads();
+      return DONE;
+    }
+    case R_POINT: return r_point(K, S);
+    case R_SWEEP: return r_sweep(K, S);
+    case R_GLOCAL: g_local(K, st.cur ^ 1); xk = X_G; return R_CACHE;
+    case R_CACHE: return r_cache(K, S);
+    case R_GXPART: return r_gxpart(K, S, xk);
+    case R_GXCACHE: return r_gxcache(K, S);
+    case R_FINISH: return r_finish(K, S);
+    case G_CAND: return g_cand(K, S);
+    case G_GLOCAL: g_local(K, st.cur ^ 1); xk = X_G; return G_HPART;
+    case G_HPART: return g_hpart(K, S, xk);
+    case G_SOLVE: return g_solve(K, S);
+    case P_SWEEP: {
+      for (int r = 0; r < max(1, rc.reps); ++r)
+        if (!sweep_sync(K, S, rc.in_x, st.cur ^ 1)) return kAbort;
+      return P_OUT;
+    }
+    case P_OUT: {
+      const DevProblem& P = K.P;
+      for (long long i = gtid(); i <= P.m; i += gstride())
+        rc.out_g[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
+      const double* Up = K.w.U + (long long)(st.cur ^ 1) * P.nloc * P.n;
+      const long long tot = (long long)P.nloc * P.n;
+      for (long long j = gtid(); j < tot; j += gstride()) rc.out_u[j] = ldcg(Up + j);
+      return DONE;
+    }
+    default:
+      return kAbort;
+  }
+}
+
+// Run the state machine until DONE, an abort, or (sharded runs) an exchange.
+__device__ void drive(const KArgs& K, Sm& S) {
+  SolverState& st = *S.st;
+  for (;;) {
+    const int step = st.step;
+    if (step == DONE) return;
+    int xk = X_NONE;
+    const int next = run_step(K, S, step, xk);
+    if (next == kAbort) {
+      if (threadIdx.x == 0) { st.status = ST_ABORT; st.step = DONE; }
+      __syncthreads();
+      return;
+    }
+    if (threadIdx.x == 0) st.step = next;
+    __syncthreads();
+    if (xk != X_NONE) {
+      if (K.rc.split) {   // the host all-reduces the buffer and relaunches
+        if (threadIdx.x == 0) { st.xkind = xk; st.status = ST_EXCHANGE; }
+        __syncthreads();
+        return;
+      }
+      // one rank: the partial is the total; G/H are read by other threads next
+      if ((xk == X_G || xk == X_H) && !gsync(K, S)) {
+        if (threadIdx.x == 0) { st.status = ST_ABORT; st.step = DONE; }
+        __syncthreads();
+        return;
+      }
     }
   }
-out:
-  if (threadIdx.x == 0) st.status = status;
-  __syncthreads();
 }
 
 __device__ void op_get(const KArgs& K, Sm& S) {
@@ -114,17 +188,6 @@ __device__ void op_get(const KArgs& K, Sm& S) {
     const double v = avg ? ldcg(w.ycum + j) / st.T : ldcg(yc + j);
     if (j < p) K.rc.out_v[j] = v; else K.rc.out_lam[j - p] = v;
   }
-}
-
-__device__ void op_probe(const KArgs& K, Sm& S) {
-  const DevProblem& P = K.P;
-  const int par = S.st->cur ^ 1;
-  for (int r = 0; r < max(1, K.rc.reps); ++r)
-    if (!sweep_sync(K, S, K.rc.in_x, par)) return;
-  for (long long i = gtid(); i <= P.m; i += gstride()) K.rc.out_g[i] = g_combine(K, (int)i);
-  const double* Up = K.w.U + (long long)par * P.nloc * P.n;
-  const long long tot = (long long)P.nloc * P.n;
-  for (long long j = gtid(); j < tot; j += gstride()) K.rc.out_u[j] = ldcg(Up + j);
 }
 
 }  // namespace rapdb
@@ -164,32 +227,32 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
       mbar_init(&S.empty[s], 1);   // each ring slot is consumed by exactly one warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (!K.rc.resume) {   // a new op: initial step
+      s_st.status = ST_RUNNING;
+      s_st.xkind = X_NONE;
+      switch (K.rc.op) {
+        case OP_RUN: s_st.step = T_BEGIN; s_st.call_done = 0; break;
+        case OP_REINIT:
+          s_st.step = R_POINT; s_st.ret = DONE; s_st.rsrc = K.rc.src; s_st.rwarm = K.rc.warm_tau;
+          if (K.rc.reset_inner) s_st.inner = 0;
+          break;
+        case OP_KKT: s_st.step = K_GXPART; s_st.kret = DONE; break;
+        case OP_GAP: s_st.step = G_CAND; break;
+        case OP_PROBE: s_st.step = P_SWEEP; break;
+        default: s_st.step = DONE; break;
+      }
+    } else {
+      s_st.status = ST_RUNNING;
+    }
   }
   __syncthreads();
-  switch (K.rc.op) {
-    case OP_RUN:
-      op_run(K, S);
-      break;
-    case OP_REINIT:
-      if (dev_reinit(K, S, K.rc.src, K.rc.warm_tau) && threadIdx.x == 0 && K.rc.reset_inner) s_st.inner = 0;
-      break;
-    case OP_KKT:
-      dev_kkt(K, S);
-      break;
-    case OP_GET:
-      op_get(K, S);
-      break;
-    case OP_PROBE:
-      op_probe(K, S);
-      break;
-    case OP_GAP:
-      dev_gap(K, S);
-      break;
-    default:
-      break;
-  }
+  if (K.rc.op == OP_GET) op_get(K, S);
+  else drive(K, S);
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) *K.w.st = s_st;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (s_st.status == ST_RUNNING) s_st.status = ST_LIMIT;   // op completed
+    *K.w.st = s_st;
+  }
 }
 
 // ========================================================================
@@ -211,6 +274,11 @@ struct rapdb_ctx {
   long long ws_bytes = 0;
   long long stage_cap = 0;  // doubles available in the staging area
   bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
+  int split = 0;            // sharded: stop at exchange points
+  rapdb_exchange_fn xcb = nullptr;
+  void* xuser = nullptr;
+  long long exchanges = 0;
+  SolverState last_st{};
 };
 
 namespace {
@@ -281,8 +349,9 @@ Layout layout_of(const rapdb_ctx* c) {
 
 long long g_launches = 0;
 
-int launch(rapdb_ctx* c, RunCfg rc) {
-  if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
+int read_state(rapdb_ctx* c, SolverState* st);
+
+int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   KArgs K;
   K.P = c->P;
   K.prm = c->prm;
@@ -297,6 +366,29 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   CK(cudaGetLastError());
   ++g_launches;
   return RAPDB_OK;
+}
+
+// Launch an op.  Single-rank contexts run it to completion in one launch
+// (asynchronous).  Sharded contexts ("split") stop at every exchange point:
+// the registered callback all-reduces the buffer rapdb_exchange_buffers names
+// (NCCL over NVLink in the Python binding) and the op resumes in a new launch.
+int launch(rapdb_ctx* c, RunCfg rc) {
+  if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
+  rc.split = c->split;
+  rc.resume = 0;
+  int r = launch_once(c, rc);
+  if (r || !c->split) return r;
+  for (;;) {
+    r = read_state(c, &c->last_st);
+    if (r) return r;
+    if (c->last_st.status != ST_EXCHANGE) return RAPDB_OK;
+    if (!c->xcb) return fail(c, RAPDB_ECONFIG, "sharded context has no exchange callback");
+    if (c->xcb(c->xuser, c->last_st.xkind) != 0) return fail(c, RAPDB_EDEVICE, "exchange callback failed");
+    ++c->exchanges;
+    rc.resume = 1;
+    r = launch_once(c, rc);
+    if (r) return r;
+  }
 }
 
 int read_state(rapdb_ctx* c, SolverState* st) {
@@ -327,6 +419,35 @@ extern "C" {
 int rapdb_abi_version(void) { return 1; }
 
 long long rapdb_launch_count(void) { return g_launches; }
+
+int rapdb_set_exchange(rapdb_ctx* c, rapdb_exchange_fn fn, void* user, int force_split) {
+  if (!c) return RAPDB_EINPUT;
+  c->xcb = fn;
+  c->xuser = user;
+  c->split = (c->nranks > 1 || force_split) ? 1 : 0;
+  return RAPDB_OK;
+}
+
+int rapdb_exchange_buffers(rapdb_ctx* c, int kind, double** b0, long long* n0, double** b1, long long* n1) {
+  if (!c || !b0 || !n0 || !b1 || !n1 || !c->have_ws) return RAPDB_EINPUT;
+  const SolverState& st = c->last_st;
+  const long long n = c->P.n, m = c->P.m;
+  *b1 = nullptr;
+  *n1 = 0;
+  switch (kind) {
+    case X_GX: *b0 = c->w.gxs; *n0 = n; break;
+    case X_G: *b0 = c->w.gval + (long long)(st.cur ^ 1) * (m + 1); *n0 = m + 1; break;
+    case X_GX2:
+      *b0 = c->w.gxs; *n0 = n;
+      *b1 = c->w.gxb + (long long)st.ig_new * n; *n1 = n;
+      break;
+    case X_H: *b0 = c->w.H; *n0 = n * n; break;
+    default: return fail(c, RAPDB_EINPUT, "unknown exchange kind");
+  }
+  return RAPDB_OK;
+}
+
+long long rapdb_exchange_count(const rapdb_ctx* c) { return c ? c->exchanges : -1; }
 
 int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
   if (!out) return RAPDB_EINPUT;
@@ -380,8 +501,9 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   if (n <= 0 || m < 0 || p < 0) return fail(c, RAPDB_EINPUT, "need n > 0, m >= 0, p >= 0");
   if (k0 < 0 || k1 > m + 1 || k1 <= k0) return fail(c, RAPDB_EINPUT, "bad local matrix range");
   if (ld < n || (ld & 1)) return fail(c, RAPDB_EINPUT, "ld must be even and >= n");
-  if (c->nranks != 1 || k0 != 0 || k1 != m + 1)
-    return fail(c, RAPDB_ECONFIG, "constraint sharding across ranks is not enabled in this build");
+  if (c->nranks == 1 && (k0 != 0 || k1 != m + 1) && !c->split)
+    return fail(c, RAPDB_EINPUT, "a single-rank context must hold all m+1 matrices (or be split)");
+  if (c->nranks > 1) c->split = 1;
   if (!Q || !q || !r || !lower || !upper || (p > 0 && (!A || !b)))
     return fail(c, RAPDB_EINPUT, "null data pointer");
   if ((reinterpret_cast<uintptr_t>(Q) & 15) != 0) return fail(c, RAPDB_EINPUT, "Q must be 16-byte aligned");

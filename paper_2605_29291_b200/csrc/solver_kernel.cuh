@@ -422,17 +422,24 @@ __device__ __forceinline__ double g_combine(const KArgs& K, int i) {
 
 // grad_x Phi(x, (v, lam)) at coordinate j from the U-cache (problem.py:207-217):
 // (u_0 + q_0) then, in i order, + lam_i (u_i + q_i) for lam_i != 0, then + A^T v.
-__device__ __forceinline__ double recombine(const KArgs& K, const double* Upar, const double* lam_s,
-                                            const double* v_s, long long j) {
+// This rank's share of sum_i w_i (u_i + q_i) over its local matrices
+// [k0, k1) (w_0 = 1, w_i = lam_i); the rank holding Q_0 starts from u_0 + q_0.
+// With one rank this is the whole sum in the reference's i order.
+__device__ __forceinline__ double recombine_local(const KArgs& K, const double* Upar, const double* lam_s,
+                                                  long long j) {
   const DevProblem& P = K.P;
   const long long n = P.n;
-  double acc = ldcg(Upar + j) + __ldg(P.q + j);
-  int i = 1;
-  for (; i + 3 <= P.m; i += 4) {
+  double acc = 0.0;
+  int i = P.k0;
+  if (i == 0) {
+    acc = ldcg(Upar + j) + __ldg(P.q + j);
+    i = 1;
+  }
+  for (; i + 3 < P.k1; i += 4) {
     double u[4], qq[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      u[k] = ldcg(Upar + (long long)(i + k) * n + j);
+      u[k] = ldcg(Upar + (long long)(i + k - P.k0) * n + j);
       qq[k] = __ldg(P.q + (long long)(i + k) * n + j);
     }
 #pragma unroll
@@ -442,15 +449,25 @@ __device__ __forceinline__ double recombine(const KArgs& K, const double* Upar, 
       acc = (l != 0.0) ? acc + t : acc;
     }
   }
-  for (; i <= P.m; ++i) {
+  for (; i < P.k1; ++i) {
     const double l = lam_s[i - 1];
-    if (l != 0.0) acc = acc + l * (ldcg(Upar + (long long)i * n + j) + __ldg(P.q + (long long)i * n + j));
+    if (l != 0.0) acc = acc + l * (ldcg(Upar + (long long)(i - P.k0) * n + j) + __ldg(P.q + (long long)i * n + j));
   }
-  if (P.p > 0) {
-    double t = 0.0;
-    for (int l = 0; l < P.p; ++l) t = t + __ldg(P.A + (long long)l * n + j) * v_s[l];
-    acc = acc + t;
-  }
+  return acc;
+}
+
+// (A^T v)_j, added after the cross-rank sum (problem.py:215-216)
+__device__ __forceinline__ double atv(const KArgs& K, const double* v_s, long long j) {
+  double t = 0.0;
+  for (int l = 0; l < K.P.p; ++l) t = t + __ldg(K.P.A + (long long)l * K.P.n + j) * v_s[l];
+  return t;
+}
+
+// full grad_x Phi for a single rank (no exchange): recombination then A^T v
+__device__ __forceinline__ double recombine(const KArgs& K, const double* Upar, const double* lam_s,
+                                            const double* v_s, long long j) {
+  double acc = recombine_local(K, Upar, lam_s, j);
+  if (K.P.p > 0) acc = acc + atv(K, v_s, j);
   return acc;
 }
 

@@ -100,7 +100,9 @@ class ApdbEngine:
     ergodic sums) is resident on the GPU."""
 
     def __init__(self, inst: ProblemInstance, config: SolverConfig, z_init: Iterate,
-                 keep_iterates: bool = False, device=None):
+                 keep_iterates: bool = False, device=None, shard=None):
+        """``shard`` (sharding.Shard): hold only matrices [k0, k1) and all-reduce
+        the per-trial partials with the other ranks."""
         inst.check_device_support()
         self.inst = inst
         self.config = cfg = config.resolved()
@@ -109,10 +111,18 @@ class ApdbEngine:
         self.keep_iterates = keep_iterates
         self.trace: List[TraceRecord] = []
         self.iterates: List[Iterate] = []
+        self.shard = shard
         idx = _device_index(device)
-        self._ctx = _capi.Context(idx)
-        self._data = inst.device_data(self._ctx.device)
-        self._ctx.bind(self._data, cfg)
+        if shard is None:
+            self._ctx = _capi.Context(idx)
+            self._data = inst.device_data(self._ctx.device)
+            self._ctx.bind(self._data, cfg)
+        else:
+            self._ctx = _capi.Context(idx, shard.rank, shard.nranks)
+            ctx = self._ctx
+            ctx.set_exchange(lambda kind: shard.exchange(ctx.exchange_views(kind)), force_split=shard.split)
+            self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1))
+            ctx.bind(self._data, cfg, shard.k0, shard.k1)
         self._trace_buf = None
         self._res = None
         self.iters = 0

@@ -148,16 +148,18 @@ class ProblemInstance:
         if not isinstance(self.cone, NonnegOrthant):
             raise ConfigurationError("the device path supports the nonnegative orthant cone")
 
-    def device_data(self, device=None, pinned_host=None):
-        """Upload (cached per device).  ``pinned_host``: optional pinned torch copy
-        of the Q stack to copy from (benchmark e2e path)."""
+    def device_data(self, device=None, pinned_host=None, krange=None):
+        """Upload (cached per device and matrix range).  ``pinned_host``: optional
+        pinned torch copy of the Q stack; ``krange=(k0, k1)``: upload only the
+        matrices of one constraint shard."""
         import torch
         dev = torch.device("cuda", 0) if device is None else torch.device(device)
-        key = str(dev)
+        k0, k1 = krange if krange is not None else (0, self.m + 1)
+        key = str(dev) if (k0, k1) == (0, self.m + 1) else f"{dev}[{k0}:{k1}]"
         cache = self._dev
         if key not in cache:
             src = pinned_host if pinned_host is not None else cache.get("_pinned")
-            cache[key] = DeviceData.upload(self, dev, src)
+            cache[key] = DeviceData.upload(self, dev, src, k0, k1)
         return cache[key]
 
     def pin_host(self):
@@ -205,16 +207,17 @@ class DeviceData:
         self.__dict__.update(kw)
 
     @classmethod
-    def upload(cls, inst: ProblemInstance, device, pinned_host=None):
+    def upload(cls, inst: ProblemInstance, device, pinned_host=None, k0=0, k1=None):
         import torch
         n, m, p = inst.n, inst.m, inst.p
+        k1 = m + 1 if k1 is None else k1
         ld = n + (n & 1)
-        zero = np.array([not np.any(inst.Q[i]) for i in range(m + 1)], dtype=np.uint8)
-        src = pinned_host if pinned_host is not None else torch.from_numpy(inst.Q)
+        zero = np.array([not np.any(inst.Q[i]) for i in range(k0, k1)], dtype=np.uint8)
+        src = (pinned_host if pinned_host is not None else torch.from_numpy(inst.Q))[k0:k1]
         if ld == n:
             Qd = src.to(device, non_blocking=pinned_host is not None)
         else:
-            Qd = torch.zeros((m + 1, n, ld), dtype=torch.float64, device=device)
+            Qd = torch.zeros((k1 - k0, n, ld), dtype=torch.float64, device=device)
             Qd[:, :, :n].copy_(src, non_blocking=pinned_host is not None)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
         lo = inst.primal_set.lower

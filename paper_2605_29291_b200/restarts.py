@@ -95,7 +95,11 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
                   budget: int = 50_000,
                   criteria: Optional[diagnostics.TerminationCriteria] = None,
                   metrics_every: int = 10, warm_tau: bool = False,
-                  record_restart_points: bool = False, device=None) -> RunResult:
+                  record_restart_points: bool = False, device=None, shard=None) -> RunResult:
+    """restarts.py:82-170.  Extra keyword arguments (not in the reference):
+    ``device`` picks the GPU; ``shard`` (sharding.Shard, e.g. from
+    ``sharding.nccl_shard(inst)`` in a torchrun job) shards the constraints over
+    ranks -- every rank calls run_restarted with the same arguments."""
     if budget < 1:
         raise ConfigurationError("budget must be >= 1")
     if policy is None:
@@ -104,7 +108,7 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
     crit_code = 0 if criteria is None else criteria.code()
     if z_init is None:
         z_init = initial_iterate(inst, config.dual_ball)
-    engine = ApdbEngine(inst, config, z_init, device=device)
+    engine = ApdbEngine(inst, config, z_init, device=device, shard=shard)
     restart_log: List[RestartEvent] = []
     outer = 0
     inner = 0

@@ -1,0 +1,133 @@
+"""Constraint sharding across GPUs.
+
+Rank r holds matrices ``[k0, k1)`` of the m+1 quadratic forms (Q_0 counts as
+rank 0's work); x, the multipliers and all vectors are replicated.  Every
+backtracking trial exchanges (all-reduce, sum) one n-vector -- this rank's
+share of ``sum_i w_i (u_i + q_i)`` -- and one (m+1)-vector of constraint values
+(exact: disjoint supports); the accept/reject decision is then computed
+identically on every rank, so the host control flow stays in lockstep without
+further communication.  The smoothed gap adds one exchange of H (n x n) per
+adaptive check.
+
+* ``nccl_shard(inst)``: the production path -- one process per GPU,
+  ``torch.distributed`` with the NCCL backend, all-reduces over NVLink/NVSwitch.
+* ``EmulatedCluster``: R shards of one instance on ONE GPU, driven by R host
+  threads that meet at each exchange (the kernels never wait on each other:
+  each launch ends at the exchange point).  Used by the tests.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+
+@dataclass
+class Shard:
+    rank: int
+    nranks: int
+    k0: int
+    k1: int
+    exchange: Optional[Callable[[list], None]] = None   # all-reduce(sum) of a list of device tensors
+    force_split: bool = False
+    name: str = ""
+
+    @property
+    def split(self) -> bool:
+        return self.nranks > 1 or self.force_split
+
+
+def plan(m: int, nranks: int, zero_flags: Optional[Sequence[bool]] = None) -> List[Tuple[int, int]]:
+    """Contiguous ranges of the m+1 matrices, balanced by streamed (non-zero)
+    matrices; every rank gets at least one matrix when m+1 >= nranks."""
+    total = m + 1
+    if nranks < 1 or nranks > total:
+        raise ValueError(f"cannot shard {total} matrices over {nranks} ranks")
+    cost = np.ones(total) if zero_flags is None else np.where(np.asarray(zero_flags, bool), 0.05, 1.0)
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    bounds = [0]
+    for r in range(1, nranks):
+        target = cum[-1] * r / nranks
+        k = int(np.searchsorted(cum, target, side="left"))
+        k = max(k, bounds[-1] + 1)
+        k = min(k, total - (nranks - r))
+        bounds.append(k)
+    bounds.append(total)
+    return [(bounds[r], bounds[r + 1]) for r in range(nranks)]
+
+
+def nccl_shard(inst, group=None) -> Shard:
+    """This process's shard for the current torch.distributed (NCCL) group."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    zero = [not np.any(inst.Q[i]) for i in range(inst.m + 1)]
+    k0, k1 = plan(inst.m, world, zero)[rank]
+
+    def allreduce(views):
+        for v in views:
+            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+
+    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl")
+
+
+class EmulatedCluster:
+    """R shards on one GPU: one host thread per rank, a rank-ordered sum at each
+    exchange (rank 0 adds the R buffers in rank order and writes the total back)."""
+
+    def __init__(self, nranks: int):
+        self.R = nranks
+        self.barrier = threading.Barrier(nranks)
+        self.slots: List[Optional[list]] = [None] * nranks
+        self.error: Optional[BaseException] = None
+
+    def shards(self, inst) -> List[Shard]:
+        zero = [not np.any(inst.Q[i]) for i in range(inst.m + 1)]
+        out = []
+        for r, (k0, k1) in enumerate(plan(inst.m, self.R, zero)):
+            out.append(Shard(rank=r, nranks=self.R, k0=k0, k1=k1, force_split=True, name="emulated",
+                             exchange=(lambda views, rr=r: self._exchange(rr, views))))
+        return out
+
+    def _exchange(self, rank, views):
+        import torch
+        self.slots[rank] = views
+        self.barrier.wait()
+        if rank == 0:
+            for i in range(len(views)):
+                tot = self.slots[0][i].clone()
+                for r in range(1, self.R):
+                    tot += self.slots[r][i]
+                for r in range(self.R):
+                    self.slots[r][i].copy_(tot)
+            torch.cuda.synchronize()
+        self.barrier.wait()
+
+    def run(self, inst, fn):
+        """fn(shard) on every rank in parallel threads; returns the per-rank results."""
+        shards = self.shards(inst)
+        results: List = [None] * self.R
+        errors: List = [None] * self.R
+
+        def body(r):
+            try:
+                results[r] = fn(shards[r])
+            except BaseException as exc:   # noqa: BLE001 -- re-raised below
+                errors[r] = exc
+                self.barrier.abort()
+
+        threads = [threading.Thread(target=body, args=(r,)) for r in range(self.R)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errors:
+            if e is not None and not isinstance(e, threading.BrokenBarrierError):
+                raise e
+        for e in errors:
+            if e is not None:
+                raise e
+        return results

@@ -1,0 +1,100 @@
+"""Constraint-sharded execution on one GPU.
+
+* forced "split" mode with one rank stops at every exchange point and resumes in
+  a new launch -- it must be bit-identical to the fused single-launch path;
+* R emulated shards (one context per shard, host threads meeting at each
+  exchange, rank-ordered sums) must reproduce the reference's accepted step
+  sizes and iterates like the unsharded path.
+The multi-process NCCL transport itself is exercised by tests/test_sharding_gloo.py
+(the same exchange protocol over torch.distributed, gloo on CPU).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+import paper_2605_29291_b200 as R
+from paper_2605_29291_b200 import instances
+from paper_2605_29291_b200.sharding import EmulatedCluster, Shard
+from test_gpu_parity import TAU, crit, inst_from, rel, trace_arr
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve(inst, shard=None, mode="yx", nm=True, policy=None, budget=300, eps=None):
+    return R.run_restarted(inst, R.SolverConfig(mode=mode, nonmonotone=nm), policy or R.FixedRestart(40),
+                           budget=budget, criteria=crit(eps), shard=shard)
+
+
+@pytest.mark.parametrize("mode,policy", [("yx", "fixed"), ("xy", "fixed"), ("yx", "adaptive")])
+def test_split_single_rank_is_bitwise_identical(mode, policy):
+    arr = instances.dense_qcqp(150, 9, 12, seed=4)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    pol = R.FixedRestart(40) if policy == "fixed" else R.AdaptiveRestart(warmup=30, check_period=60)
+    fused = _solve(inst, None, mode, True, pol, 300, 1e-9)
+    calls = []
+    shard = Shard(rank=0, nranks=1, k0=0, k1=arr.m + 1, force_split=True,
+                  exchange=lambda views: calls.append(len(views)))
+    split = _solve(inst, shard, mode, True, pol, 300, 1e-9)
+    assert calls, "split mode never reached an exchange point"
+    np.testing.assert_array_equal(trace_arr(split.trace)[:, :7], trace_arr(fused.trace)[:, :7])
+    np.testing.assert_array_equal(split.solution.x, fused.solution.x)
+    np.testing.assert_array_equal(split.solution.lam, fused.solution.lam)
+    assert [e.iteration for e in split.restart_log] == [e.iteration for e in fused.restart_log]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("key,mode,nm", [("yx_mono", "yx", False), ("yx_nm", "yx", True), ("xy_nm", "xy", True)])
+def test_emulated_shards_small_qcqp(nranks, key, mode, nm):
+    g = load_golden("small_qcqp")
+    inst = inst_from(g["Q"], g["q"], g["r"], g["lower"], g["upper"])
+    cluster = EmulatedCluster(nranks)
+
+    def body(shard):
+        eng = R.ApdbEngine(inst, R.SolverConfig(mode=mode, nonmonotone=nm), R.initial_iterate(inst), shard=shard)
+        eng.run_block(200)
+        return trace_arr(eng.trace), eng.last
+
+    outs = cluster.run(inst, body)
+    for tr, z in outs:
+        np.testing.assert_array_equal(tr[:, TAU], g[f"{key}/trace"][:200, TAU])
+        assert rel(z.x, g[f"{key}/snap_x"][-1]) <= 1e-9
+        assert rel(z.lam, g[f"{key}/snap_lam"][-1]) <= 1e-9
+    for tr, z in outs[1:]:      # replicas agree bit for bit
+        np.testing.assert_array_equal(z.x, outs[0][1].x)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_emulated_shards_c0_restarts_and_kkt(nranks):
+    g = load_golden("c0")
+    arr = instances.config_instance("C0")
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    cluster = EmulatedCluster(nranks)
+
+    def body(shard):
+        return R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=False), R.NoRestart(),
+                               budget=50000, criteria=crit(1e-6), shard=shard)
+
+    for res in cluster.run(inst, body):
+        tr = trace_arr(res.trace)
+        np.testing.assert_array_equal(tr[:200, TAU], g["mono_none/trace"][:200, TAU])
+        assert res.converged and res.iterations == int(g["mono_none/iterations"])
+        assert abs(res.metrics.f_value - g["mono_none/metrics"][5]) <= 1e-9 * abs(g["mono_none/metrics"][5])
+
+
+def test_emulated_shards_adaptive_gap():
+    g = load_golden("small_qcqp")
+    inst = inst_from(g["Q"], g["q"], g["r"], g["lower"], g["upper"])
+    cluster = EmulatedCluster(2)
+
+    def body(shard):
+        return R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True),
+                               R.AdaptiveRestart(warmup=50, check_period=100), budget=1500,
+                               criteria=crit(1e-8), shard=shard)
+
+    ref_it = list(g["yx_nm_ada/restart_iters"])
+    ref_gaps = g["yx_nm_ada/restart_gaps"]
+    meaningful = [it for it, (gn, gr) in zip(ref_it, ref_gaps) if gr > 1e-8]
+    for res in cluster.run(inst, body):
+        np.testing.assert_array_equal(trace_arr(res.trace)[:200, TAU], g["yx_nm_ada/trace"][:200, TAU])
+        assert [e.iteration for e in res.restart_log][:len(meaningful)] == meaningful
