@@ -6,8 +6,11 @@ CLI's rapdb-yx policy (``FixedRestart(500)``, cli.py:90-107) and monotone
 backtracking (the variant that converges on C1; the non-monotone variant is
 timed on a fixed 1000-iteration budget and reported under ``nonmonotone``).
 
-* ``value``        accepted iterations / s, Q stack resident in HBM (N ranks:
-                   sum over ranks, each rank an independent replica: replicas only).
+* ``value``        accepted iterations / s, Q stack resident in HBM.  N ranks
+                   (torchrun): the constraints are sharded over the GPUs and each
+                   trial all-reduces one n-vector and one (m+1)-vector over NCCL
+                   (``scaling: strong``, one solve); ``--replicas`` runs
+                   independent replicas instead (``scaling: weak``).
 * ``ms_per_step``  = time-to-1e-6-KKT of one solve.
 * ``e2e``          the same solve through the public API with the instance on
                    the HOST: pinned H2D of the 6.4 GB Q stack + vectors, solve,
@@ -48,6 +51,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with N>1: independent replicas instead of constraint sharding")
+    ap.add_argument("--shard", action="store_true",
+                    help="force the constraint-sharded (NCCL exchange) path even with one rank")
     ap.add_argument("--cpu-sample-iters", type=int, default=2)
     ap.add_argument("--skip-cpu", action="store_true")
     return ap.parse_args()
@@ -116,6 +123,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+_RESULT_OUT = None
+
+
+def emit(out):
+    """The one JSON result line, on the original stdout (library chatter such
+    as NCCL's version banner is routed to stderr)."""
+    stream = _RESULT_OUT if _RESULT_OUT is not None else sys.stdout
+    stream.write(json.dumps(out) + "\n")
+    stream.flush()
+
+
+def _claim_stdout():
+    global _RESULT_OUT
+    sys.stdout.flush()
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -180,20 +205,29 @@ def run_reference(args):
            "config": config_block(arr, args.config, "yx monotone, per-step sample of accepted iterations"),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def main():
     args = parse()
+    _claim_stdout()
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
     ws, rank, local = dist_env()
-    if ws > 1:
+    sharded = (ws > 1 and not args.replicas) or args.shard
+    os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
+    if ws > 1 or args.shard:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if not dist.is_initialized():
+            if ws == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29511")
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
+            dist.init_process_group("nccl")
     else:
         dist = None
         torch.cuda.set_device(0)
@@ -201,15 +235,22 @@ def main():
 
     import paper_2605_29291_b200 as R
     from paper_2605_29291_b200 import _capi, instances
+    from paper_2605_29291_b200.sharding import nccl_shard
 
     arr = instances.config_instance(args.config)
     inst = R.ProblemInstance.from_arrays(arr, validate=False)
     cfg = R.SolverConfig(mode="yx", nonmonotone=False)
     pol = R.FixedRestart(500)
     crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
+    shard = None
+    if sharded:
+        shard = nccl_shard(inst)
+        shard.force_split = True
+    krange = None if shard is None else (shard.k0, shard.k1)
 
     def solve(c=cfg, budget=50_000, criteria=crit):
-        return R.run_restarted(inst, c, pol, budget=budget, criteria=criteria, metrics_every=10, device=dev)
+        return R.run_restarted(inst, c, pol, budget=budget, criteria=criteria, metrics_every=10, device=dev,
+                               shard=shard)
 
     def barrier():
         if dist is not None:
@@ -230,7 +271,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    inst.device_data(dev)
+    inst.device_data(dev, krange=krange)
     for _ in range(args.warmup):
         solve()
 
@@ -249,7 +290,8 @@ def main():
     clk = clocks.stop()
     t_ms = max_over_ranks(ev0.elapsed_time(ev1))
     iters_local = sum(r.iterations for r in results)
-    iters_all = sum_over_ranks(iters_local)
+    # sharded: every rank runs the same solve (strong scaling); replicas: sum
+    iters_all = iters_local if sharded else sum_over_ranks(iters_local)
     value = iters_all / (t_ms / 1e3)
     conv = all(r.converged for r in results)
     st = results[-1].device_stats
@@ -262,16 +304,19 @@ def main():
     peak, peak_src = measured_peak()
 
     # standalone sweep launch (one kernel launch = one fused sweep), CUDA events
-    ev = inst._evaluator()
-    xprobe = torch.from_numpy(np.asarray(results[-1].solution.x)).to(dev)
-    ev.ctx.probe_sweep(xprobe, reps=1)
-    _, _, probe_ms = ev.ctx.probe_sweep(xprobe, reps=10)
+    probe_ms = None
+    if shard is None:
+        ev = inst._evaluator()
+        xprobe = torch.from_numpy(np.asarray(results[-1].solution.x)).to(dev)
+        ev.ctx.probe_sweep(xprobe, reps=1)
+        _, _, probe_ms = ev.ctx.probe_sweep(xprobe, reps=10)
 
     # ---- e2e through the public API with host-resident inputs -----------
     inst.pin_host()
     inst.drop_device_data()
     torch.cuda.synchronize()
-    h2d = inst.Q.nbytes + inst.q.nbytes + inst.r.nbytes + 2 * arr.n * 8 + inst.A.nbytes + inst.b.nbytes
+    q_bytes = inst.Q.nbytes if shard is None else inst.Q[shard.k0:shard.k1].nbytes
+    h2d = q_bytes + inst.q.nbytes + inst.r.nbytes + 2 * arr.n * 8 + inst.A.nbytes + inst.b.nbytes
     e2e_iters, e2e_s, d2h = 0, 0.0, 0
     for _ in range(args.steps):
         inst.drop_device_data()
@@ -285,10 +330,10 @@ def main():
         d2h = (2 * (arr.n + arr.m + arr.p) * 8 + r.device_stats["run_launches"] * 0
                + r.iterations * 11 * 8 + 8 * 8)
     e2e_s = max_over_ranks(e2e_s)
-    e2e_value = sum_over_ranks(e2e_iters) / e2e_s
+    e2e_value = (e2e_iters if sharded else sum_over_ranks(e2e_iters)) / e2e_s
 
     # non-monotone variant: fixed 1000-iteration budget (it/s only)
-    inst.device_data(dev)
+    inst.device_data(dev, krange=krange)
     nm_cfg = R.SolverConfig(mode="yx", nonmonotone=True)
     torch.cuda.synchronize()
     tn = time.perf_counter()
@@ -316,10 +361,12 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded CounterRng, BASELINE config 1 shapes; random instance, no dataset)",
             "config": config_block(arr, args.config, "yx monotone + FixedRestart(500) (rapdb-yx)",
-                                   {"parallelism": "replicas only" if ws > 1 else "single GPU",
+                                   {"parallelism": (f"constraint-sharded over {ws} GPU(s), NCCL all-reduce per trial"
+                                                    if sharded else ("replicas only" if ws > 1 else "single GPU")),
+                                    "shard_range": None if shard is None else [shard.k0, shard.k1],
                                     "iterations_per_solve": results[-1].iterations,
                                     "evals_per_solve": results[-1].evals, "converged": conv,
                                     "final_kkt": results[-1].metrics.kkt_residual}),
@@ -330,7 +377,7 @@ def main():
                          "bytes_per_launch_def": "sweeps x (m+1) n^2 8 B",
                          "sweep_phase_gbs": sweep_phase_gbs,
                          "standalone_sweep_ms": probe_ms,
-                         "standalone_sweep_gbs": sweep_bytes / (probe_ms / 1e3) / 1e9,
+                         "standalone_sweep_gbs": None if probe_ms is None else sweep_bytes / (probe_ms / 1e3) / 1e9,
                          "frac_of_8tbs": achieved / 8000.0},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -340,7 +387,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist is not None:
         dist.destroy_process_group()
 
