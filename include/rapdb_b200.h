@@ -100,6 +100,10 @@ int rapdb_exchange_buffers(rapdb_ctx* ctx, int kind, double** buf0, long long* c
 /* number of exchanges performed by this context so far */
 long long rapdb_exchange_count(const rapdb_ctx* ctx);
 
+/* cumulative device time (ns, CTA 0 globaltimer) and call counts per step of
+ * the op state machine (step ids: rapdb_dev.cuh enum Step), for profiling */
+int rapdb_step_profile(rapdb_ctx* ctx, double* ns, long long* counts, int nsteps);
+
 /* version of the ABI (bumped on incompatible change) */
 int rapdb_abi_version(void);
 

@@ -46,7 +46,13 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
-           "rapdb_exchange_count"]
+           "rapdb_exchange_count", "rapdb_step_profile"]
+
+STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
+              "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
+              "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
+              "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
+              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT"]
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
@@ -90,6 +96,7 @@ def load(path: str = LIB_PATH):
                                            C.POINTER(C.c_void_p), C.POINTER(LL)]
     lib.rapdb_exchange_count.argtypes = [P]
     lib.rapdb_exchange_count.restype = LL
+    lib.rapdb_step_profile.argtypes = [P, C.POINTER(D), C.POINTER(LL), I]
     _lib = lib
     return lib
 
@@ -177,6 +184,13 @@ class Context:
 
     def exchange_count(self):
         return int(self.lib.rapdb_exchange_count(self.h))
+
+    def step_profile(self):
+        """{step name: (total device ms, calls)} accumulated since bind."""
+        ns = (C.c_double * 40)()
+        cnt = (C.c_longlong * 40)()
+        self._check(self.lib.rapdb_step_profile(self.h, ns, cnt, 40))
+        return {name: (ns[i] / 1e6, int(cnt[i])) for i, name in enumerate(STEP_NAMES) if cnt[i]}
 
     # -- binding -----------------------------------------------------------
     def bind(self, data, cfg, k0=0, k1=None):

@@ -58,6 +58,8 @@ struct SolverState {
   double tau, tau_start, slack, sigma, alpha_n, beta_n, phi_new, theta;
   long long call_done;     // accepted iterations in the current rapdb_run call
   int step, ret, kret, xkind, evals, rsrc, rwarm, pad2;
+  double step_ns[40];      // device time per state-machine step (CTA 0, globaltimer)
+  long long step_cnt[40];
 };
 
 // steps of the resumable op state machine

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -84,7 +86,9 @@ __device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
     }
     case A_RESTART: {   // FixedRestart (restarts.py:126-135)
       const long long total = st.iters;
-      if (rc.fixed_period > 0 && st.inner >= rc.fixed_period && total < rc.budget) {
+      const bool due = rc.fixed_period > 0 && st.inner >= rc.fixed_period && total < rc.budget;
+      __syncthreads();   // every thread has read st.inner before thread 0 resets it below
+      if (due) {
         if (rc.stop_at_fixed) {
           if (threadIdx.x == 0) st.status = ST_FIXED_DUE;
           __syncthreads();
@@ -149,9 +153,30 @@ __device__ void drive(const KArgs& K, Sm& S) {
   SolverState& st = *S.st;
   for (;;) {
     const int step = st.step;
+    // All shared state (st, in shared memory) is written by thread 0 only, and
+    // every write is separated from the other threads' reads by a barrier: here,
+    // nobody may overwrite st.step (end of this iteration) before all threads
+    // have read it -- a step without an internal barrier let thread 0 race
+    // ahead and split the CTA across two steps (a bar.sync deadlock).
+    __syncthreads();
     if (step == DONE) return;
     int xk = X_NONE;
+    unsigned long long t0 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer();
+    if (threadIdx.x == 0) {   // progress beacon, readable by the host while the kernel runs
+      volatile int* bcn = K.w.abort_flag + 32 + 4 * blockIdx.x;
+      bcn[0] = step;
+      bcn[1] = (int)S.gen;
+      bcn[2] = (int)st.call_done;
+      bcn[3] = (int)S.pseq;
+    }
     const int next = run_step(K, S, step, xk);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && step < 40) {
+      const unsigned long long t1 = globaltimer();
+      if (t1 > t0) st.step_ns[step] += (double)(t1 - t0);
+      st.step_cnt[step] += 1;
+    }
+    __syncthreads();   // the step's reads of st are done before thread 0 writes below
     if (next == kAbort) {
       if (threadIdx.x == 0) { st.status = ST_ABORT; st.step = DONE; }
       __syncthreads();
@@ -336,7 +361,7 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_HY] = n * 8;
   sz[B_ST] = sizeof(SolverState);
   sz[B_BAR] = 64;
-  sz[B_ABORT] = 128;
+  sz[B_ABORT] = 128 + 16LL * G;   // flag + diagnostics + per-CTA progress beacons
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -391,8 +416,51 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   }
 }
 
+// The host side of the watchdog: if an op does not finish within 120 s, read
+// the per-CTA progress beacons over a non-blocking stream (the kernel is still
+// resident) and fail with them instead of blocking forever.
+int wait_stream(rapdb_ctx* c) {
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      return cuda_fail(c, q, "kernel");
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+      cudaStream_t ds;
+      std::vector<int> b(4 * c->G + 32, -1);
+      if (cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) == cudaSuccess) {
+        cudaMemcpyAsync(b.data(), c->w.abort_flag, b.size() * sizeof(int), cudaMemcpyDeviceToHost, ds);
+        cudaStreamSynchronize(ds);
+      }
+      std::string msg = "op did not finish within 120 s (device hang); per-CTA step/gen/iter/pseq:";
+      for (int i = 0; i < c->G; ++i) {
+        const int* v = b.data() + 32 + 4 * i;
+        char t[64];
+        std::snprintf(t, sizeof t, " %d:%d/%d/%d/%d", i, v[0], v[1], v[2], v[3]);
+        msg += t;
+      }
+      std::fprintf(stderr, "[rapdb] %s\n", msg.c_str());
+      c->err = msg;
+      return RAPDB_EDEVICE;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
+  cudaEventDestroy(ev);
+  return RAPDB_OK;
+}
+
 int read_state(rapdb_ctx* c, SolverState* st) {
   int ab = 0;
+  {
+    const int wr = wait_stream(c);   // poll first: a pageable D2H copy would block behind a hung kernel
+    if (wr) return wr;
+  }
   CK(cudaMemcpyAsync(st, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -448,6 +516,18 @@ int rapdb_exchange_buffers(rapdb_ctx* c, int kind, double** b0, long long* n0, d
 }
 
 long long rapdb_exchange_count(const rapdb_ctx* c) { return c ? c->exchanges : -1; }
+
+int rapdb_step_profile(rapdb_ctx* c, double* ns, long long* counts, int nsteps) {
+  if (!c || !ns || !counts || !c->have_ws) return RAPDB_EINPUT;
+  SolverState st;
+  int r = read_state(c, &st);
+  if (r) return r;
+  for (int i = 0; i < nsteps && i < 40; ++i) {
+    ns[i] = st.step_ns[i];
+    counts[i] = st.step_cnt[i];
+  }
+  return RAPDB_OK;
+}
 
 int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
   if (!out) return RAPDB_EINPUT;
