@@ -104,6 +104,8 @@ struct SweepPlan {
   int ncw;               // consumer warps used by the sweep (<= nstages)
   int cpr;               // column chunks per row (> 1: rows wider than a stage)
   int chunk;             // doubles per chunk (== ld when cpr == 1)
+  int rc_cols;           // gradient recombination by CTA column blocks (many matrices)
+  int pad3;
   long long stage_bytes; // per ring slot (multiple of 128)
   long long rows_total;  // nact * n
   long long xs_bytes;    // x staging bytes (multiple of 128)

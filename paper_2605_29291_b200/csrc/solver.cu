@@ -190,8 +190,9 @@ __device__ void drive(const KArgs& K, Sm& S) {
         __syncthreads();
         return;
       }
-      // one rank: the partial is the total; G/H are read by other threads next
-      if ((xk == X_G || xk == X_H) && !gsync(K, S)) {
+      // one rank: the partial is the total; G/H (and column-block gradients) are
+      // read by other threads next
+      if ((xk == X_G || xk == X_H || K.sp.rc_cols) && !gsync(K, S)) {
         if (threadIdx.x == 0) { st.status = ST_ABORT; st.step = DONE; }
         __syncthreads();
         return;
@@ -228,7 +229,9 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
   __shared__ int s_flag[4];
   __shared__ unsigned s_prog[kConsumerWarps];
   __shared__ unsigned s_tag[32], s_rel[32];
+  __shared__ double s_rc[kWarps][32];
   Sm S;
+  S.rc = s_rc;
   S.prog = s_prog;
   S.tag = s_tag;
   S.rel = s_rel;
@@ -629,7 +632,12 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
     sp.stage_bytes = align_up((long long)sp.chunk * 8, 128);
   }
   sp.xs_bytes = align_up(row_bytes, 128);
-  const long long static_smem = 8 * (kWarps * 8 + NSLOT + 4 + 2 * kMaxTR * 8) + (long long)sizeof(SolverState) + 64;
+  const char* env_rc = std::getenv("RAPDB_RC_COLS");
+  sp.rc_cols = env_rc ? std::atoi(env_rc) : (k1 - k0 >= 24 ? 1 : 0);
+  cudaFuncAttributes fa{};
+  long long static_smem = 16384;
+  if (cudaFuncGetAttributes(&fa, (const void*)rapdb_solver_kernel) == cudaSuccess)
+    static_smem = (long long)fa.sharedSizeBytes;
   const long long budget = (long long)c->optin - static_smem - 2048;
   long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
   ns = std::min(ns, max_stages);

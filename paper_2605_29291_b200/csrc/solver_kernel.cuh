@@ -35,6 +35,7 @@ struct Sm {
   volatile unsigned* prog; // [8] units consumed per consumer warp in the current sweep
   volatile unsigned* tag;  // [32] sequence number of the tile last issued into each slot
   volatile unsigned* rel;  // [32] sequence number of the tile last released from each slot
+  double (*rc)[32];        // [kWarps][32] chunk partials of recombine_cols
   unsigned long long gen;  // grid-barrier generation (thread 0)
   unsigned pseq;           // pipeline sequence (producer lane / consumers)
 };
@@ -420,6 +421,35 @@ __device__ __forceinline__ double g_combine(const KArgs& K, int i) {
   return 0.5 * sxu + sqx + __ldg(P.r + i);
 }
 
+// The same value computed by a whole warp (every lane gets it): the (CTA, warp)
+// segment partials are spread over the lanes and butterfly-reduced -- a fixed
+// order, so the bits do not depend on timing.
+__device__ __forceinline__ double g_combine_warp(const KArgs& K, int i) {
+  const DevProblem& P = K.P;
+  const int lane = threadIdx.x & 31;
+  const int slot = __ldg(P.mat_slot + (i - P.k0));
+  double sxu = 0.0, sqx = 0.0;
+  if (slot < 0) {
+    sqx = ldcg(K.w.zq + (-slot - 1));
+  } else {
+    const int lo = __ldg(P.seg_lo + slot), hi = __ldg(P.seg_hi + slot);
+    const int ncw = K.sp.ncw;
+    const int cnt = (hi - lo + 1) * ncw;
+    double ax = 0.0, aq = 0.0;
+    for (int e = lane; e < cnt; e += 32) {
+      const int b = lo + e / ncw, w = e - (e / ncw) * ncw;
+      const int a0 = __ldg(P.cta_a0 + b);
+      if (a0 < 0) continue;
+      const long long at = ((long long)b * kConsumerWarps + w) * K.sp.segmax + (slot - a0);
+      ax += ldcg(K.w.segxu + at);
+      aq += ldcg(K.w.segqx + at);
+    }
+    sxu = warp_sum(ax);
+    sqx = warp_sum(aq);
+  }
+  return 0.5 * sxu + sqx + __ldg(P.r + i);
+}
+
 // grad_x Phi(x, (v, lam)) at coordinate j from the U-cache (problem.py:207-217):
 // (u_0 + q_0) then, in i order, + lam_i (u_i + q_i) for lam_i != 0, then + A^T v.
 // This rank's share of sum_i w_i (u_i + q_i) over its local matrices
@@ -454,6 +484,57 @@ __device__ __forceinline__ double recombine_local(const KArgs& K, const double* 
     if (l != 0.0) acc = acc + l * (ldcg(Upar + (long long)(i - P.k0) * n + j) + __ldg(P.q + (long long)i * n + j));
   }
   return acc;
+}
+
+// recombine_local for every column, for many matrices: each CTA takes 32-column
+// blocks, its 9 warps take contiguous chunks of the local matrices, and warp 0
+// adds the chunk partials in warp order (fixed order -> deterministic).  The
+// per-thread variant above leaves all but n threads idle and is latency-bound
+// for m in the hundreds (C1: 24 us -> ~4 us per trial).
+__device__ void recombine_cols(const KArgs& K, Sm& S, const double* Upar, const double* lam_s, double* out) {
+  const DevProblem& P = K.P;
+  const long long n = P.n;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nl = P.k1 - P.k0;
+  const int l0 = (w * nl) / kWarps, l1 = ((w + 1) * nl) / kWarps;
+  const long long nblk = (n + 31) / 32;
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long long j = blk * 32 + lane;
+    double acc = 0.0;
+    if (j < n) {
+      int lm = l0;
+      if (lm == 0 && P.k0 == 0 && l1 > 0) {
+        acc = ldcg(Upar + j) + __ldg(P.q + j);
+        lm = 1;
+      }
+      for (; lm + 3 < l1; lm += 4) {
+        double u[4], qq[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          u[k] = ldcg(Upar + (long long)(lm + k) * n + j);
+          qq[k] = __ldg(P.q + (long long)(P.k0 + lm + k) * n + j);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double l = lam_s[P.k0 + lm + k - 1];
+          const double t = l * (u[k] + qq[k]);
+          acc = (l != 0.0) ? acc + t : acc;
+        }
+      }
+      for (; lm < l1; ++lm) {
+        const double l = lam_s[P.k0 + lm - 1];
+        if (l != 0.0) acc = acc + l * (ldcg(Upar + (long long)lm * n + j) + __ldg(P.q + (long long)(P.k0 + lm) * n + j));
+      }
+    }
+    S.rc[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && j < n) {
+      double t = S.rc[0][lane];
+      for (int k = 1; k < kWarps; ++k) t += S.rc[k][lane];
+      out[j] = t;
+    }
+    __syncthreads();
+  }
 }
 
 // (A^T v)_j, added after the cross-rank sum (problem.py:215-216)

@@ -48,8 +48,12 @@ __device__ __forceinline__ BallScale ball_from_slots(const KArgs& K, Sm& S, int 
 __device__ __forceinline__ void g_local(const KArgs& K, int par) {
   const DevProblem& P = K.P;
   double* gv = K.w.gval + (long long)par * (P.m + 1);
-  for (long long i = gtid(); i <= P.m; i += gstride())
-    gv[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
+  const long long gw = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * kWarps;
+  for (long long i = gw; i <= P.m; i += nw) {     // one warp per matrix
+    const double v = (i >= P.k0 && i < P.k1) ? g_combine_warp(K, (int)i) : 0.0;
+    if ((threadIdx.x & 31) == 0) gv[i] = v;
+  }
 }
 
 // =========================================================== APDB-yx trial
@@ -97,7 +101,8 @@ __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
   double* lam_s = S.stage + P.p;
   stage_dual(K, w.ytr, bs, v_s, lam_s);
   const double* Uc = w.U + (long long)st.cur * P.nloc * P.n;
-  for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
+  if (K.sp.rc_cols) recombine_cols(K, S, Uc, lam_s, w.gxs);
+  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
   xk = X_GX;
   return TY_PRIMAL;
 }
@@ -340,9 +345,14 @@ __device__ int tx_gxpart(const KArgs& K, Sm& S, int& xk) {
   stage_dual(K, w.y + (long long)st.cur * np, BallScale{1.0, 1.0, 0, 0}, v_k, lam_k);
   const double* Un = w.U + (long long)(st.cur ^ 1) * P.nloc * n;
   double* gnew = w.gxb + (long long)st.ig_new * n;
-  for (long long j = gtid(); j < n; j += gstride()) {
-    w.gxs[j] = recombine_local(K, Un, lam_k, j);
-    gnew[j] = recombine_local(K, Un, lam_n, j);
+  if (K.sp.rc_cols) {
+    recombine_cols(K, S, Un, lam_k, w.gxs);
+    recombine_cols(K, S, Un, lam_n, gnew);
+  } else {
+    for (long long j = gtid(); j < n; j += gstride()) {
+      w.gxs[j] = recombine_local(K, Un, lam_k, j);
+      gnew[j] = recombine_local(K, Un, lam_n, j);
+    }
   }
   xk = X_GX2;
   return TX_NORMS;
@@ -434,7 +444,8 @@ __device__ int k_gxpart(const KArgs& K, Sm& S, int& xk) {
   double* lam_s = S.stage + P.p;
   stage_dual(K, w.y + (long long)st.cur * (P.p + P.m), BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
   const double* Uc = w.U + (long long)st.cur * P.nloc * P.n;
-  for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
+  if (K.sp.rc_cols) recombine_cols(K, S, Uc, lam_s, w.gxs);
+  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
   xk = X_GX;
   return K_FINISH;
 }
@@ -590,7 +601,8 @@ __device__ int r_gxpart(const KArgs& K, Sm& S, int& xk) {
   double* lam_s = S.stage + P.p;
   stage_dual(K, w.y + (long long)nxt * (P.p + P.m), BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
   const double* Un = w.U + (long long)nxt * P.nloc * P.n;
-  for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Un, lam_s, j);
+  if (K.sp.rc_cols) recombine_cols(K, S, Un, lam_s, w.gxs);
+  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Un, lam_s, j);
   xk = X_GX;
   return R_GXCACHE;
 }

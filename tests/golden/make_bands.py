@@ -50,7 +50,7 @@ POLICIES = {
 }
 
 
-def main(seeds=8):
+def main(seeds=24):
     arr = instances.config_instance("C0")
     crit = dict(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
     out = {}
