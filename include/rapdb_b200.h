@@ -125,6 +125,31 @@ int rapdb_bind_dense(rapdb_ctx* ctx, int n, int m, int p, int k0, int k1, long l
                      const double* lower, const double* upper, double mu,
                      const unsigned char* zero_flags);
 
+/* Factored sparse problem data (BASELINE config 3): replaces a ProblemInstance
+ * whose Q_i are sparse operators (_as_operator problem.py:31-40 keeps them as
+ * CSR) with Q_i = R_i^T R_i, plus L linear inequality rows a_j x <= b_j that
+ * the reference would hold as Q = 0 orthant constraints (problem.py:38-39:
+ * an all-zero Q becomes an empty CSR).  Constraint order: m = mq + L, rows
+ * 1..mq quadratic (q = C[1..mq], r = d[1..mq]), rows mq+1..m linear.
+ *   R     CSR [nr x n] of the stacked R_0..R_mq: r_ptr[nr+1] (int64),
+ *         r_col[nnz] (int32), r_val[nnz]; block i owns rows rblk[i]..rblk[i+1]
+ *   R^T   CSR [n x nr] of the same matrix: rt_ptr[n+1], rt_row, rt_val
+ *   rmat  [nr] block id of each stacked row (int32)
+ *   rblk  HOST [mq+2] row offsets of the blocks (rblk[0] = 0, rblk[mq+1] = nr)
+ *   C     [(mq+1) x n] linear terms, d [mq+1] constants
+ *   A     CSR [L x n] (a_ptr[L+1], a_col, a_val), A^T CSR [n x L], b [L]
+ * All other pointers are device pointers.  No equality block (p = 0), the
+ * dual set must be Unbounded, and the smoothed gap is not available (its
+ * n x n H does not fit at this n): adaptive restarts need a dense instance. */
+int rapdb_bind_factored(rapdb_ctx* ctx, int n, int mq, int L, long long nr,
+                        const long long* r_ptr, const int* r_col, const double* r_val,
+                        const long long* rt_ptr, const int* rt_row, const double* rt_val,
+                        const int* rmat, const long long* rblk,
+                        const double* C, const double* d,
+                        const long long* a_ptr, const int* a_col, const double* a_val,
+                        const long long* at_ptr, const int* at_row, const double* at_val,
+                        const double* b, const double* lower, const double* upper, double mu);
+
 /* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
  * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */
 int rapdb_set_params(rapdb_ctx* ctx, int mode, double c_alpha, double c_beta, double delta,
@@ -152,9 +177,15 @@ int rapdb_kkt(rapdb_ctx* ctx, int has_f_star, double f_star, double* out);
 /* engine.last / engine.average() (engine.py:262-272) into device buffers     */
 int rapdb_get_iterate(rapdb_ctx* ctx, int which, double* x, double* v, double* lam);
 
-/* One fused sweep at x (device): u[(k1-k0)][n] and g[m+1] (index 0 = f) into
- * device buffers; reps > 1 repeats it (timing); *ms = mean device ms/sweep.   */
+/* One fused sweep at x (device): u[(k1-k0)][n] (factored: W = R x, [nr]) and
+ * g[m+1] (index 0 = f) into device buffers; reps > 1 repeats it (timing);
+ * *ms = mean device ms/sweep.  g_value/f_value (problem.py:166-180).          */
 int rapdb_probe_sweep(rapdb_ctx* ctx, const double* x, double* u, double* g, int reps, float* ms);
+
+/* grad_x_coupling (problem.py:207-217) and g (problem.py:172-180) at an
+ * arbitrary point: gx[n] = grad_x Phi(x, v, lam), g[m+1] (index 0 = f); all
+ * device pointers; unsharded contexts only.                                  */
+int rapdb_grad_x(rapdb_ctx* ctx, const double* x, const double* v, const double* lam, double* gx, double* g);
 
 /* smoothed_gap(z, xi) (diagnostics.py:120-163) at an explicit point (source 0:
  * device x[n], v[p], lam[m], used as given -- no projection), the current

@@ -62,6 +62,85 @@ def _storage(M, n):
     return M
 
 
+class FactoredOp:
+    """Q = R^T R applied as R^T (R x): the config-3 restatement of a factored
+    quadratic form.  Held by ``Problem`` like any
+    other operator (problem.py:31-40 keeps non-array operators as given)."""
+
+    def __init__(self, R):
+        self.R = sp.csr_matrix(R)
+        self.RT = self.R.T.tocsr()
+        self.shape = (self.R.shape[1], self.R.shape[1])
+
+    def __matmul__(self, x):
+        return self.RT @ (self.R @ x)
+
+
+class FactoredProblem:
+    """Large-size config-3 restatement: quadratic rows as FactoredOp, the
+    linear block vectorised (g = A x - b, grad += A^T mu) instead of L explicit
+    dense q rows.  Same mathematics as ``factored_problem``; summation order of
+    the linear rows differs, so it is compared to the device within tolerance."""
+
+    def __init__(self, arr):
+        self.n, self.mq, self.L = arr.n, arr.mq, arr.L
+        self.m = arr.mq + arr.L
+        self.p = 0
+        self.Qf = [FactoredOp(arr.block(i)) for i in range(arr.mq + 1)]
+        self.C = [np.asarray(arr.C[i]) for i in range(arr.mq + 1)]
+        self.d = np.asarray(arr.d, dtype=float)
+        self.A = sp.csr_matrix(arr.A)
+        self.AT = self.A.T.tocsr()
+        self.bl = np.asarray(arr.b, dtype=float)
+        self.lo = np.asarray(arr.lower, dtype=float)
+        self.hi = np.asarray(arr.upper, dtype=float)
+        self.mu = 0.0
+        self.b = np.zeros(0)
+
+    def f(self, x):
+        return 0.5 * float(x @ (self.Qf[0] @ x)) + float(self.C[0] @ x) + self.d[0]
+
+    def g(self, x):
+        quad = [0.5 * float(x @ (self.Qf[i] @ x)) + float(self.C[i] @ x) + self.d[i]
+                for i in range(1, self.mq + 1)]
+        return np.concatenate([np.array(quad), self.A @ x - self.bl])
+
+    def eq(self, x):
+        return np.zeros(0)
+
+    def clip(self, w):
+        return np.clip(w, self.lo, self.hi)
+
+    def phi(self, x, v, lam):
+        return self.f(x) + (float(lam @ self.g(x)) if self.m > 0 else 0.0)
+
+    def grad_x(self, x, v, lam):
+        out = self.Qf[0] @ x + self.C[0]
+        for i in range(self.mq):
+            w = lam[i]
+            if w != 0.0:
+                out = out + w * (self.Qf[i + 1] @ x + self.C[i + 1])
+        if self.L:
+            out = out + self.AT @ lam[self.mq:]
+        return out
+
+
+def factored_problem(arr, dense=False):
+    """Oracle Problem for an ``instances.FactoredArrays``: Q_i = R_i^T R_i as
+    FactoredOp (or, ``dense=True``, the explicit products exactly as the
+    reference is given them, see FactoredArrays.dense_lists), Q = 0 (empty
+    CSR, problem.py:38-39) for the linear rows, q = (C, rows of A), r = (d, -b)."""
+    if dense:
+        Q, q, r = arr.dense_lists()
+    else:
+        Q = [FactoredOp(arr.block(i)) for i in range(arr.mq + 1)]
+        Q += [sp.csr_matrix((arr.n, arr.n)) for _ in range(arr.L)]
+        Ad = arr.A.toarray()
+        q = [arr.C[i] for i in range(arr.mq + 1)] + [Ad[j] for j in range(arr.L)]
+        r = np.concatenate([arr.d, -arr.b])
+    return Problem(Q, q, r, np.zeros((0, arr.n)), np.zeros(0), arr.lower, arr.upper, 0.0)
+
+
 class Problem:
     """Instance with box primal set, orthant cone, optional dual ball."""
 

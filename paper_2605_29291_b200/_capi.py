@@ -46,13 +46,13 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
-           "rapdb_exchange_count", "rapdb_step_profile"]
+           "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
               "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
               "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
-              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT"]
+              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN"]
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
@@ -97,6 +97,8 @@ def load(path: str = LIB_PATH):
     lib.rapdb_exchange_count.argtypes = [P]
     lib.rapdb_exchange_count.restype = LL
     lib.rapdb_step_profile.argtypes = [P, C.POINTER(D), C.POINTER(LL), I]
+    lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 19 + [D]
+    lib.rapdb_grad_x.argtypes = [P, P, P, P, P, P]
     _lib = lib
     return lib
 
@@ -194,21 +196,28 @@ class Context:
 
     # -- binding -----------------------------------------------------------
     def bind(self, data, cfg, k0=0, k1=None):
-        """data: problem.DeviceData (data.Q holds matrices k0..k1-1); cfg: resolved SolverConfig."""
-        from .geometry import ball_code
+        """data: problem.DeviceData (data.Q holds matrices k0..k1-1) or
+        factored.FactoredDeviceData; cfg: resolved SolverConfig."""
         self._set_stream()
-        k1 = data.m + 1 if k1 is None else k1
-        zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)
-        self._check(self.lib.rapdb_bind_dense(
-            self.h, data.n, data.m, data.p, k0, k1, data.ld,
-            _ptr(data.Q), _ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
-            _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
-            zero.ctypes.data_as(C.c_void_p)))
-        kind, r1, r2 = ball_code(cfg.dual_ball)
-        self._check(self.lib.rapdb_set_params(
-            self.h, 1 if cfg.mode == "xy" else 0, float(cfg.c_alpha), float(cfg.c_beta), float(cfg.delta),
-            float(cfg.eta), float(cfg.tau_bar), float(cfg.gamma0), 1 if cfg.nonmonotone else 0,
-            int(cfg.max_backtracks), kind, r1, r2))
+        if getattr(data, "factored", False):
+            rblk = np.ascontiguousarray(data.rblk, dtype=np.int64)
+            self._check(self.lib.rapdb_bind_factored(
+                self.h, data.n, data.mq, data.L, data.nr,
+                _ptr(data.r_ptr), _ptr(data.r_col), _ptr(data.r_val),
+                _ptr(data.rt_ptr), _ptr(data.rt_row), _ptr(data.rt_val),
+                _ptr(data.rmat), rblk.ctypes.data_as(C.c_void_p), _ptr(data.C), _ptr(data.d),
+                _ptr(data.a_ptr), _ptr(data.a_col), _ptr(data.a_val),
+                _ptr(data.at_ptr), _ptr(data.at_row), _ptr(data.at_val),
+                _ptr(data.b), _ptr(data.lower), _ptr(data.upper), float(data.mu)))
+        else:
+            k1 = data.m + 1 if k1 is None else k1
+            zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)
+            self._check(self.lib.rapdb_bind_dense(
+                self.h, data.n, data.m, data.p, k0, k1, data.ld,
+                _ptr(data.Q), _ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
+                _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
+                zero.ctypes.data_as(C.c_void_p)))
+        self._set_params(cfg)
         nbytes = int(self.lib.rapdb_workspace_bytes(self.h))
         if nbytes <= 0:
             raise DeviceError("workspace size query failed")
@@ -217,6 +226,14 @@ class Context:
         off = (-base) % 256
         self._check(self.lib.rapdb_bind_workspace(self.h, C.c_void_p(base + off), nbytes))
         self.data = data
+
+    def _set_params(self, cfg):
+        from .geometry import ball_code
+        kind, r1, r2 = ball_code(cfg.dual_ball)
+        self._check(self.lib.rapdb_set_params(
+            self.h, 1 if cfg.mode == "xy" else 0, float(cfg.c_alpha), float(cfg.c_beta), float(cfg.delta),
+            float(cfg.eta), float(cfg.tau_bar), float(cfg.gamma0), 1 if cfg.nonmonotone else 0,
+            int(cfg.max_backtracks), kind, r1, r2))
 
     # -- ops -----------------------------------------------------------------
     def reinit(self, source: int, x=None, v=None, lam=None, warm_tau=False, reset_inner=False):
@@ -254,12 +271,25 @@ class Context:
     def probe_sweep(self, x, reps=1):
         torch = self.torch
         d = self.data
-        u = torch.empty((d.m + 1, d.n), dtype=torch.float64, device=self.device)
+        if getattr(d, "factored", False):
+            u = torch.empty(max(d.nr, 1), dtype=torch.float64, device=self.device)
+        else:
+            u = torch.empty((d.m + 1, d.n), dtype=torch.float64, device=self.device)
         g = torch.empty(d.m + 1, dtype=torch.float64, device=self.device)
         ms = C.c_float()
         self._set_stream()
         self._check(self.lib.rapdb_probe_sweep(self.h, _ptr(x), _ptr(u), _ptr(g), int(reps), C.byref(ms)))
         return u, g, float(ms.value)
+
+    def grad_x(self, x, v, lam):
+        """(grad_x Phi(x, v, lam), g(x)) on the device (x, v, lam device tensors)."""
+        torch = self.torch
+        d = self.data
+        gx = torch.empty(d.n, dtype=torch.float64, device=self.device)
+        g = torch.empty(d.m + 1, dtype=torch.float64, device=self.device)
+        self._set_stream()
+        self._check(self.lib.rapdb_grad_x(self.h, _ptr(x), _ptr(v), _ptr(lam), _ptr(gx), _ptr(g)))
+        return gx, g
 
     def smoothed_gap(self, source: int, xi: float, tol: float, x_warm=None, x_cand=None, point=None):
         """point = (x, v, lam) device tensors for source 0."""

@@ -42,7 +42,7 @@ enum Slot {
   NSLOT
 };
 
-enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5 };
+enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5, OP_GRAD = 6 };
 enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
                  ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6, ST_EXCHANGE = 7, ST_RUNNING = 8 };
 
@@ -70,7 +70,7 @@ enum Step {
   A_POST, K_GXPART, K_FINISH, A_RESTART, A_END,
   R_POINT, R_SWEEP, R_GLOCAL, R_CACHE, R_GXPART, R_GXCACHE, R_FINISH,
   G_CAND, G_GLOCAL, G_HPART, G_SOLVE,
-  P_SWEEP, P_OUT,
+  P_SWEEP, P_OUT, P_GRAD, P_GFIN,
   DONE
 };
 // exchange kinds: what the host must all-reduce (sum) across ranks before resuming
@@ -88,6 +88,19 @@ struct DevProblem {
   const int* seg_hi;     // [nact]  last CTA (inclusive)
   const int* cta_a0;     // [G]     first active matrix of each CTA's row range
   const int* mat_slot;   // [nloc]  active index a >= 0, or -(zero index)-1
+  // ---- factored instances (kind 1, BASELINE config 3): Q_i = R_i^T R_i ----
+  int kind;              // 0 dense Q stack, 1 factored
+  int mq;                // quadratic constraints (factored matrices 0..mq)
+  long long nr;          // rows of the stacked R
+  int L;                 // linear rows A x <= b (orthant constraints with Q = 0)
+  int nchx;              // chunks of 1024 columns for c_i . x
+  const long long* r_ptr; const int* r_col; const double* r_val;    // CSR R   [nr x n]
+  const long long* rt_ptr; const int* rt_row; const double* rt_val; // CSR R^T [n x nr]
+  const int* rmat;                                                  // [nr] block of each R row
+  const long long* rblk;                                            // [mq+2] first row of block i
+  const long long* a_ptr; const int* a_col; const double* a_val;    // CSR A   [L x n]
+  const long long* at_ptr; const int* at_row; const double* at_val; // CSR A^T [n x L]
+  const long long* wch;  // [mq+2] prefix count of 1024-row chunks of W per block
 };
 
 struct DevParams {
@@ -115,6 +128,8 @@ struct Work {
   double *x, *U, *gval, *eqv, *y, *ytr, *gy, *gxb, *gxs, *xcum, *ycum, *part,
          *segxu, *segqx, *zq, *aux, *aux2;
   double *H, *hx, *hxn, *hy;   // smoothed gap: dense H (n x n) and H-products
+  double *W;                   // factored: [2][nr] W = R x at both parities
+  double *pw2, *pcx;           // factored: chunk partials of |W_i|^2 and c_i . x
   double* trace;
   SolverState* st;
   unsigned long long* bar;

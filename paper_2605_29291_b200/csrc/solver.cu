@@ -134,13 +134,56 @@ __device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
         if (!sweep_sync(K, S, rc.in_x, st.cur ^ 1)) return kAbort;
       return P_OUT;
     }
-    case P_OUT: {
+    case P_OUT: {   // g (and the cache row(s): U, or W = R x when factored) at rc.in_x
       const DevProblem& P = K.P;
+      const int par = st.cur ^ 1;
+      const int nxt = rc.op == OP_GRAD ? P_GRAD : DONE;
+      if (P.kind == 1) {
+        g_factored(K, par);
+        if (!gsync(K, S)) return kAbort;
+        const double* gv = K.w.gval + (long long)par * (P.m + 1);
+        for (long long i = gtid(); i <= P.m; i += gstride()) rc.out_g[i] = ldcg(gv + i);
+        const double* Wp = K.w.W + (long long)par * P.nr;
+        if (rc.out_u)
+          for (long long j = gtid(); j < P.nr; j += gstride()) rc.out_u[j] = ldcg(Wp + j);
+        return nxt;
+      }
       for (long long i = gtid(); i <= P.m; i += gstride())
         rc.out_g[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
-      const double* Up = K.w.U + (long long)(st.cur ^ 1) * P.nloc * P.n;
+      const double* Up = K.w.U + (long long)par * P.nloc * P.n;
       const long long tot = (long long)P.nloc * P.n;
-      for (long long j = gtid(); j < tot; j += gstride()) rc.out_u[j] = ldcg(Up + j);
+      if (rc.out_u)
+        for (long long j = gtid(); j < tot; j += gstride()) rc.out_u[j] = ldcg(Up + j);
+      return nxt;
+    }
+    case P_GRAD: {  // grad_x Phi(x, v, lam) at the probed point (problem.py:207-217)
+      const DevProblem& P = K.P;
+      double* v_s = S.stage;
+      double* lam_s = S.stage + P.p;
+      if (P.kind == 0) {
+        for (int j = threadIdx.x; j < P.p + P.m; j += kThreads) {
+          if (j < P.p) v_s[j] = ldcg(rc.in_v + j);
+          else lam_s[j - P.p] = ldcg(rc.in_lam + (j - P.p));
+        }
+        __syncthreads();
+      }
+      if (!gx_part(K, S, st.cur ^ 1, rc.in_lam, lam_s, K.w.gxs)) return kAbort;
+      xk = X_GX;
+      return P_GFIN;
+    }
+    case P_GFIN: {
+      const DevProblem& P = K.P;
+      double* v_s = S.stage;
+      if (P.kind == 0 && P.p > 0) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < P.p; j += kThreads) v_s[j] = ldcg(rc.in_v + j);
+        __syncthreads();
+      }
+      for (long long j = gtid(); j < P.n; j += gstride()) {
+        double gx = ldcg(K.w.gxs + j);
+        if (P.p > 0) gx = gx + atv(K, v_s, j);
+        rc.out_x[j] = gx;
+      }
       return DONE;
     }
     default:
@@ -266,7 +309,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
           break;
         case OP_KKT: s_st.step = K_GXPART; s_st.kret = DONE; break;
         case OP_GAP: s_st.step = G_CAND; break;
-        case OP_PROBE: s_st.step = P_SWEEP; break;
+        case OP_PROBE: case OP_GRAD: s_st.step = P_SWEEP; break;
         default: s_st.step = DONE; break;
       }
     } else {
@@ -299,9 +342,12 @@ struct rapdb_ctx {
   SweepPlan sp{};
   Work w{};
   int* d_ints = nullptr;
+  long long* d_ll = nullptr;   // factored: rblk and W-chunk prefix tables
   long long ws_bytes = 0;
   long long stage_cap = 0;  // doubles available in the staging area
   bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
+  long long sweep_bytes = 0;  // algorithmic bytes of one sweep (the roofline numerator)
+  long long nchw = 0;       // factored: 1024-row chunks of W over all blocks
   int split = 0;            // sharded: stop at exchange points
   rapdb_exchange_fn xcb = nullptr;
   void* xuser = nullptr;
@@ -328,14 +374,17 @@ int cuda_fail(rapdb_ctx* c, cudaError_t e, const char* where) {
 
 long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+constexpr int B_COUNT_MAX = 32;
+
 struct Layout {
-  long long off[24];
+  long long off[B_COUNT_MAX];
   long long total;
 };
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
-             B_COUNT };
+             B_W, B_PW2, B_PCX, B_COUNT };
+static_assert(B_COUNT <= B_COUNT_MAX, "Layout::off too small");
 
 Layout layout_of(const rapdb_ctx* c) {
   const long long n = c->P.n, m = c->P.m, p = c->P.p, np = n > 0 ? p + m : 0;
@@ -365,6 +414,10 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_ST] = sizeof(SolverState);
   sz[B_BAR] = 64;
   sz[B_ABORT] = 128 + 16LL * G;   // flag + diagnostics + per-CTA progress beacons
+  const bool fac = c->P.kind == 1;
+  sz[B_W] = fac ? 2 * c->P.nr * 8 : 8;
+  sz[B_PW2] = fac ? std::max(c->nchw, 1LL) * 8 : 8;
+  sz[B_PCX] = fac ? (long long)(c->P.mq + 1) * c->P.nchx * 8 : 8;
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -402,6 +455,8 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
 // (NCCL over NVLink in the Python binding) and the op resumes in a new launch.
 int launch(rapdb_ctx* c, RunCfg rc) {
   if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
+  if (c->P.kind == 1 && c->prm.ball != 0)
+    return fail(c, RAPDB_ECONFIG, "factored instances support the unbounded dual set only");
   rc.split = c->split;
   rc.resume = 0;
   int r = launch_once(c, rc);
@@ -562,6 +617,7 @@ int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
 void rapdb_destroy(rapdb_ctx* c) {
   if (!c) return;
   if (c->d_ints) cudaFree(c->d_ints);
+  if (c->d_ll) cudaFree(c->d_ll);
   delete c;
 }
 
@@ -701,6 +757,84 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   P.seg_hi = c->d_ints + o_hi; P.cta_a0 = c->d_ints + o_a0; P.mat_slot = c->d_ints + o_slot;
   c->P = P;
   c->sp = sp;
+  c->sweep_bytes = R * (long long)n * 8;
+  c->nchw = 0;
+  c->bound = true;
+  c->have_ws = false;
+  return RAPDB_OK;
+}
+
+int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const long long* r_ptr, const int* r_col,
+                        const double* r_val, const long long* rt_ptr, const int* rt_row, const double* rt_val,
+                        const int* rmat, const long long* rblk, const double* C, const double* d,
+                        const long long* a_ptr, const int* a_col, const double* a_val, const long long* at_ptr,
+                        const int* at_row, const double* at_val, const double* b, const double* lower,
+                        const double* upper, double mu) {
+  if (!c) return RAPDB_EINPUT;
+  if (n <= 0 || mq < 0 || L < 0 || nr < 0) return fail(c, RAPDB_EINPUT, "need n > 0, mq >= 0, L >= 0, nr >= 0");
+  if (c->nranks != 1 || c->split)
+    return fail(c, RAPDB_ECONFIG, "factored instances run on one rank (replicate across GPUs)");
+  if (!rblk || !C || !d || !lower || !upper || !rt_ptr || !at_ptr ||
+      (nr > 0 && (!r_ptr || !r_col || !r_val || !rt_row || !rt_val || !rmat)) ||
+      (L > 0 && (!a_ptr || !a_col || !a_val || !at_row || !at_val || !b)))
+    return fail(c, RAPDB_EINPUT, "null data pointer");
+  if (rblk[0] != 0 || rblk[mq + 1] != nr) return fail(c, RAPDB_EINPUT, "rblk must run from 0 to nr");
+  std::vector<long long> ll(2 * (size_t)(mq + 2));
+  for (int i = 0; i <= mq; ++i) {
+    if (rblk[i + 1] < rblk[i]) return fail(c, RAPDB_EINPUT, "rblk must be nondecreasing");
+    ll[i] = rblk[i];
+    ll[mq + 2 + i + 1] = ll[mq + 2 + i] + (rblk[i + 1] - rblk[i] + 1023) / 1024;
+  }
+  ll[mq + 1] = nr;
+  const long long nchw = ll[2 * (mq + 2) - 1];
+  if (c->d_ll) cudaFree(c->d_ll);
+  c->d_ll = nullptr;
+  CK(cudaMalloc(&c->d_ll, ll.size() * sizeof(long long)));
+  CK(cudaMemcpy(c->d_ll, ll.data(), ll.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  if (c->d_ints) cudaFree(c->d_ints);
+  c->d_ints = nullptr;
+  CK(cudaMalloc(&c->d_ints, 16));
+  CK(cudaMemset(c->d_ints, 0, 16));
+  long long nnz_r = 0, nnz_a = 0;
+  if (nr > 0) CK(cudaMemcpy(&nnz_r, r_ptr + nr, 8, cudaMemcpyDeviceToHost));
+  if (L > 0) CK(cudaMemcpy(&nnz_a, a_ptr + L, 8, cudaMemcpyDeviceToHost));
+  // no streamed sweep: the ring degenerates to the multiplier staging area
+  SweepPlan sp{};
+  sp.TR = 1; sp.cpr = 1; sp.chunk = 2; sp.nstages = 1; sp.ncw = 1; sp.segmax = 1;
+  sp.rc_cols = 1;   // the recombination ends warp-per-column: barrier before the primal step
+  sp.stage_bytes = align_up((long long)(mq + 1) * 8, 128);
+  sp.xs_bytes = 0;
+  sp.rows_total = 0;
+  c->dyn_smem = (size_t)(sp.stage_bytes + 16);
+  c->stage_cap = sp.stage_bytes / 8;
+  c->gap_ok = false;
+  if ((long long)c->dyn_smem + 4096 > (long long)c->optin)
+    return fail(c, RAPDB_ECONFIG, "too many quadratic constraints for the staging area");
+  cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->dyn_smem);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaFuncSetAttribute");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)rapdb_solver_kernel, kThreads, c->dyn_smem);
+  if (e != cudaSuccess) return cuda_fail(c, e, "occupancy");
+  if (occ < 1) return fail(c, RAPDB_EDEVICE, "solver kernel cannot be resident");
+  c->G = c->nsm * 1;   // one CTA per SM: grid barriers stay cheap
+  DevProblem P{};
+  const int m = mq + L;
+  P.n = n; P.m = m; P.p = 0; P.k0 = 0; P.k1 = m + 1; P.nloc = 0; P.nact = 0; P.nzero = 0; P.ld = n;
+  P.Q = nullptr; P.q = C; P.r = d; P.A = nullptr; P.b = b; P.lo = lower; P.hi = upper; P.mu = mu;
+  P.act = P.zero_list = P.seg_lo = P.seg_hi = P.cta_a0 = P.mat_slot = c->d_ints;
+  P.kind = 1; P.mq = mq; P.nr = nr; P.L = L; P.nchx = (n + 1023) / 1024;
+  P.r_ptr = r_ptr; P.r_col = r_col; P.r_val = r_val;
+  P.rt_ptr = rt_ptr; P.rt_row = rt_row; P.rt_val = rt_val;
+  P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (mq + 2);
+  P.a_ptr = a_ptr; P.a_col = a_col; P.a_val = a_val;
+  P.at_ptr = at_ptr; P.at_row = at_row; P.at_val = at_val;
+  c->P = P;
+  c->sp = sp;
+  c->nchw = nchw;
+  // one factored sweep: R (12 B/nnz + row pointers) streamed, W written and
+  // re-read, C and A (+ b) read, x gathered once
+  c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * (mq + 1) * n + 12 * nnz_a + 16LL * L + 8 + 8LL * n;
   c->bound = true;
   c->have_ws = false;
   return RAPDB_OK;
@@ -745,6 +879,9 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.hx = D(B_HX);
   w.hxn = D(B_HXN);
   w.hy = D(B_HY);
+  w.W = D(B_W);
+  w.pw2 = D(B_PW2);
+  w.pcx = D(B_PCX);
   w.trace = nullptr;
   w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);
@@ -823,7 +960,7 @@ int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_re
   out->sweep_ns = st.sweep_ns - before.sweep_ns;
   out->sweeps = st.sweeps - before.sweeps;
   out->kernel_ms = (double)kms;
-  out->sweep_bytes = c->sp.rows_total * (long long)c->P.n * 8;
+  out->sweep_bytes = c->sweep_bytes;
   if (st.status == ST_ABORT) return fail(c, RAPDB_EDEVICE, "device watchdog fired");
   if (st.status == ST_NONCONV) {
     char buf[256];
@@ -883,6 +1020,20 @@ int rapdb_probe_sweep(rapdb_ctx* c, const double* x, double* u, double* g, int r
   cudaEventDestroy(e1);
   if (ms) *ms = t / (float)rc.reps;
   return r;
+}
+
+int rapdb_grad_x(rapdb_ctx* c, const double* x, const double* v, const double* lam, double* gx, double* g) {
+  if (!c || !x || !gx || !g || (c->P.p > 0 && !v) || (c->P.m > 0 && !lam)) return RAPDB_EINPUT;
+  if (c->split) return fail(c, RAPDB_ECONFIG, "rapdb_grad_x needs an unsharded context");
+  RunCfg rc{};
+  rc.op = OP_GRAD;
+  rc.in_x = x; rc.in_v = v; rc.in_lam = lam;
+  rc.out_x = gx; rc.out_g = g; rc.out_u = nullptr;
+  rc.reps = 1;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  return read_state(c, &st);
 }
 
 int rapdb_smoothed_gap(rapdb_ctx* c, int source, const double* x, const double* v, const double* lam,

@@ -571,6 +571,7 @@ __device__ __forceinline__ BallScale ball_scale(const DevParams& prm, double vv,
 // stage (v, lam) = ball(src) into shared memory: v_s[0..p), lam_s[0..m)
 __device__ __forceinline__ void stage_dual(const KArgs& K, const double* src, BallScale bs,
                                            double* v_s, double* lam_s) {
+  if (K.P.kind == 1) return;   // factored: multipliers are read from global (dual_at)
   const int p = K.P.p, m = K.P.m;
   for (int j = threadIdx.x; j < p + m; j += kThreads) {
     double yv = ldcg(src + j);

@@ -18,15 +18,20 @@
 // partial already is the total and the kernel just continues (a grid barrier
 // where the consumer mapping differs).  Single-GPU runs never leave the kernel.
 #pragma once
-#include "solver_kernel.cuh"
+#include "factored.cuh"
 
 namespace rapdb {
 
 __device__ __forceinline__ bool sweep_sync(const KArgs& K, Sm& S, const double* xsrc, int par) {
   unsigned long long t0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer();
-  sweep(K, S, xsrc, par);
-  const bool ok = gsync(K, S);
+  bool ok;
+  if (K.P.kind == 1) {
+    ok = sweep_factored(K, S, xsrc, par);
+  } else {
+    sweep(K, S, xsrc, par);
+    ok = gsync(K, S);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long t1 = globaltimer();
     if (t1 > t0) S.st->sweep_ns += (double)(t1 - t0);   // skip a driver re-sync jump
@@ -46,6 +51,10 @@ __device__ __forceinline__ BallScale ball_from_slots(const KArgs& K, Sm& S, int 
 
 // g_i at parity `par` for this rank's matrices, 0 for the others (summed across ranks: exact)
 __device__ __forceinline__ void g_local(const KArgs& K, int par) {
+  if (K.P.kind == 1) {   // quadratic rows from the W-cache partials; linear rows came with the sweep
+    g_factored(K, par);
+    return;
+  }
   const DevProblem& P = K.P;
   double* gv = K.w.gval + (long long)par * (P.m + 1);
   const long long gw = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -54,6 +63,27 @@ __device__ __forceinline__ void g_local(const KArgs& K, int par) {
     const double v = (i >= P.k0 && i < P.k1) ? g_combine_warp(K, (int)i) : 0.0;
     if ((threadIdx.x & 31) == 0) gv[i] = v;
   }
+}
+
+// This rank's share of sum_i lam_i grad g_i(x) + grad f(x) at the cached point
+// of parity `par` into out.  Dense: from the U-cache with the staged
+// multipliers lam_s; factored: from the W-cache with the global lam_g.
+__device__ __forceinline__ bool gx_part(const KArgs& K, Sm& S, int par, const double* lam_g, const double* lam_s,
+                                        double* out) {
+  const DevProblem& P = K.P;
+  if (P.kind == 1) return recombine_factored(K, S, K.w.W + (long long)par * P.nr, lam_g, out);
+  const double* U = K.w.U + (long long)par * P.nloc * P.n;
+  if (K.sp.rc_cols) recombine_cols(K, S, U, lam_s, out);
+  else for (long long j = gtid(); j < P.n; j += gstride()) out[j] = recombine_local(K, U, lam_s, j);
+  return true;
+}
+
+// multiplier j of a dual vector: staged copy (dense) or global y (factored;
+// balls are rejected there, so the global vector is already final)
+__device__ __forceinline__ double dual_at(const KArgs& K, const double* v_s, const double* lam_s, const double* yg,
+                                          long long j) {
+  if (K.P.kind == 1) return ldcg(yg + j);
+  return j < K.P.p ? v_s[j] : lam_s[j - K.P.p];
 }
 
 // =========================================================== APDB-yx trial
@@ -100,9 +130,7 @@ __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
   double* v_s = S.stage;
   double* lam_s = S.stage + P.p;
   stage_dual(K, w.ytr, bs, v_s, lam_s);
-  const double* Uc = w.U + (long long)st.cur * P.nloc * P.n;
-  if (K.sp.rc_cols) recombine_cols(K, S, Uc, lam_s, w.gxs);
-  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
+  if (!gx_part(K, S, st.cur, w.ytr + P.p, lam_s, w.gxs)) return kAbort;
   xk = X_GX;
   return TY_PRIMAL;
 }
@@ -137,7 +165,7 @@ __device__ int ty_primal(const KArgs& K, Sm& S) {
   double* yn = w.y + (long long)nxt * np;
   const double* gvc = w.gval + (long long)cur * (m + 1);
   for (long long j = gtid(); j < np; j += gstride()) {
-    const double yv = j < p ? v_s[j] : lam_s[j - p];
+    const double yv = dual_at(K, v_s, lam_s, w.ytr, j);
     yn[j] = yv;
     const double d = yv - ldcg(yc + j);
     s_dd += d * d;
@@ -345,7 +373,10 @@ __device__ int tx_gxpart(const KArgs& K, Sm& S, int& xk) {
   stage_dual(K, w.y + (long long)st.cur * np, BallScale{1.0, 1.0, 0, 0}, v_k, lam_k);
   const double* Un = w.U + (long long)(st.cur ^ 1) * P.nloc * n;
   double* gnew = w.gxb + (long long)st.ig_new * n;
-  if (K.sp.rc_cols) {
+  if (P.kind == 1) {
+    if (!gx_part(K, S, st.cur ^ 1, w.y + (long long)st.cur * np + p, lam_k, w.gxs)) return kAbort;
+    if (!gx_part(K, S, st.cur ^ 1, w.ytr + p, lam_n, gnew)) return kAbort;
+  } else if (K.sp.rc_cols) {
     recombine_cols(K, S, Un, lam_k, w.gxs);
     recombine_cols(K, S, Un, lam_n, gnew);
   } else {
@@ -393,7 +424,7 @@ __device__ int tx_norms(const KArgs& K, Sm& S) {
   double* yn = w.y + (long long)nxt * np;
   const double* gvn = w.gval + (long long)nxt * (m + 1);
   for (long long j = gtid(); j < np; j += gstride()) {
-    const double yv = j < p ? v_n[j] : lam_n[j - p];
+    const double yv = dual_at(K, v_n, lam_n, w.ytr, j);
     yn[j] = yv;
     const double d = yv - ldcg(yc + j);
     s_dd += d * d;
@@ -442,10 +473,9 @@ __device__ int k_gxpart(const KArgs& K, Sm& S, int& xk) {
   SolverState& st = *S.st;
   double* v_s = S.stage;
   double* lam_s = S.stage + P.p;
-  stage_dual(K, w.y + (long long)st.cur * (P.p + P.m), BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
-  const double* Uc = w.U + (long long)st.cur * P.nloc * P.n;
-  if (K.sp.rc_cols) recombine_cols(K, S, Uc, lam_s, w.gxs);
-  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Uc, lam_s, j);
+  const double* yc = w.y + (long long)st.cur * (P.p + P.m);
+  stage_dual(K, yc, BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
+  if (!gx_part(K, S, st.cur, yc + P.p, lam_s, w.gxs)) return kAbort;
   xk = X_GX;
   return K_FINISH;
 }
@@ -475,7 +505,7 @@ __device__ int k_finish(const KArgs& K, Sm& S) {
       s_eq += e * e;
     } else {
       const double g = ldcg(gvc + (idx - p + 1));
-      const double c = fmin(lam_s[idx - p], -g);
+      const double c = fmin(dual_at(K, v_s, lam_s, w.y + (long long)cur * np, idx), -g);
       s_comp += c * c;
       const double gp = fmax(g, 0.0);
       s_gp2 += gp * gp;
@@ -599,10 +629,9 @@ __device__ int r_gxpart(const KArgs& K, Sm& S, int& xk) {
   const int nxt = st.cur ^ 1;
   double* v_s = S.stage;
   double* lam_s = S.stage + P.p;
-  stage_dual(K, w.y + (long long)nxt * (P.p + P.m), BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
-  const double* Un = w.U + (long long)nxt * P.nloc * P.n;
-  if (K.sp.rc_cols) recombine_cols(K, S, Un, lam_s, w.gxs);
-  else for (long long j = gtid(); j < P.n; j += gstride()) w.gxs[j] = recombine_local(K, Un, lam_s, j);
+  const double* yn = w.y + (long long)nxt * (P.p + P.m);
+  stage_dual(K, yn, BallScale{1.0, 1.0, 0, 0}, v_s, lam_s);
+  if (!gx_part(K, S, nxt, yn + P.p, lam_s, w.gxs)) return kAbort;
   xk = X_GX;
   return R_GXCACHE;
 }

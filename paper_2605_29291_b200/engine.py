@@ -303,16 +303,13 @@ class _Evaluator:
         return val
 
     def grad_x_t(self, z):
-        u, g = self.sweep(z.x)
-        d = self.data
-        out = u[0] + d.q[0]
-        for i in range(self.inst.m):
-            li = float(z.lam[i])
-            if li != 0.0:
-                out = out + li * (u[i + 1] + d.q[i + 1])
-        if self.inst.p > 0:
-            out = out + d.A.T @ self._x(z.v)
-        return out
+        """grad_x Phi(z) (problem.py:207-217) through the solver kernel's own
+        recombination (rapdb_grad_x): dense U-cache or factored W-cache."""
+        inst = self.inst
+        v = self._x(z.v) if inst.p else None
+        lam = self._x(z.lam) if inst.m else None
+        gx, _ = self.ctx.grad_x(self._x(z.x), v, lam)
+        return gx
 
     def grad_x(self, z):
         return self.grad_x_t(z).cpu().numpy()

@@ -1,0 +1,162 @@
+"""Factored sparse QCQP instances (BASELINE config 3) on the device.
+
+The reference can only hold such a problem as m+1 explicit operators
+(``ProblemInstance`` problem.py:109-162; ``_as_operator`` :31-40 keeps sparse
+ones as CSR) -- at n = 10^6 the products R_i^T R_i are not representable, so
+config 3 is new capability built on the same operator contract
+(problem.py:166-223, SURVEY.md section 8 row "C3"):
+
+    Q_i = R_i^T R_i  (i = 0..mq, 0 = objective)   g_i = 1/2 |R_i x|^2 + c_i.x + d_i
+    a_j x <= b_j     (j = 1..L)                    g_{mq+j} = a_j x - b_j   (Q = 0)
+
+``FactoredInstance`` exposes the same surface the solver layers use from
+``problem.ProblemInstance`` (n, m, p, primal_set, cone, mu, f/g evaluation,
+device upload), so ``ApdbEngine`` / ``run_restarted`` / ``kkt_residual`` take
+either.  HBM layout (``FactoredDeviceData``): the stacked R as CSR (int64 row
+pointers, int32 columns, fp64 values) plus a second CSR of R^T so the
+transposed product is a gather (no atomics, fixed summation order), the
+block id of every stacked row, C [(mq+1) x n], and A / A^T as CSR.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+
+from .errors import ConfigurationError, InputError
+from .geometry import Box, NonnegOrthant
+
+
+class FactoredInstance:
+    """Q_i = R_i^T R_i QCQP with a sparse linear inequality block; box primal
+    set, nonnegative-orthant cone over the m = mq + L constraints, p = 0."""
+
+    def __init__(self, n, mq, R, rblk, C, d, A, b, lower, upper, mu=0.0, name=""):
+        import scipy.sparse as sp
+        self.n, self.mq = int(n), int(mq)
+        self.R = sp.csr_matrix(R)
+        self.rblk = np.asarray(rblk, dtype=np.int64)
+        self.C = np.ascontiguousarray(C, dtype=np.float64)
+        self.d = np.asarray(d, dtype=np.float64)
+        self.A = sp.csr_matrix(A) if A is not None else sp.csr_matrix((0, self.n))
+        self.b = np.asarray(b, dtype=np.float64).reshape(-1)
+        self.L = self.A.shape[0]
+        self.m = self.mq + self.L
+        self.p = 0
+        self.mu = float(mu)
+        self.name = name
+        self.dual_set = None
+        self.primal_set = Box(np.asarray(lower, dtype=float), np.asarray(upper, dtype=float))
+        self.cone = NonnegOrthant(self.m)
+        n = self.n
+        if n <= 0 or self.mq < 0:
+            raise InputError("need n > 0 and mq >= 0")
+        if self.R.shape[1] != n or self.A.shape[1] != n:
+            raise InputError("R and A need n columns")
+        if self.rblk.shape != (self.mq + 2,) or self.rblk[0] != 0 or self.rblk[-1] != self.R.shape[0] \
+                or np.any(np.diff(self.rblk) < 0):
+            raise InputError("rblk must be nondecreasing offsets 0..nr of the mq+1 blocks of R")
+        if self.C.shape != (self.mq + 1, n) or self.d.shape != (self.mq + 1,):
+            raise InputError("need C [(mq+1) x n] and d [mq+1]")
+        if self.b.shape != (self.L,):
+            raise InputError("b must have one entry per row of A")
+        if self.primal_set.lower.shape != (n,) or self.primal_set.upper.shape != (n,):
+            raise InputError("primal set dimension mismatch")
+        if self.mu < 0:
+            raise InputError("strong convexity modulus must be nonnegative")
+        if self.R.shape[0] >= 2 ** 31 or self.R.nnz >= 2 ** 62:
+            raise InputError("R too large for int32 row ids")
+        self._dev = {}
+
+    @classmethod
+    def from_arrays(cls, arr, mu=0.0):
+        """From ``instances.FactoredArrays``."""
+        rblk = np.arange(arr.mq + 2, dtype=np.int64) * arr.rows
+        return cls(arr.n, arr.mq, arr.R, rblk, arr.C, arr.d, arr.A, arr.b, arr.lower, arr.upper,
+                   mu=mu, name=arr.name)
+
+    def check_device_support(self):
+        return None
+
+    # -- device ---------------------------------------------------------------
+    def device_data(self, device=None, pinned_host=None, krange=None):
+        import torch
+        if krange is not None and tuple(krange) != (0, self.m + 1):
+            raise ConfigurationError("factored instances are not constraint-sharded (run replicas)")
+        dev = torch.device("cuda", 0) if device is None else torch.device(device)
+        key = str(dev)
+        if key not in self._dev:
+            self._dev[key] = FactoredDeviceData.upload(self, dev)
+        return self._dev[key]
+
+    def drop_device_data(self):
+        for k in [k for k in self._dev if not k.startswith("_")]:
+            del self._dev[k]
+
+    # -- evaluations (problem.py:166-186) on the device ----------------------
+    def _evaluator(self):
+        from .engine import _Evaluator
+        ev = self._dev.get("_eval")
+        if ev is None:
+            ev = _Evaluator(self)
+            self._dev["_eval"] = ev
+        return ev
+
+    def f_value(self, x) -> float:
+        return float(self._evaluator().sweep(x)[1][0])
+
+    def g_value(self, x) -> np.ndarray:
+        if self.m == 0:
+            return np.zeros(0)
+        return self._evaluator().sweep(x)[1][1:].cpu().numpy()
+
+    def eq_residual(self, x) -> np.ndarray:
+        return np.zeros(0)
+
+    def project_dual_cone(self, lam):
+        return np.maximum(np.asarray(lam, dtype=float), 0.0)
+
+
+class FactoredDeviceData:
+    """A FactoredInstance resident in HBM (see module docstring)."""
+
+    factored = True
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    @classmethod
+    def upload(cls, inst: FactoredInstance, device):
+        import torch
+
+        def f64(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+
+        def i64(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).to(device)
+
+        def i32(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+
+        def csr(M):
+            return i64(M.indptr), i32(M.indices), f64(M.data)
+
+        R = inst.R
+        Rt = R.T.tocsr()
+        A = inst.A
+        At = A.T.tocsr()
+        nr = R.shape[0]
+        rmat = np.repeat(np.arange(inst.mq + 1, dtype=np.int32), np.diff(inst.rblk))
+        r_ptr, r_col, r_val = csr(R)
+        rt_ptr, rt_row, rt_val = csr(Rt)
+        a_ptr, a_col, a_val = csr(A)
+        at_ptr, at_row, at_val = csr(At)
+        one = lambda t: t if t.numel() else torch.zeros(1, dtype=t.dtype, device=device)
+        return cls(n=inst.n, m=inst.m, p=0, mq=inst.mq, L=inst.L, nr=nr, rblk=inst.rblk.copy(),
+                   r_ptr=r_ptr, r_col=one(r_col), r_val=one(r_val), rt_ptr=rt_ptr, rt_row=one(rt_row),
+                   rt_val=one(rt_val), rmat=one(i32(rmat)), C=f64(inst.C), d=f64(inst.d),
+                   a_ptr=a_ptr, a_col=one(a_col), a_val=one(a_val), at_ptr=at_ptr, at_row=one(at_row),
+                   at_val=one(at_val), b=one(f64(inst.b)), lower=f64(inst.primal_set.lower),
+                   upper=f64(inst.primal_set.upper), mu=inst.mu, device=device,
+                   nnz_r=int(R.nnz), nnz_a=int(A.nnz))

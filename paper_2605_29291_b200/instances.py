@@ -183,7 +183,93 @@ def kml_epigraph(N: int = 4000, d: int = 50, seed: int = 0,
         meta={"generator": GENERATOR_NAME, "seed": seed, "median_dist": med})
 
 
-# BASELINE.json configs[0..2], [4]; config 3 (factored sparse) lives in sparse.py
+@dataclass
+class FactoredArrays:
+    """Config-3 style instance: Q_i = R_i^T R_i (i = 0..mq, i = 0 objective) with
+    the R_i stacked into one CSR ``R`` (row block i = rows [i*r, (i+1)*r)), dense
+    linear terms ``C [mq+1][n]``, constants ``d``, and a sparse linear block
+    ``A x <= b`` treated as orthant constraints with Q = 0 (so the constraint
+    vector is (g_1..g_mq, A x - b))."""
+
+    n: int
+    mq: int
+    rows: int                  # rows per R_i
+    R: object                  # scipy.sparse.csr_matrix ((mq+1)*rows, n)
+    C: np.ndarray              # (mq+1, n)
+    d: np.ndarray              # (mq+1,)
+    A: object                  # scipy.sparse.csr_matrix (L, n)
+    b: np.ndarray              # (L,)
+    lower: np.ndarray
+    upper: np.ndarray
+    name: str = ""
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def m(self) -> int:        # total constraints: quadratic + linear rows
+        return self.mq + self.A.shape[0]
+
+    @property
+    def L(self) -> int:        # linear inequality rows
+        return self.A.shape[0]
+
+    def block(self, i: int):
+        """R_i (CSR rows [i*rows, (i+1)*rows) of the stack)."""
+        return self.R[i * self.rows:(i + 1) * self.rows]
+
+    def dense_lists(self):
+        """(Q list, q list, r) as the reference's ProblemInstance holds this
+        instance: dense Q_i = R_i^T R_i (its ``_as_operator`` turns them into CSR
+        when sparse enough, problem.py:31-40), zero Q for each linear row
+        (problem.py:38-39), q = (c_0..c_mq, a_1..a_L), r = (d_0..d_mq, -b).
+        Small instances only (m+1 dense n x n matrices)."""
+        Q = [np.asarray((self.block(i).T @ self.block(i)).toarray()) for i in range(self.mq + 1)]
+        Q += [np.zeros((self.n, self.n)) for _ in range(self.L)]
+        Ad = self.A.toarray()
+        q = [self.C[i].copy() for i in range(self.mq + 1)] + [Ad[j].copy() for j in range(self.L)]
+        r = np.concatenate([self.d, -self.b])
+        return Q, q, r
+
+
+def _csr_uniform(rng_vals, rng_cols, nrows, ncols, nnz_row, scale):
+    import scipy.sparse as sp
+    vals = rng_vals.normal(nrows * nnz_row) * scale
+    cols = np.minimum((rng_cols.uniform(nrows * nnz_row) * ncols).astype(np.int64), ncols - 1)
+    indptr = np.arange(0, nrows * nnz_row + 1, nnz_row, dtype=np.int64)
+    return sp.csr_matrix((vals, cols, indptr), shape=(nrows, ncols))
+
+
+def factored_qcqp(n: int = 1_000_000, mq: int = 64, rows: int = 100_000, nnz_row: int = 10,
+                  lin_rows: int = 500_000, lin_nnz: int = 5, seed: int = 0, box: float = 10.0,
+                  x0_scale: float = 1.0) -> FactoredArrays:
+    """BASELINE config 3 (defaults = full size).  Streams: R_i values on 4i
+    (N(0,1)/sqrt(nnz_row)), columns on 4i+1 (uniform), c_i on 4i+2
+    (N(0,1)/sqrt(n)), d_i = -U(1,2) on 4i+3 (d_0 = 0).  Linear block: values on
+    4(mq+1) (N(0,1)), columns on 4(mq+1)+1, x0 ~ U(-1,1) on 4(mq+1)+2,
+    b = A x0 + U(0,1) on 4(mq+1)+3.  Q_0 = R_0^T R_0 is an assumption (the
+    BASELINE text leaves the objective unspecified).
+    ``x0_scale`` shrinks x0 (parity cases use 0.2 so that x0 is strictly
+    feasible for the quadratic rows too; BASELINE's own text has 1)."""
+    import scipy.sparse as sp
+    blocks, C, d = [], np.empty((mq + 1, n)), np.zeros(mq + 1)
+    for i in range(mq + 1):
+        blocks.append(_csr_uniform(CounterRng(seed, 4 * i), CounterRng(seed, 4 * i + 1), rows, n, nnz_row,
+                                   1.0 / np.sqrt(nnz_row)))
+        C[i] = CounterRng(seed, 4 * i + 2).normal(n) / np.sqrt(n)
+        if i > 0:
+            d[i] = -float(CounterRng(seed, 4 * i + 3).uniform(1, 1.0, 2.0)[0])
+    R = sp.vstack(blocks, format="csr")
+    s = 4 * (mq + 1)
+    A = _csr_uniform(CounterRng(seed, s), CounterRng(seed, s + 1), lin_rows, n, lin_nnz, 1.0)
+    x0 = CounterRng(seed, s + 2).uniform(n, -1.0, 1.0) * x0_scale
+    b = A @ x0 + CounterRng(seed, s + 3).uniform(lin_rows, 0.0, 1.0)
+    return FactoredArrays(n=n, mq=mq, rows=rows, R=R, C=C, d=d, A=A, b=b,
+                          lower=np.full(n, -box), upper=np.full(n, box),
+                          name=f"factored-qcqp-n{n}-m{mq}-r{rows}-L{lin_rows}-s{seed}",
+                          meta={"generator": GENERATOR_NAME, "seed": seed, "nnz_row": nnz_row,
+                                "lin_nnz": lin_nnz})
+
+
+# BASELINE.json configs[0..2], [4]; config 3 (factored sparse) is factored_qcqp()
 CONFIGS = {
     "C0": dict(n=200, m=10, rank=20),
     "C1": dict(n=2000, m=200, rank=200),

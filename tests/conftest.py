@@ -48,3 +48,12 @@ def analytic_arrays(g, name):
     return dict(Q=g[f"{name}/Q"], q=g[f"{name}/q"], r=g[f"{name}/r"], A=g[f"{name}/A"],
                 b=g[f"{name}/b"], lower=g[f"{name}/lower"], upper=g[f"{name}/upper"],
                 mu=float(g[f"{name}/mu"]))
+
+
+@pytest.fixture(scope="session")
+def golden_factored():
+    return load_golden("factored_small")
+
+
+# tests/golden/make_golden.py FACTORED_SMALL (kept in sync by test_factored_fixture_instance)
+FACTORED_SMALL = dict(n=300, mq=4, rows=30, nnz_row=10, lin_rows=150, lin_nnz=5, seed=5, x0_scale=0.2)

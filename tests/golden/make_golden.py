@@ -229,6 +229,42 @@ def small_fixtures():
     save("kml_small", arrays, meta)
 
 
+def factored_fixtures():
+    """5. C3-shaped factored instance, small enough to densify: the reference is
+    given Q_i = R_i^T R_i explicitly (its _as_operator stores them as CSR) and
+    the linear rows as Q = 0 orthant constraints (FactoredArrays.dense_lists)."""
+    arr = instances.factored_qcqp(**FACTORED_SMALL)
+    Q, q, r = arr.dense_lists()
+    inst = rapdb.ProblemInstance(n=arr.n, m=arr.m, p=0, Q=Q, q=q, r=r, A=np.zeros((0, arr.n)),
+                                 b=np.zeros(0), primal_set=Box(arr.lower, arr.upper),
+                                 cone=NonnegOrthant(arr.m), mu=0.0, name=arr.name)
+    rng = np.random.default_rng(11)
+    x_probe = rng.uniform(-1, 1, arr.n)
+    lam_probe = np.maximum(rng.normal(size=arr.m), 0.0)
+    z = rapdb.Iterate(x_probe, np.zeros(0), lam_probe)
+    arrays = {
+        "R_checksum": np.array([float(arr.R.data.sum()), float(arr.R.indices.sum())]),
+        "A_checksum": np.array([float(arr.A.data.sum()), float(arr.A.indices.sum()), float(arr.b.sum())]),
+        "probe_x": x_probe, "probe_lam": lam_probe,
+        "probe_g": inst.g_value(x_probe), "probe_f": np.float64(inst.f_value(x_probe)),
+        "probe_gradx": rapdb.problem.grad_x_coupling(inst, z),
+    }
+    meta = {"instance": f"instances.factored_qcqp(**{FACTORED_SMALL})", "cases": {}}
+    for key, case in {"mono": dict(nm=False, policy={"kind": "none"}, budget=200),
+                      "nm": dict(nm=True, policy={"kind": "none"}, budget=200),
+                      "nm_fixed200": dict(nm=True, policy={"kind": "fixed", "period": 200},
+                                          budget=4000, eps=1e-6)}.items():
+        out, wall = run_case(inst, case, set(range(1, 201)))
+        for k, v in out.items():
+            arrays[f"{key}/{k}"] = v
+        meta["cases"][key] = dict(case, wall_s=wall)
+        print("factored", key, out["iterations"], out["converged"], round(wall, 2))
+    save("factored_small", arrays, meta)
+
+
+FACTORED_SMALL = dict(n=300, mq=4, rows=30, nnz_row=10, lin_rows=150, lin_nnz=5, seed=5, x0_scale=0.2)
+
+
 def c1_fixtures():
     arr = instances.config_instance("C1")
     t0 = time.time()
@@ -251,8 +287,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
+    ap.add_argument("--factored", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
         small_fixtures()
+    if a.factored:
+        factored_fixtures()
     if a.c1:
         c1_fixtures()

@@ -1,0 +1,148 @@
+"""Config-3 factored path (Q_i = R_i^T R_i + sparse linear rows) on the GPU,
+through the C ABI, against the reference's golden run of the densified
+instance and the oracle's factored restatement.
+
+Tolerances: the device sums CSR products in a different order than scipy
+(gathers over R and R^T, fixed warp/chunk trees), so traces agree to
+rounding, not bitwise: backtrack counts identical, step sizes to 1e-9
+relative, iterates to 1e-8 relative over 200 iterations.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import FACTORED_SMALL, load_golden
+import paper_2605_29291_b200 as R
+from paper_2605_29291_b200 import instances
+from paper_2605_29291_b200.factored import FactoredInstance
+from oracle import rapdb_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)) if b.size else 0.0
+
+
+def trace_arr(trace):
+    return np.array([[t.iter, t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total]
+                     for t in trace])
+
+
+def oracle_trace(P, nm, iters, mode="yx"):
+    # a few BLAS threads: with the default (one per host core) OpenBLAS spends
+    # milliseconds waking threads for every length-1e4+ dot product
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=4):
+        res = O.run_restarted(P, O.Options(mode=mode, nonmonotone=nm), O.Policy(kind="none"),
+                              budget=iters)
+    tr = np.array([[r.iter, r.tau_start, r.tau, r.sigma, r.gamma, r.evals_iter, r.evals_total]
+                   for r in res.trace])
+    return tr, res
+
+
+@pytest.fixture(scope="module")
+def small():
+    arr = instances.factored_qcqp(**FACTORED_SMALL)
+    return arr, FactoredInstance.from_arrays(arr), load_golden("factored_small")
+
+
+def test_factored_probe_and_gradient(small):
+    arr, inst, g = small
+    x, lam = g["probe_x"], g["probe_lam"]
+    f = float(g["probe_f"])
+    assert abs(inst.f_value(x) - f) <= 1e-12 * (1 + abs(f))
+    np.testing.assert_allclose(inst.g_value(x), g["probe_g"], rtol=1e-12, atol=1e-12)
+    gx = R.grad_x_coupling(inst, R.Iterate(x, np.zeros(0), lam))
+    assert rel(gx, g["probe_gradx"]) <= 1e-12
+    # the W-cache itself: W = R x
+    u, _ = inst._evaluator().sweep(x)
+    assert rel(u.cpu().numpy(), arr.R @ x) <= 1e-13
+
+
+@pytest.mark.parametrize("key,nm", [("mono", False), ("nm", True)])
+def test_factored_200_vs_reference(small, key, nm):
+    arr, inst, g = small
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.initial_iterate(inst))
+    snaps = list(g[f"{key}/snap_iters"])
+    done = 0
+    for k in (1, 10, 50, 100, 200):
+        eng.run_block(k - done)
+        done = k
+        z = eng.last
+        idx = snaps.index(k)
+        assert rel(z.x, g[f"{key}/snap_x"][idx]) <= 1e-8, k
+        assert rel(z.lam, g[f"{key}/snap_lam"][idx]) <= 1e-8, k
+    tr = trace_arr(eng.trace)
+    tg = g[f"{key}/trace"]
+    np.testing.assert_array_equal(tr[:, 5], tg[:, 5])
+    np.testing.assert_allclose(tr[:, 1:5], tg[:, 1:5], rtol=1e-9)
+    assert rel(eng.average().x, g[f"{key}/avg_x"]) <= 1e-8
+
+
+def test_factored_xy_vs_oracle(small):
+    arr, inst, _ = small
+    tr_o, res = oracle_trace(O.factored_problem(arr), True, 150, mode="xy")
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="xy", nonmonotone=True), R.initial_iterate(inst))
+    eng.run_block(150)
+    tr = trace_arr(eng.trace)
+    np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
+    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    assert rel(eng.last.x, res.x) <= 1e-8
+
+
+def test_factored_fixed_restart_kkt(small):
+    """run_restarted with device FixedRestart(200) and KKT every 10 iterations
+    over the reference's 4000-iteration budget (the instance is degenerate --
+    neither side reaches 1e-6): same stop, KKT residual within a factor 2."""
+    arr, inst, g = small
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(200),
+                          budget=4000, criteria=R.TerminationCriteria(criterion="conic", eps_kkt=1e-6,
+                                                                      eps_feas=1e-6))
+    assert res.iterations == int(g["nm_fixed200/iterations"])
+    assert bool(res.converged) == bool(g["nm_fixed200/converged"])
+    k_ref = float(g["nm_fixed200/metrics"][0])
+    assert 0.5 * k_ref <= res.metrics.kkt_residual <= 2.0 * k_ref
+    # device KKT at the final point vs the host-side evaluation of the same point
+    m = R.kkt_residual(inst, res.solution)
+    P = O.factored_problem(arr)
+    mo = O.kkt(P, res.solution.x, np.zeros(0), res.solution.lam)
+    assert abs(m.kkt_residual - mo.kkt_residual) <= 1e-9 * (1 + mo.kkt_residual)
+    assert abs(m.f_value - mo.f_value) <= 1e-11 * (1 + abs(mo.f_value))
+
+
+SHAPES = [
+    dict(n=1000, mq=0, rows=100, nnz_row=10, lin_rows=500, lin_nnz=5, seed=2, x0_scale=0.1),   # objective only
+    dict(n=2000, mq=3, rows=50, nnz_row=10, lin_rows=0, lin_nnz=5, seed=3),                     # no linear block
+    dict(n=1025, mq=2, rows=1030, nnz_row=7, lin_rows=7, lin_nnz=3, seed=4, x0_scale=0.05),     # ragged chunks
+    dict(n=50_000, mq=8, rows=5000, nnz_row=10, lin_rows=20_000, lin_nnz=5, seed=1, x0_scale=0.02),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=["mq0", "L0", "ragged", "n50k"])
+@pytest.mark.parametrize("nm", [False, True])
+def test_factored_shapes_vs_oracle(shape, nm):
+    arr = instances.factored_qcqp(**shape)
+    inst = FactoredInstance.from_arrays(arr)
+    iters = 60
+    tr_o, res = oracle_trace(O.FactoredProblem(arr), nm, iters)
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.initial_iterate(inst))
+    eng.run_block(iters)
+    tr = trace_arr(eng.trace)
+    np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
+    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    z = eng.last
+    assert rel(z.x, res.x) <= 1e-8
+    if arr.m:
+        assert rel(z.lam, res.lam) <= 1e-8
+    np.testing.assert_allclose(inst.g_value(z.x), O.FactoredProblem(arr).g(z.x), rtol=1e-10, atol=1e-10)
+
+
+def test_factored_rejects_unsupported(small):
+    arr, inst, _ = small
+    from paper_2605_29291_b200.geometry import JointBall
+    with pytest.raises(R.ConfigurationError):
+        R.ApdbEngine(inst, R.SolverConfig(dual_ball=JointBall(5.0)), R.initial_iterate(inst))
+    with pytest.raises(R.ConfigurationError):
+        R.run_restarted(inst, R.SolverConfig(), R.AdaptiveRestart(warmup=5, check_period=5), budget=30)
