@@ -125,6 +125,30 @@ int rapdb_bind_dense(rapdb_ctx* ctx, int n, int m, int p, int k0, int k1, long l
                      const double* lower, const double* upper, double mu,
                      const unsigned char* zero_flags);
 
+/* Packed symmetric layout of the same stack (the default of the Python
+ * binding).  Every Q_i is symmetric (the reference validates it at load time,
+ * problem.py:142-144), so only the upper block triangle is stored and
+ * streamed: half the HBM bytes of the row-major stack.  Qp is the local shard
+ * [k1-k0][rapdb_packed_doubles(n)] built by rapdb_pack_symmetric; every other
+ * argument is as for rapdb_bind_dense.  Layout: 32 x 32 row-major sub-tiles in
+ * 64 x 64 units, units block-row-major over Bi <= Bj, diagonal units storing
+ * (0,0), (0,1), (1,1) (paper_2605_29291_b200/csrc/symsweep.cuh).             */
+int rapdb_bind_dense_packed(rapdb_ctx* ctx, int n, int m, int p, int k0, int k1,
+                            const double* Qp, const double* q, const double* r,
+                            const double* A, const double* b,
+                            const double* lower, const double* upper, double mu,
+                            const unsigned char* zero_flags);
+
+/* doubles of one packed n x n matrix (upper block triangle incl. zero padding) */
+long long rapdb_packed_doubles(int n);
+
+/* Pack `count` dense n x n matrices (row stride ld, matrix stride mat_stride
+ * doubles) into the packed layout at dst (device).  src may be device memory
+ * or page-locked host memory (read through the unified address space, so only
+ * the upper triangle crosses PCIe).  Runs on `stream` and synchronises it.  */
+int rapdb_pack_symmetric(int n, long long count, const double* src, long long ld,
+                         long long mat_stride, double* dst, void* stream);
+
 /* Factored sparse problem data (BASELINE config 3): replaces a ProblemInstance
  * whose Q_i are sparse operators (_as_operator problem.py:31-40 keeps them as
  * CSR) with Q_i = R_i^T R_i, plus L linear inequality rows a_j x <= b_j that

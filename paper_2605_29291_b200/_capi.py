@@ -46,7 +46,8 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_dense", "rapdb_set_params", "rapdb_workspace_bytes", "rapdb_bind_workspace",
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
-           "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x"]
+           "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x",
+           "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
@@ -61,6 +62,20 @@ X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
 def launch_count() -> int:
     """Kernel launches issued by the native library in this process."""
     return int(load().rapdb_launch_count())
+
+
+def packed_doubles(n: int) -> int:
+    """Doubles of one packed (upper block triangle) n x n matrix."""
+    return int(load().rapdb_packed_doubles(int(n)))
+
+
+def pack_symmetric(n: int, count: int, src_ptr: int, ld: int, mat_stride: int, dst_ptr: int, stream_ptr: int):
+    """Pack `count` dense matrices (device or page-locked host memory) into the
+    packed symmetric layout at dst (device); synchronises the stream."""
+    code = load().rapdb_pack_symmetric(int(n), int(count), C.c_void_p(src_ptr), int(ld), int(mat_stride),
+                                       C.c_void_p(dst_ptr), C.c_void_p(stream_ptr))
+    if code != 0:
+        raise DeviceError(f"rapdb_pack_symmetric failed (code {code})")
 
 
 def load(path: str = LIB_PATH):
@@ -80,6 +95,10 @@ def load(path: str = LIB_PATH):
     lib.rapdb_last_error.argtypes = [P, C.c_char_p, I]
     lib.rapdb_set_stream.argtypes = [P, P]
     lib.rapdb_bind_dense.argtypes = [P, I, I, I, I, I, LL, P, P, P, P, P, P, P, D, P]
+    lib.rapdb_bind_dense_packed.argtypes = [P, I, I, I, I, I, P, P, P, P, P, P, P, D, P]
+    lib.rapdb_packed_doubles.argtypes = [I]
+    lib.rapdb_packed_doubles.restype = LL
+    lib.rapdb_pack_symmetric.argtypes = [I, LL, P, LL, LL, P, P]
     lib.rapdb_set_params.argtypes = [P, I, D, D, D, D, D, D, I, I, I, D, D]
     lib.rapdb_workspace_bytes.argtypes = [P]
     lib.rapdb_workspace_bytes.restype = LL
@@ -212,11 +231,15 @@ class Context:
         else:
             k1 = data.m + 1 if k1 is None else k1
             zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)
-            self._check(self.lib.rapdb_bind_dense(
-                self.h, data.n, data.m, data.p, k0, k1, data.ld,
-                _ptr(data.Q), _ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
-                _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
-                zero.ctypes.data_as(C.c_void_p)))
+            tail = (_ptr(data.q), _ptr(data.r), _ptr(data.A) if data.p else None,
+                    _ptr(data.b) if data.p else None, _ptr(data.lower), _ptr(data.upper), float(data.mu),
+                    zero.ctypes.data_as(C.c_void_p))
+            if getattr(data, "layout", "rows") == "packed":
+                self._check(self.lib.rapdb_bind_dense_packed(
+                    self.h, data.n, data.m, data.p, k0, k1, _ptr(data.Q), *tail))
+            else:
+                self._check(self.lib.rapdb_bind_dense(
+                    self.h, data.n, data.m, data.p, k0, k1, data.ld, _ptr(data.Q), *tail))
         self._set_params(cfg)
         nbytes = int(self.lib.rapdb_workspace_bytes(self.h))
         if nbytes <= 0:

@@ -183,7 +183,58 @@ __device__ int g_hpart(const KArgs& K, Sm& S, int& xk) {
     // this rank's share: Q0 if held (and not all-zero), then its local Q_i
     const bool q0 = P.k0 == 0 && __ldg(P.mat_slot) >= 0;
     const int i_lo = P.k0 == 0 ? 1 : P.k0;
-    for (long long r = gw; r < n; r += nw) {
+    if (K.sp.layout == 1) {
+      // packed stack: one stored 32 x 32 sub-tile per warp (lane l = column l),
+      // the mirrored lower sub-tile written through a per-warp shared transpose
+      const sym::Geom& g = K.sp.geom;
+      const long long mat_doubles = g.spm * sym::kTD;
+      const long long toff = ((long long)m * 8 + 255) / 256 * 256;
+      double* tb = reinterpret_cast<double*>(S.ring + toff) + (threadIdx.x >> 5) * (32 * 33);
+      for (long long it = gw; it < g.spm; it += nw) {
+        int lo = 0, hi = g.upm - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (K.sp.units[mid].off <= it) lo = mid; else hi = mid - 1;
+        }
+        const sym::Unit un = K.sp.units[lo];
+        int rs, cs, sr, sc;
+        sym::unit_subtiles(g, un.bi, un.bj, rs, cs);
+        sym::unit_sub(un.bi == un.bj, cs, (int)(it - un.off), sr, sc);
+        const int R0 = (2 * un.bi + sr) * 32, C0 = (2 * un.bj + sc) * 32;
+        double h[32];
+        if (q0) {
+          const double* t = P.Q + it * sym::kTD + lane;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) h[r] = __ldg(t + r * 32);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) h[r] = 0.0;
+        }
+        for (int i = i_lo; i < P.k1; ++i) {
+          const double l = lam_s[i - 1];
+          if (l == 0.0 || __ldg(P.mat_slot + (i - P.k0)) < 0) continue;   // diagnostics.py:146
+          const double* t = P.Q + (long long)(i - P.k0) * mat_doubles + it * sym::kTD + lane;
+          double qv[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) qv[r] = __ldg(t + r * 32);
+#pragma unroll
+          for (int r = 0; r < 32; ++r) h[r] = h[r] + l * qv[r];
+        }
+        const int c = C0 + lane;
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          if (R0 + r < n && c < n) H[(long long)(R0 + r) * n + c] = h[r];
+        if (R0 != C0) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) tb[r * 33 + lane] = h[r];
+          __syncwarp();
+          for (int rr = 0; rr < 32; ++rr)
+            if (C0 + rr < n && R0 + lane < n) H[(long long)(C0 + rr) * n + R0 + lane] = tb[lane * 33 + rr];
+          __syncwarp();
+        }
+      }
+    }
+    for (long long r = gw; r < n && K.sp.layout == 0; r += nw) {
       for (int cb = 0; cb < n; cb += 32 * KC) {
         double h[KC];
 #pragma unroll

@@ -1,7 +1,8 @@
 // rapdb_dev.cuh -- device data structures and primitives of the B200 rAPDB path.
 //
 // Layout in HBM (one context, single rank shard [k0, k1) of the m+1 matrices):
-//   Q     [nloc][n][ld]   fp64, row-major, ld even (16-B rows for bulk copies)
+//   Q     [nloc][n][ld]   fp64, row-major, ld even (16-B rows for bulk copies), or
+//         [nloc][spm][32][32] packed upper block triangle (layout 1, symsweep.cuh)
 //   q     [m+1][n], r [m+1], A [p][n], b [p], lower/upper [n]
 //   x     [2][n]          parity `cur` = accepted x_k, `cur^1` = trial x_new
 //   U     [2][nloc][n]    u_i = Q_i x for both parities (the U-cache)
@@ -15,6 +16,8 @@
 //   xcum  [n], ycum [p+m] ergodic accumulators (engine.py:244-249)
 //   part  [NSLOT][G]      per-CTA partial sums (fixed-order grid reductions)
 //   segxu/segqx [G][8][segmax]  per-(CTA, warp, matrix-segment) x.u and q.x sums
+//               (packed layout: [nact][nbB] per-(matrix, 64-row block) sums)
+//   Pt    [nact][nbB][nbB][64]  packed layout: unit partial products (symsweep.cuh)
 //
 // All arithmetic is IEEE binary64.  The file is compiled with -fmad=false so
 // scalar control reproduces the reference's Python-float operation order
@@ -23,11 +26,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "symsweep.cuh"
+
 namespace rapdb {
 
-constexpr int kThreads = 288;      // 8 consumer warps + 1 bulk-copy producer warp
-constexpr int kConsumerWarps = 8;
-constexpr int kWarps = 9;
+constexpr int kThreads = 256;      // 7 consumer warps + 1 bulk-copy producer warp (2 warps per SMSP: 255-register cap)
+constexpr int kConsumerWarps = 7;
+constexpr int kWarps = 8;
 constexpr int kMaxTR = 32;         // rows per tile upper bound
 
 enum Slot {
@@ -122,6 +127,10 @@ struct SweepPlan {
   long long stage_bytes; // per ring slot (multiple of 128)
   long long rows_total;  // nact * n
   long long xs_bytes;    // x staging bytes (multiple of 128)
+  int layout;            // 0 row-major stack [nloc][n][ld], 1 packed symmetric (symsweep.cuh)
+  int pad4;
+  sym::Geom geom;        // layout 1: unit geometry of one matrix
+  const sym::Unit* units;  // layout 1: [upm] unit table (device)
 };
 
 struct Work {
@@ -130,6 +139,7 @@ struct Work {
   double *H, *hx, *hxn, *hy;   // smoothed gap: dense H (n x n) and H-products
   double *W;                   // factored: [2][nr] W = R x at both parities
   double *pw2, *pcx;           // factored: chunk partials of |W_i|^2 and c_i . x
+  double *Pt;                  // layout 1: per-unit partial products [nact][nbB][nbB][64]
   double* trace;
   SolverState* st;
   unsigned long long* bar;

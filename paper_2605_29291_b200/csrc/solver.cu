@@ -343,6 +343,7 @@ struct rapdb_ctx {
   Work w{};
   int* d_ints = nullptr;
   long long* d_ll = nullptr;   // factored: rblk and W-chunk prefix tables
+  sym::Unit* d_units = nullptr;  // packed layout: unit table
   long long ws_bytes = 0;
   long long stage_cap = 0;  // doubles available in the staging area
   bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
@@ -383,7 +384,7 @@ struct Layout {
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
-             B_W, B_PW2, B_PCX, B_COUNT };
+             B_W, B_PW2, B_PCX, B_PT, B_COUNT };
 static_assert(B_COUNT <= B_COUNT_MAX, "Layout::off too small");
 
 Layout layout_of(const rapdb_ctx* c) {
@@ -402,8 +403,11 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_XCUM] = n * 8;
   sz[B_YCUM] = std::max(np, 1LL) * 8;
   sz[B_PART] = (long long)NSLOT * G * 8;
-  sz[B_SEGXU] = G * kConsumerWarps * c->sp.segmax * 8;
-  sz[B_SEGQX] = G * kConsumerWarps * c->sp.segmax * 8;
+  const bool packed = c->sp.layout == 1;
+  const long long nseg = packed ? std::max(1LL, (long long)c->P.nact * c->sp.geom.nbB)
+                                : G * kConsumerWarps * c->sp.segmax;
+  sz[B_SEGXU] = nseg * 8;
+  sz[B_SEGQX] = nseg * 8;
   sz[B_ZQ] = std::max(c->P.nzero, 1) * 8LL;
   sz[B_AUX] = n * 8;
   sz[B_AUX2] = n * 8;
@@ -418,6 +422,7 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_W] = fac ? 2 * c->P.nr * 8 : 8;
   sz[B_PW2] = fac ? std::max(c->nchw, 1LL) * 8 : 8;
   sz[B_PCX] = fac ? (long long)(c->P.mq + 1) * c->P.nchx * 8 : 8;
+  sz[B_PT] = packed ? std::max(1LL, (long long)c->P.nact) * c->sp.geom.nbB * c->sp.geom.nbB * sym::kB * 8 : 8;
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -618,6 +623,7 @@ void rapdb_destroy(rapdb_ctx* c) {
   if (!c) return;
   if (c->d_ints) cudaFree(c->d_ints);
   if (c->d_ll) cudaFree(c->d_ll);
+  if (c->d_units) cudaFree(c->d_units);
   delete c;
 }
 
@@ -633,13 +639,62 @@ int rapdb_set_stream(rapdb_ctx* c, void* s) {
   return RAPDB_OK;
 }
 
+namespace {
+int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k1, long long ld, const double* Q,
+                    const double* q, const double* r, const double* A, const double* b,
+                    const double* lower, const double* upper, double mu, const unsigned char* zero_flags);
+}
+
 int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long long ld, const double* Q,
                      const double* q, const double* r, const double* A, const double* b,
                      const double* lower, const double* upper, double mu, const unsigned char* zero_flags) {
+  return bind_dense_impl(c, 0, n, m, p, k0, k1, ld, Q, q, r, A, b, lower, upper, mu, zero_flags);
+}
+
+int rapdb_bind_dense_packed(rapdb_ctx* c, int n, int m, int p, int k0, int k1, const double* Qp,
+                            const double* q, const double* r, const double* A, const double* b,
+                            const double* lower, const double* upper, double mu, const unsigned char* zero_flags) {
+  return bind_dense_impl(c, 1, n, m, p, k0, k1, n + (n & 1), Qp, q, r, A, b, lower, upper, mu, zero_flags);
+}
+
+long long rapdb_packed_doubles(int n) {
+  if (n <= 0) return -1;
+  return sym::make_geom(n).spm * sym::kTD;
+}
+
+int rapdb_pack_symmetric(int n, long long count, const double* src, long long ld, long long mat_stride,
+                         double* dst, void* stream) {
+  if (n <= 0 || count < 0 || ld < n || mat_stride < (long long)n * ld - (ld - n) || !src || !dst) return RAPDB_EINPUT;
+  if (count == 0) return RAPDB_OK;
+  const sym::Geom g = sym::make_geom(n);
+  std::vector<sym::Unit> hu(g.upm);
+  sym::fill_units(g, hu.data());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  sym::Unit* du = nullptr;
+  if (cudaMallocAsync(&du, hu.size() * sizeof(sym::Unit), st) != cudaSuccess) return RAPDB_EDEVICE;
+  if (cudaMemcpyAsync(du, hu.data(), hu.size() * sizeof(sym::Unit), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return RAPDB_EDEVICE;
+  for (long long a0 = 0; a0 < count; a0 += 65535) {
+    const int cnt = (int)std::min(65535LL, count - a0);
+    sym::pack_kernel<<<dim3(g.upm, cnt), 256, 0, st>>>(g, du, src + a0 * mat_stride, ld, mat_stride,
+                                                         dst + a0 * g.spm * sym::kTD);
+    ++g_launches;
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(du, st);
+  if (e != cudaSuccess) return RAPDB_EDEVICE;
+  return cudaStreamSynchronize(st) == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+namespace {
+int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k1, long long ld, const double* Q,
+                    const double* q, const double* r, const double* A, const double* b,
+                    const double* lower, const double* upper, double mu, const unsigned char* zero_flags) {
   if (!c) return RAPDB_EINPUT;
   if (n <= 0 || m < 0 || p < 0) return fail(c, RAPDB_EINPUT, "need n > 0, m >= 0, p >= 0");
   if (k0 < 0 || k1 > m + 1 || k1 <= k0) return fail(c, RAPDB_EINPUT, "bad local matrix range");
   if (ld < n || (ld & 1)) return fail(c, RAPDB_EINPUT, "ld must be even and >= n");
+  if (layout == 1 && n > 32767 * 64) return fail(c, RAPDB_EINPUT, "n too large for the packed layout");
   if (c->nranks == 1 && (k0 != 0 || k1 != m + 1) && !c->split)
     return fail(c, RAPDB_EINPUT, "a single-rank context must hold all m+1 matrices (or be split)");
   if (c->nranks > 1) c->split = 1;
@@ -688,6 +743,17 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
     sp.stage_bytes = align_up((long long)sp.chunk * 8, 128);
   }
   sp.xs_bytes = align_up(row_bytes, 128);
+  sp.layout = layout;
+  if (layout == 1) {
+    // packed symmetric stack: one unit (<= 4 sub-tiles, 32 KB) per ring slot,
+    // x staged zero-padded to whole 64-row blocks
+    sp.geom = sym::make_geom(n);
+    sp.TR = 1;
+    sp.cpr = 1;
+    sp.chunk = (int)ld;
+    sp.stage_bytes = 4LL * sym::kTD * 8;
+    sp.xs_bytes = align_up((long long)sp.geom.nbB * sym::kB * 8, 128);
+  }
   const char* env_rc = std::getenv("RAPDB_RC_COLS");
   sp.rc_cols = env_rc ? std::atoi(env_rc) : (k1 - k0 >= 24 ? 1 : 0);
   cudaFuncAttributes fa{};
@@ -696,7 +762,7 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
     static_smem = (long long)fa.sharedSizeBytes;
   const long long budget = (long long)c->optin - static_smem - 2048;
   long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
-  ns = std::min(ns, max_stages);
+  ns = std::min(ns, layout == 1 ? std::min(max_stages, 8LL) : max_stages);
   if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense path (x does not fit in shared memory)");
   sp.nstages = (int)ns;
   sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
@@ -705,6 +771,8 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   // smoothed gap: five shared n-vectors + staged multipliers in xs+ring, and a
   // dense n x n H in the workspace (skipped for very large n)
   c->gap_ok = (5LL * n + m + p + m + 64) * 8 <= sp.xs_bytes + ns * sp.stage_bytes && n <= 16384;
+  if (layout == 1)   // per-warp 32 x 33 transpose buffers after the staged multipliers (gap.cuh)
+    c->gap_ok = c->gap_ok && align_up((long long)m * 8, 256) + kWarps * 32LL * 33 * 8 <= ns * sp.stage_bytes;
   if (2LL * (p + m) > c->stage_cap)
     return fail(c, RAPDB_ECONFIG, "too many multipliers for the shared-memory dual staging area");
   cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
@@ -758,11 +826,23 @@ int rapdb_bind_dense(rapdb_ctx* c, int n, int m, int p, int k0, int k1, long lon
   c->P = P;
   c->sp = sp;
   c->sweep_bytes = R * (long long)n * 8;
+  if (layout == 1) {
+    // the unit table rides in its own allocation (8-byte entries)
+    if (c->d_units) cudaFree(c->d_units);
+    c->d_units = nullptr;
+    std::vector<sym::Unit> hu(sp.geom.upm);
+    sym::fill_units(sp.geom, hu.data());
+    CK(cudaMalloc(&c->d_units, hu.size() * sizeof(sym::Unit)));
+    CK(cudaMemcpy(c->d_units, hu.data(), hu.size() * sizeof(sym::Unit), cudaMemcpyHostToDevice));
+    c->sp.units = c->d_units;
+    c->sweep_bytes = (long long)act.size() * sp.geom.spm * sym::kTD * 8;   // packed bytes streamed
+  }
   c->nchw = 0;
   c->bound = true;
   c->have_ws = false;
   return RAPDB_OK;
 }
+}  // namespace
 
 int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const long long* r_ptr, const int* r_col,
                         const double* r_val, const long long* rt_ptr, const int* rt_row, const double* rt_val,
@@ -882,6 +962,7 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.W = D(B_W);
   w.pw2 = D(B_PW2);
   w.pcx = D(B_PCX);
+  w.Pt = D(B_PT);
   w.trace = nullptr;
   w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);

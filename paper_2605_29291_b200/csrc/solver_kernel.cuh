@@ -140,7 +140,156 @@ __device__ __forceinline__ double rowdot(const double* row, const double* xs, lo
 // dots it with the staged x and releases the slot.  There is no CTA-wide
 // barrier per tile, so the ring keeps nstages*stage_bytes of HBM reads in
 // flight per SM; chunk partials of a row are summed in chunk order.
-__device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
+// equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
+__device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par) {
+  const DevProblem& P = K.P;
+  const int n = P.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long items = (long long)P.p + P.nzero;
+  for (long long it = (long long)blockIdx.x * kWarps + warp; it < items; it += (long long)gridDim.x * kWarps) {
+    const double* vec = it < P.p ? P.A + it * n : P.q + (long long)(P.k0 + __ldg(P.zero_list + (it - P.p))) * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(__ldg(vec + j), S.xs[j], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (it < P.p) K.w.eqv[(long long)par * P.p + it] = s - __ldg(P.b + it);
+      else K.w.zq[it - P.p] = s;
+    }
+  }
+}
+
+// The packed-symmetric sweep (layout 1, symsweep.cuh): stream the upper block
+// triangle of every streamed matrix (round-robin units over the CTAs, TMA
+// bulk copies into the ring, one consumer warp per unit) into the unit
+// partials Pt; grid barrier; then reduce Pt in fixed order into the U-cache
+// and the per-(matrix, 64-row block) x.u and q.x sums that g_combine adds.
+__device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc, int par) {
+  const DevProblem& P = K.P;
+  const SweepPlan& sp = K.sp;
+  const sym::Geom& g = sp.geom;
+  const int n = P.n;
+  const int xlen = g.nbB * sym::kB;
+  for (int j = threadIdx.x; j < xlen; j += kThreads) S.xs[j] = (j < n) ? ldcg(xsrc + j) : 0.0;
+  // generic-proxy use of the ring (dual staging) before the bulk copies below
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long total = (long long)P.nact * g.upm;
+  const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncw = sp.ncw;
+  const unsigned base = S.pseq;
+  const unsigned ns = (unsigned)sp.nstages;
+  const long long mat_doubles = g.spm * sym::kTD;
+  const long long pstride = (long long)g.nbB * g.nbB * sym::kB;
+  const int upm = g.upm;
+  // hoisted into registers: S is a by-reference local (stack) object and every
+  // S.field access in the loops below would otherwise be a local-memory load
+  unsigned char* const ring = S.ring;
+  uint64_t* const fullb = S.full;
+  uint64_t* const emptyb = S.empty;
+  const double* const xs = S.xs;
+  int* const abort_flag = K.w.abort_flag;
+  double* const Pt = K.w.Pt;
+  const sym::Unit* const units = sp.units;
+  const long long stage_bytes = sp.stage_bytes;
+  const int* const act = P.act;
+  const double* const Qst = P.Q;
+  const sym::Geom gg = g;
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      long long a = b / upm;
+      int u = (int)(b - a * upm);
+      unsigned s = base % ns, use = base / ns;
+      for (long long k = 0; k < mine; ++k) {
+        if (use > 0 && !mbar_wait(&emptyb[s], (use - 1) & 1, abort_flag)) break;
+        const sym::Unit un = units[u];
+        int rs, cs;
+        const unsigned bytes = (unsigned)sym::unit_subtiles(gg, un.bi, un.bj, rs, cs) * sym::kTD * 8u;
+        mbar_expect_tx(&fullb[s], bytes);
+        bulk_g2s(ring + (long long)s * stage_bytes,
+                 Qst + (long long)__ldg(act + a) * mat_doubles + (long long)un.off * sym::kTD, bytes,
+                 &fullb[s], pol);
+        u += G;
+        while (u >= upm) { u -= upm; ++a; }
+        if (++s == ns) { s = 0; ++use; }
+      }
+    }
+  } else if (warp < ncw) {
+    const long long gi = b + (long long)warp * G;
+    long long a = gi / upm;
+    int u = (int)(gi - a * upm);
+    unsigned s = (base + warp) % ns, use = (base + warp) / ns;
+    const int adv = ncw * G;
+    for (long long k = warp; k < mine; k += ncw) {
+      if (!mbar_wait(&fullb[s], use & 1, abort_flag)) break;
+      const sym::Unit un = units[u];
+      sym::consume_unit(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xs,
+                        un.bi, un.bj, Pt + a * pstride);
+      // generic-proxy reads of the slot before the producer's next bulk write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyb[s]);
+      u += adv;
+      while (u >= upm) { u -= upm; ++a; }
+      s += ncw;
+      while (s >= ns) { s -= ns; ++use; }
+    }
+  }
+  S.pseq = base + (unsigned)mine;
+  if (!gsync(K, S)) return;   // aborted: the caller's barrier reports it
+  // phase B: u = sum_K Pt[a][B][K] (K order), U-cache rows, block x.u and q.x
+  const int nbB = g.nbB;
+  const long long items = (long long)P.nact * nbB;
+  double* U = K.w.U + (long long)par * P.nloc * n;
+  for (long long it = (long long)b * kWarps + warp; it < items; it += (long long)G * kWarps) {
+    const int a = (int)(it / nbB);
+    const int B = (int)(it - (long long)a * nbB);
+    const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
+    double sx = 0.0, sy = 0.0;
+    int kk = 0;
+    for (; kk + 4 <= nbB; kk += 4) {
+      const double2 t0 = __ldcg(pp + (kk + 0) * 32), t1 = __ldcg(pp + (kk + 1) * 32);
+      const double2 t2 = __ldcg(pp + (kk + 2) * 32), t3 = __ldcg(pp + (kk + 3) * 32);
+      sx += t0.x; sy += t0.y;
+      sx += t1.x; sy += t1.y;
+      sx += t2.x; sy += t2.y;
+      sx += t3.x; sy += t3.y;
+    }
+    for (; kk < nbB; ++kk) {
+      const double2 t = __ldcg(pp + kk * 32);
+      sx += t.x; sy += t.y;
+    }
+    const int lm = __ldg(P.act + a);
+    const double* qa = P.q + (long long)(P.k0 + lm) * n;
+    const int r = B * sym::kB + 2 * lane;
+    double xu = 0.0, qx = 0.0;
+    if (r < n) {
+      U[(long long)lm * n + r] = sx;
+      xu = xs[r] * sx;
+      qx = __ldg(qa + r) * xs[r];
+    }
+    if (r + 1 < n) {
+      U[(long long)lm * n + r + 1] = sy;
+      xu = xu + xs[r + 1] * sy;
+      qx = qx + __ldg(qa + r + 1) * xs[r + 1];
+    }
+    xu = warp_sum(xu);
+    qx = warp_sum(qx);
+    if (lane == 0) {
+      K.w.segxu[it] = xu;
+      K.w.segqx[it] = qx;
+    }
+  }
+  sweep_tail(K, S, par);
+}
+
+__device__ __noinline__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
+  if (K.sp.layout == 1) {
+    sweep_sym(K, S, xsrc, par);
+    return;
+  }
   const DevProblem& P = K.P;
   const SweepPlan& sp = K.sp;
   const int n = P.n;
@@ -380,18 +529,7 @@ __device__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
   }
   S.pseq = base + (unsigned)ntiles;
   __syncthreads();
-  // equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
-  const long long items = (long long)P.p + P.nzero;
-  for (long long it = (long long)b * kWarps + warp; it < items; it += (long long)G * kWarps) {
-    const double* vec = it < P.p ? P.A + it * n : P.q + (long long)(P.k0 + __ldg(P.zero_list + (it - P.p))) * n;
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(__ldg(vec + j), S.xs[j], s);
-    s = warp_sum(s);
-    if (lane == 0) {
-      if (it < P.p) K.w.eqv[(long long)par * P.p + it] = s - __ldg(P.b + it);
-      else K.w.zq[it - P.p] = s;
-    }
-  }
+  sweep_tail(K, S, par);
 }
 
 // g_i (i = 0..m, i = 0 is f) from the sweep's segment sums: 0.5*x.u + q.x + r
@@ -404,6 +542,14 @@ __device__ __forceinline__ double g_combine(const KArgs& K, int i) {
   if (slot < 0) {
     sxu = 0.0;
     sqx = ldcg(K.w.zq + (-slot - 1));
+  } else if (K.sp.layout == 1) {
+    const int nbB = K.sp.geom.nbB;
+    sxu = 0.0;
+    sqx = 0.0;
+    for (int B = 0; B < nbB; ++B) {
+      sxu += ldcg(K.w.segxu + (long long)slot * nbB + B);
+      sqx += ldcg(K.w.segqx + (long long)slot * nbB + B);
+    }
   } else {
     const int lo = __ldg(P.seg_lo + slot), hi = __ldg(P.seg_hi + slot);
     sxu = 0.0;
@@ -431,6 +577,15 @@ __device__ __forceinline__ double g_combine_warp(const KArgs& K, int i) {
   double sxu = 0.0, sqx = 0.0;
   if (slot < 0) {
     sqx = ldcg(K.w.zq + (-slot - 1));
+  } else if (K.sp.layout == 1) {
+    const int nbB = K.sp.geom.nbB;
+    double ax = 0.0, aq = 0.0;
+    for (int B = lane; B < nbB; B += 32) {
+      ax += ldcg(K.w.segxu + (long long)slot * nbB + B);
+      aq += ldcg(K.w.segqx + (long long)slot * nbB + B);
+    }
+    sxu = warp_sum(ax);
+    sqx = warp_sum(aq);
   } else {
     const int lo = __ldg(P.seg_lo + slot), hi = __ldg(P.seg_hi + slot);
     const int ncw = K.sp.ncw;

@@ -1,0 +1,208 @@
+// symsweep.cuh -- packed-symmetric Q-stack sweep (sm_100a, fp64).
+//
+// Every Q_i is symmetric (the reference validates it, problem.py:142-144), so
+// the sweep streams only the upper block triangle: half the HBM bytes of the
+// row-major stack.  Layout of one matrix (the "packed" stack, [nloc][spm][32][32]):
+//   32 x 32 sub-tiles (8 KB, row-major) grouped into 64 x 64 "units", units in
+//   block-row-major order over the upper triangle (Bi <= Bj).  An off-diagonal
+//   unit holds its rs x cs sub-tiles (rs, cs = 2 except at a ragged edge) in
+//   row-major order; a diagonal unit holds (0,0), (0,1), (1,1) -- the (1,0)
+//   sub-tile is the transpose of (0,1).  Rows/columns beyond n are zero.
+// One unit is one contiguous 1-D bulk copy (8-32 KB).
+//
+// Sweep = two phases separated by a grid barrier:
+//   A  stream: CTA b takes global units b, b+G, b+2G, ... (round-robin, so
+//      all CTAs work on the same few matrices at a time and the partials stay
+//      L2-resident).  A consumer warp computes, for off-diagonal unit (Bi, Bj):
+//        R = U_blk x[Bj]      (row contribution to u[Bi], 64 values)
+//        C = U_blk^T x[Bi]    (column contribution to u[Bj], 64 values)
+//      C is lane-local (lane l owns column l); R is formed by a butterfly
+//      transpose-reduction of 32 per-lane products.  Diagonal units give the
+//      full D x[Bi].  Each result lands in its own slot of
+//        Pt[a][B][K][64]: K < B: C of unit (K, B); K = B: diagonal; K > B: R
+//      of unit (B, K) -- every slot written exactly once.
+//   B  reduce: u[a][B*64 + r] = sum_K Pt[a][B][K][r] in K order -- a fixed
+//      order independent of the grid, so results are bitwise reproducible and
+//      independent of how units were assigned to CTAs or ranks.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rapdb {
+namespace sym {
+
+constexpr int kT = 32;            // sub-tile edge
+constexpr int kTD = kT * kT;      // doubles per sub-tile
+constexpr int kB = 64;            // unit (block) edge
+
+struct Geom {
+  int n, nb32, nbB, upm;          // upm: units per matrix
+  long long spm;                  // sub-tiles per matrix
+};
+
+__host__ __device__ inline Geom make_geom(int n) {
+  Geom g;
+  g.n = n;
+  g.nb32 = (n + kT - 1) / kT;
+  g.nbB = (g.nb32 + 1) / 2;
+  g.upm = g.nbB * (g.nbB + 1) / 2;
+  long long s = 0;
+  for (int bi = 0; bi < g.nbB; ++bi) {
+    const int rs = (2 * bi + 1 < g.nb32) ? 2 : 1;
+    for (int bj = bi; bj < g.nbB; ++bj) {
+      const int cs = (2 * bj + 1 < g.nb32) ? 2 : 1;
+      s += (bi == bj) ? (rs == 2 ? 3 : 1) : rs * cs;
+    }
+  }
+  g.spm = s;
+  return g;
+}
+
+// unit table entry: sub-tile offset of the unit inside its matrix, and (Bi, Bj)
+struct Unit { int off; short bi, bj; };
+
+// host: fill the per-matrix unit table (upm entries, block-row-major)
+inline void fill_units(const Geom& g, Unit* out) {
+  int k = 0, off = 0;
+  for (int bi = 0; bi < g.nbB; ++bi) {
+    const int rs = (2 * bi + 1 < g.nb32) ? 2 : 1;
+    for (int bj = bi; bj < g.nbB; ++bj) {
+      const int cs = (2 * bj + 1 < g.nb32) ? 2 : 1;
+      out[k].off = off;
+      out[k].bi = (short)bi;
+      out[k].bj = (short)bj;
+      off += (bi == bj) ? (rs == 2 ? 3 : 1) : rs * cs;
+      ++k;
+    }
+  }
+}
+
+__device__ __forceinline__ int unit_subtiles(const Geom& g, int bi, int bj, int& rs, int& cs) {
+  rs = (2 * bi + 1 < g.nb32) ? 2 : 1;
+  cs = (2 * bj + 1 < g.nb32) ? 2 : 1;
+  return (bi == bj) ? (rs == 2 ? 3 : 1) : rs * cs;
+}
+
+// (sub-row, sub-col) of the k-th stored sub-tile of a unit
+__device__ __forceinline__ void unit_sub(bool diag, int cs, int k, int& sr, int& sc) {
+  if (diag) { sr = (k == 2) ? 1 : 0; sc = (k == 0) ? 0 : 1; }
+  else { sr = k / cs; sc = k - sr * cs; }
+}
+
+// Pack dense matrices (row stride ld, device or mapped host memory) into the
+// packed layout.  grid = (upm, count), block = 256.
+__global__ void pack_kernel(Geom g, const Unit* __restrict__ units, const double* __restrict__ src,
+                            long long ld, long long mat_stride, double* __restrict__ dst) {
+  const int u = blockIdx.x;
+  const long long a = blockIdx.y;
+  const Unit un = units[u];
+  int rs, cs;
+  const int ns = unit_subtiles(g, un.bi, un.bj, rs, cs);
+  const bool diag = un.bi == un.bj;
+  const double* S = src + a * mat_stride;
+  double* D = dst + (a * g.spm + un.off) * (long long)kTD;
+  for (int k = 0; k < ns; ++k) {
+    int sr, sc;
+    unit_sub(diag, cs, k, sr, sc);
+    const int r0 = (2 * un.bi + sr) * kT, c0 = (2 * un.bj + sc) * kT;
+    for (int e = threadIdx.x; e < kTD; e += blockDim.x) {
+      const int r = r0 + (e >> 5), c = c0 + (e & 31);
+      D[(long long)k * kTD + e] = (r < g.n && c < g.n) ? S[(long long)r * ld + c] : 0.0;
+    }
+  }
+}
+
+// lane l ends with sum over lanes of v[l]  (row l of a 32 x 32 product)
+__device__ __forceinline__ double transpose_reduce(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool hi = (lane & w) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const double send = hi ? v[k] : v[k + w];
+      const double keep = hi ? v[k + w] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
+// C-way product of one sub-tile: lane l gets sum_r T[r][l] * xr[r]
+__device__ __forceinline__ double col_dot(const double* __restrict__ T, const double* __restrict__ xr) {
+  const int lane = threadIdx.x & 31;
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int r = 0; r < kT; r += 2) {
+    const double2 xx = *reinterpret_cast<const double2*>(xr + r);
+    c0 = fma(T[r * kT + lane], xx.x, c0);
+    c1 = fma(T[(r + 1) * kT + lane], xx.y, c1);
+  }
+  return c0 + c1;
+}
+
+// One unit held in shared memory (tile) -> its slots of Pt.  xs: staged x,
+// zero padded to nbB * 64.  Pa: Pt + a * nbB * nbB * 64 (this matrix).
+__device__ __forceinline__ void consume_unit(const Geom& g, const double* __restrict__ tile,
+                                             const double* __restrict__ xs, int bi, int bj,
+                                             double* __restrict__ Pa) {
+  const int lane = threadIdx.x & 31;
+  int rs, cs;
+  unit_subtiles(g, bi, bj, rs, cs);
+  const double* xr = xs + bi * kB;
+  const double* xc = xs + bj * kB;
+  const long long nbB = g.nbB;
+  if (bi == bj) {
+    // (0,0): D00 x0 (C-way, symmetric);  (0,1): row part -> rows 0..31,
+    // column part -> rows 32..63;  (1,1): D11 x1 -> rows 32..63
+    double o0 = col_dot(tile, xr);
+    double o1 = 0.0;
+    if (rs == 2) {
+      const double* T01 = tile + kTD;
+      const double xj = xc[kT + lane];
+      double v[32];
+      double c = 0.0;
+#pragma unroll
+      for (int r = 0; r < kT; ++r) {
+        const double q = T01[r * kT + lane];
+        v[r] = q * xj;
+        c = fma(q, xr[r], c);
+      }
+      o0 = o0 + transpose_reduce(v);
+      o1 = c + col_dot(tile + 2 * kTD, xr + kT);
+    }
+    double* out = Pa + ((long long)bi * nbB + bi) * kB;
+    out[lane] = o0;
+    out[kT + lane] = o1;
+    return;
+  }
+  double c[2] = {0.0, 0.0};
+  double* outR = Pa + ((long long)bi * nbB + bj) * kB;
+  for (int sr = 0; sr < rs; ++sr) {
+    double v[32];
+#pragma unroll
+    for (int r = 0; r < kT; ++r) v[r] = 0.0;
+    for (int sc = 0; sc < cs; ++sc) {
+      const double* T = tile + (sr * cs + sc) * kTD;
+      const double xj = xc[sc * kT + lane];
+      const double* xi = xr + sr * kT;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < kT; r += 2) {
+        const double2 xx = *reinterpret_cast<const double2*>(xi + r);
+        const double q0 = T[r * kT + lane], q1 = T[(r + 1) * kT + lane];
+        v[r] = fma(q0, xj, v[r]);
+        v[r + 1] = fma(q1, xj, v[r + 1]);
+        c0 = fma(q0, xx.x, c0);
+        c1 = fma(q1, xx.y, c1);
+      }
+      c[sc] = c[sc] + (c0 + c1);
+    }
+    outR[sr * kT + lane] = transpose_reduce(v);
+  }
+  double* outC = Pa + ((long long)bj * nbB + bi) * kB;
+  for (int sc = 0; sc < cs; ++sc) outC[sc * kT + lane] = c[sc];
+}
+
+}  // namespace sym
+}  // namespace rapdb

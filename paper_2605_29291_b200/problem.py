@@ -17,6 +17,7 @@ device vector ops); nothing here evaluates Q products on the host.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -162,6 +163,15 @@ class ProblemInstance:
             cache[key] = DeviceData.upload(self, dev, src, k0, k1)
         return cache[key]
 
+    def zero_flags(self) -> np.ndarray:
+        """All-zero flags of the m+1 matrices (computed once: the instance is
+        immutable).  All-zero matrices are never streamed (C4's Q_0)."""
+        z = self._dev.get("_zero")
+        if z is None:
+            z = np.array([not np.any(self.Q[i]) for i in range(self.m + 1)], dtype=np.uint8)
+            self._dev["_zero"] = z
+        return z
+
     def pin_host(self):
         """Keep a page-locked copy of the Q stack so uploads run at full PCIe rate."""
         import torch
@@ -170,8 +180,8 @@ class ProblemInstance:
         return self._dev["_pinned"]
 
     def drop_device_data(self):
-        """Release the device copies (the pinned host copy is kept)."""
-        for k in [k for k in self._dev if k != "_pinned"]:
+        """Release the device copies (the pinned host copy and zero flags are kept)."""
+        for k in [k for k in self._dev if k not in ("_pinned", "_zero")]:
             del self._dev[k]
 
     # -- evaluations (problem.py:166-186) on the device --------------------
@@ -207,14 +217,22 @@ class DeviceData:
         self.__dict__.update(kw)
 
     @classmethod
-    def upload(cls, inst: ProblemInstance, device, pinned_host=None, k0=0, k1=None):
+    def upload(cls, inst: ProblemInstance, device, pinned_host=None, k0=0, k1=None, layout=None):
+        """layout "packed" (default; env RAPDB_LAYOUT): the upper block
+        triangle in 32 x 32 sub-tiles (csrc/symsweep.cuh), half the bytes of
+        the stack; "rows": the row-major stack [k1-k0][n][ld]."""
         import torch
         n, m, p = inst.n, inst.m, inst.p
         k1 = m + 1 if k1 is None else k1
         ld = n + (n & 1)
-        zero = np.array([not np.any(inst.Q[i]) for i in range(k0, k1)], dtype=np.uint8)
+        layout = layout or os.environ.get("RAPDB_LAYOUT", "packed")
+        if layout not in ("packed", "rows"):
+            raise ConfigurationError(f"unknown Q-stack layout {layout!r}")
+        zero = inst.zero_flags()[k0:k1].copy()
         src = (pinned_host if pinned_host is not None else torch.from_numpy(inst.Q))[k0:k1]
-        if ld == n:
+        if layout == "packed":
+            Qd = _upload_packed(src, n, device, pinned_host is not None)
+        elif ld == n:
             Qd = src.to(device, non_blocking=pinned_host is not None)
         else:
             Qd = torch.zeros((k1 - k0, n, ld), dtype=torch.float64, device=device)
@@ -224,7 +242,34 @@ class DeviceData:
         hi = inst.primal_set.upper
         return cls(n=n, m=m, p=p, ld=ld, Q=Qd, q=t(inst.q), r=t(inst.r),
                    A=t(inst.A) if p else None, b=t(inst.b) if p else None,
-                   lower=t(lo), upper=t(hi), mu=float(inst.mu), zero_flags=zero, device=device)
+                   lower=t(lo), upper=t(hi), mu=float(inst.mu), zero_flags=zero, device=device,
+                   layout=layout)
+
+
+def _upload_packed(src, n, device, pinned):
+    """Dense host matrices -> packed symmetric stack on the device.  Page-locked
+    sources are packed straight from host memory (only the upper triangle
+    crosses PCIe; env RAPDB_PACK_STAGED=1 forces staging); otherwise chunks
+    of <= 1 GB are staged on the device and packed there."""
+    import torch
+    from . import _capi
+    cnt = src.shape[0]
+    spm = _capi.packed_doubles(n)
+    Qp = torch.empty((max(cnt, 1), spm), dtype=torch.float64, device=device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    if cnt == 0:
+        return Qp
+    if pinned and os.environ.get("RAPDB_PACK_STAGED", "0") != "1":
+        _capi.pack_symmetric(n, cnt, src.data_ptr(), n, n * n, Qp.data_ptr(), stream)
+        return Qp
+    chunk = max(1, min(cnt, (1 << 30) // (n * n * 8)))
+    stage = torch.empty((chunk, n, n), dtype=torch.float64, device=device)
+    for c0 in range(0, cnt, chunk):
+        c = min(chunk, cnt - c0)
+        stage[:c].copy_(src[c0:c0 + c], non_blocking=pinned)
+        _capi.pack_symmetric(n, c, stage.data_ptr(), n, n * n, Qp[c0].data_ptr(), stream)
+    del stage
+    return Qp
 
 
 def _check_point(inst: ProblemInstance, z: Iterate):

@@ -64,7 +64,7 @@ def nccl_shard(inst, group=None) -> Shard:
     import torch.distributed as dist
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    zero = [not np.any(inst.Q[i]) for i in range(inst.m + 1)]
+    zero = inst.zero_flags().astype(bool)
     k0, k1 = plan(inst.m, world, zero)[rank]
 
     def allreduce(views):
@@ -85,7 +85,7 @@ class EmulatedCluster:
         self.error: Optional[BaseException] = None
 
     def shards(self, inst) -> List[Shard]:
-        zero = [not np.any(inst.Q[i]) for i in range(inst.m + 1)]
+        zero = inst.zero_flags().astype(bool)
         out = []
         for r, (k0, k1) in enumerate(plan(inst.m, self.R, zero)):
             out.append(Shard(rank=r, nranks=self.R, k0=k0, k1=k1, force_split=True, name="emulated",

@@ -1,0 +1,217 @@
+// sym_probe.cu -- standalone prototype of the packed-symmetric Q sweep
+// (paper_2605_29291_b200/csrc/symsweep.cuh): correctness against a dense
+// matvec and timing of stream + reduce at BASELINE shapes.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -I. -o sym_probe tools/sym_probe.cu
+// usage: sym_probe n nmat [reps] [nstages]
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include "paper_2605_29291_b200/csrc/symsweep.cuh"
+
+using namespace rapdb::sym;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
+
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ bool try_wait(uint64_t* b, unsigned par) {
+  unsigned ok;
+  asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+               : "=r"(ok) : "r"(su32(b)), "r"(par) : "memory");
+  return ok;
+}
+
+__device__ double hval(long long a, long long r, long long c) {
+  if (r > c) { long long t = r; r = c; c = t; }
+  unsigned long long z = (unsigned long long)(a * 1000003 + r * 7919 + c * 104729 + 12345);
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5 + (r == c ? 2.0 : 0.0);
+}
+
+__global__ void gen_dense(double* D, int n, long long nmat) {
+  const long long tot = nmat * n * (long long)n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    const long long a = i / ((long long)n * n), rc = i - a * (long long)n * n;
+    D[i] = hval(a, rc / n, rc % n);
+  }
+}
+
+__global__ void dense_mv(const double* D, int n, long long nmat, const double* x, double* u) {
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long row = gw; row < nmat * n; row += nw) {
+    const double* d = D + row * n;
+    double s = 0;
+    for (int c = lane; c < n; c += 32) s = fma(d[c], x[c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (!lane) u[row] = s;
+  }
+}
+
+__global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict__ units, const double* __restrict__ Qp,
+                                                  int nmat, const double* __restrict__ x, double* __restrict__ Pt,
+                                                  int ns, int slot_bytes, int xs_bytes) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  double* xs = reinterpret_cast<double*>(sm);
+  unsigned char* ring = sm + xs_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (long long)ns * slot_bytes);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(1));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int j = threadIdx.x; j < g.nbB * kB; j += blockDim.x) xs[j] = j < g.n ? x[j] : 0.0;
+  __syncthreads();
+  const long long total = (long long)nmat * g.upm;
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
+  const int ncw = ns < 8 ? ns : 8;
+  const long long mat_doubles = g.spm * kTD;
+  if (warp == 8) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      long long a = b / g.upm;
+      int u = (int)(b - a * g.upm);
+      int s = 0;
+      unsigned use = 0;
+      for (long long k = 0; k < mine; ++k) {
+        if (use > 0) while (!try_wait(&empty[s], (use - 1) & 1)) {}
+        const Unit un = units[u];
+        int rs, cs;
+        const unsigned bytes = (unsigned)unit_subtiles(g, un.bi, un.bj, rs, cs) * kTD * 8;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(su32(ring + (long long)s * slot_bytes)), "l"(Qp + a * mat_doubles + (long long)un.off * kTD),
+                     "r"(bytes), "r"(su32(&full[s])), "l"(pol) : "memory");
+        u += G;
+        while (u >= g.upm) { u -= g.upm; ++a; }
+        if (++s == ns) { s = 0; ++use; }
+      }
+    }
+  } else if (warp < ncw) {
+    long long gi = b + (long long)warp * G;
+    long long a = gi / g.upm;
+    int u = (int)(gi - a * g.upm);
+    int s = warp;
+    unsigned use = 0;
+    const long long pstride = (long long)g.nbB * g.nbB * kB;
+    for (long long k = warp; k < mine; k += ncw) {
+      while (!try_wait(&full[s], use & 1)) {}
+      const Unit un = units[u];
+      consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
+                   Pt + a * pstride);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+      u += ncw * G;
+      while (u >= g.upm) { u -= g.upm; ++a; }
+      s += ncw;
+      while (s >= ns) { s -= ns; ++use; }
+    }
+  }
+}
+
+__global__ void phase_b(Geom g, int nmat, const double* __restrict__ Pt, double* __restrict__ U) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int nbB = g.nbB;
+  for (long long it = gw; it < (long long)nmat * nbB; it += nw) {
+    const long long a = it / nbB;
+    const int B = (int)(it - a * nbB);
+    const double2* p = reinterpret_cast<const double2*>(Pt + (a * nbB + B) * (long long)nbB * kB) + lane;
+    double sx = 0.0, sy = 0.0;
+    int K = 0;
+    for (; K + 4 <= nbB; K += 4) {
+      const double2 t0 = __ldcg(p + (K + 0) * 32), t1 = __ldcg(p + (K + 1) * 32);
+      const double2 t2 = __ldcg(p + (K + 2) * 32), t3 = __ldcg(p + (K + 3) * 32);
+      sx += t0.x; sy += t0.y; sx += t1.x; sy += t1.y; sx += t2.x; sy += t2.y; sx += t3.x; sy += t3.y;
+    }
+    for (; K < nbB; ++K) { const double2 t = __ldcg(p + K * 32); sx += t.x; sy += t.y; }
+    const int r = B * kB + 2 * lane;
+    if (r < g.n) U[a * g.n + r] = sx;
+    if (r + 1 < g.n) U[a * g.n + r + 1] = sy;
+  }
+}
+
+int main(int argc, char** argv) {
+  const int n = argc > 1 ? atoi(argv[1]) : 2000;
+  const int nmat = argc > 2 ? atoi(argv[2]) : 201;
+  const int reps = argc > 3 ? atoi(argv[3]) : 20;
+  int ns = argc > 4 ? atoi(argv[4]) : 0;
+  const Geom g = make_geom(n);
+  std::vector<Unit> hu(g.upm);
+  fill_units(g, hu.data());
+  int nsm;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  double *D, *Qp, *Pt, *x, *U, *Uref;
+  Unit* units;
+  const long long dense_b = (long long)nmat * n * n * 8, packed_b = (long long)nmat * g.spm * kTD * 8;
+  const long long pt_b = (long long)nmat * g.nbB * g.nbB * kB * 8;
+  CK(cudaMalloc(&D, dense_b));
+  CK(cudaMalloc(&Qp, packed_b));
+  CK(cudaMalloc(&Pt, pt_b));
+  CK(cudaMalloc(&x, n * 8));
+  CK(cudaMalloc(&U, (long long)nmat * n * 8));
+  CK(cudaMalloc(&Uref, (long long)nmat * n * 8));
+  CK(cudaMalloc(&units, g.upm * sizeof(Unit)));
+  CK(cudaMemcpy(units, hu.data(), g.upm * sizeof(Unit), cudaMemcpyHostToDevice));
+  std::vector<double> hx(n);
+  for (int i = 0; i < n; ++i) hx[i] = std::sin(0.37 * i + 1.0);
+  CK(cudaMemcpy(x, hx.data(), n * 8, cudaMemcpyHostToDevice));
+  gen_dense<<<nsm * 8, 256>>>(D, n, nmat);
+  pack_kernel<<<dim3(g.upm, nmat), 256>>>(g, units, D, n, (long long)n * n, Qp);
+  dense_mv<<<nsm * 8, 256>>>(D, n, nmat, x, Uref);
+  CK(cudaDeviceSynchronize());
+  const int xs_bytes = ((g.nbB * kB * 8) + 127) / 128 * 128;
+  const int slot = 4 * kTD * 8;
+  if (ns <= 0) ns = (int)((227 * 1024 - xs_bytes - 1024) / slot);
+  const int smem = xs_bytes + ns * slot + 2 * ns * 8;
+  CK(cudaFuncSetAttribute(phase_a, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+  float msa = 0, msb = 0;
+  for (int it = 0; it < reps + 2; ++it) {
+    cudaEventRecord(e0);
+    phase_a<<<nsm, 288, smem>>>(g, units, Qp, nmat, x, Pt, ns, slot, xs_bytes);
+    cudaEventRecord(e1);
+    phase_b<<<nsm * 4, 256>>>(g, nmat, Pt, U);
+    cudaEventRecord(e2);
+    CK(cudaEventSynchronize(e2));
+    float a_, b_;
+    cudaEventElapsedTime(&a_, e0, e1);
+    cudaEventElapsedTime(&b_, e1, e2);
+    if (it >= 2) { msa += a_; msb += b_; }
+  }
+  CK(cudaGetLastError());
+  msa /= reps; msb /= reps;
+  std::vector<double> hU((long long)nmat * n), hR((long long)nmat * n);
+  CK(cudaMemcpy(hU.data(), U, hU.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hR.data(), Uref, hR.size() * 8, cudaMemcpyDeviceToHost));
+  double err = 0, mx = 0;
+  for (size_t i = 0; i < hU.size(); ++i) { err = fmax(err, fabs(hU[i] - hR[i])); mx = fmax(mx, fabs(hR[i])); }
+  // dense-row sweep for comparison: warp-per-row ldg matvec
+  cudaEventRecord(e0);
+  for (int it = 0; it < 5; ++it) dense_mv<<<nsm * 8, 256>>>(D, n, nmat, x, Uref);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float msd;
+  cudaEventElapsedTime(&msd, e0, e1);
+  msd /= 5;
+  printf("n=%d nmat=%d ns=%d smem=%d  packed %.3f GB (dense %.3f GB, Pt %.1f MB)\n", n, nmat, ns, smem,
+         packed_b / 1e9, dense_b / 1e9, pt_b / 1e6);
+  printf("phaseA %.4f ms (%.1f GB/s packed)  phaseB %.4f ms  total %.4f ms  dense-equiv %.1f GB/s\n", msa,
+         packed_b / msa / 1e6, msb, msa + msb, dense_b / (msa + msb) / 1e6);
+  printf("dense ldg matvec %.4f ms (%.1f GB/s)   max|err| %.3e  (max|u| %.3e)\n", msd, dense_b / msd / 1e6, err, mx);
+  return 0;
+}
