@@ -296,6 +296,8 @@ def main():
     conv = all(r.converged for r in results)
     st = results[-1].device_stats
     sweep_bytes = st["sweep_bytes"]
+    layout = os.environ.get("RAPDB_LAYOUT", "packed")
+    dense_bytes = (arr.m + 1 if shard is None else shard.k1 - shard.k0) * arr.n * arr.n * 8
     kern_ms = sum(r.device_stats["kernel_ms"] for r in results)
     sweeps = sum(r.device_stats["sweeps"] for r in results)
     sweep_ns = sum(r.device_stats["sweep_ns"] for r in results)
@@ -315,7 +317,14 @@ def main():
     inst.pin_host()
     inst.drop_device_data()
     torch.cuda.synchronize()
-    q_bytes = inst.Q.nbytes if shard is None else inst.Q[shard.k0:shard.k1].nbytes
+    nloc = arr.m + 1 if shard is None else shard.k1 - shard.k0
+    if layout == "packed" and os.environ.get("RAPDB_PACK_STAGED", "0") != "1":
+        # packed straight from page-locked host memory: only the stored upper
+        # block triangle crosses PCIe
+        from paper_2605_29291_b200.problem import packed_source_elements
+        q_bytes = nloc * packed_source_elements(arr.n) * 8
+    else:
+        q_bytes = nloc * arr.n * arr.n * 8
     h2d = q_bytes + inst.q.nbytes + inst.r.nbytes + 2 * arr.n * 8 + inst.A.nbytes + inst.b.nbytes
     e2e_iters, e2e_s, d2h = 0, 0.0, 0
     for _ in range(args.steps):
@@ -374,7 +383,12 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "rapdb_solver_kernel (whole launch: sweeps + all other phases)",
-                         "bytes_per_launch_def": "sweeps x (m+1) n^2 8 B",
+                         "layout": layout,
+                         "bytes_per_launch_def": ("sweeps x packed-symmetric stack bytes "
+                                                  "(m+1) x rapdb_packed_doubles(n) x 8 (upper block triangle)"
+                                                  if layout == "packed" else "sweeps x (m+1) n^2 8 B"),
+                         "sweep_bytes": sweep_bytes,
+                         "dense_equivalent_gbs": sweeps * dense_bytes / (kern_ms / 1e3) / 1e9,
                          "sweep_phase_gbs": sweep_phase_gbs,
                          "standalone_sweep_ms": probe_ms,
                          "standalone_sweep_gbs": None if probe_ms is None else sweep_bytes / (probe_ms / 1e3) / 1e9,

@@ -222,11 +222,12 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     int u = (int)(gi - a * upm);
     unsigned s = (base + warp) % ns, use = (base + warp) / ns;
     const int adv = ncw * G;
+    const uint64_t keep = sym::evict_last_policy();
     for (long long k = warp; k < mine; k += ncw) {
       if (!mbar_wait(&fullb[s], use & 1, abort_flag)) break;
       const sym::Unit un = units[u];
       sym::consume_unit(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xs,
-                        un.bi, un.bj, Pt + a * pstride);
+                        un.bi, un.bj, Pt + a * pstride, keep);
       // generic-proxy reads of the slot before the producer's next bulk write
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();

@@ -112,6 +112,18 @@ __global__ void pack_kernel(Geom g, const Unit* __restrict__ units, const double
   }
 }
 
+// store that asks L2 to keep the line (the unit partials are re-read by the
+// reduction phase right after the stream; evict_last keeps them out of DRAM)
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // lane l ends with sum over lanes of v[l]  (row l of a 32 x 32 product)
 __device__ __forceinline__ double transpose_reduce(double (&v)[32]) {
   const int lane = threadIdx.x & 31;
@@ -145,7 +157,7 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ T, const do
 // zero padded to nbB * 64.  Pa: Pt + a * nbB * nbB * 64 (this matrix).
 __device__ __forceinline__ void consume_unit(const Geom& g, const double* __restrict__ tile,
                                              const double* __restrict__ xs, int bi, int bj,
-                                             double* __restrict__ Pa) {
+                                             double* __restrict__ Pa, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   int rs, cs;
   unit_subtiles(g, bi, bj, rs, cs);
@@ -172,8 +184,8 @@ __device__ __forceinline__ void consume_unit(const Geom& g, const double* __rest
       o1 = c + col_dot(tile + 2 * kTD, xr + kT);
     }
     double* out = Pa + ((long long)bi * nbB + bi) * kB;
-    out[lane] = o0;
-    out[kT + lane] = o1;
+    st_keep(out + lane, o0, pol);
+    st_keep(out + kT + lane, o1, pol);
     return;
   }
   double c[2] = {0.0, 0.0};
@@ -198,10 +210,10 @@ __device__ __forceinline__ void consume_unit(const Geom& g, const double* __rest
       }
       c[sc] = c[sc] + (c0 + c1);
     }
-    outR[sr * kT + lane] = transpose_reduce(v);
+    st_keep(outR + sr * kT + lane, transpose_reduce(v), pol);
   }
   double* outC = Pa + ((long long)bj * nbB + bi) * kB;
-  for (int sc = 0; sc < cs; ++sc) outC[sc * kT + lane] = c[sc];
+  for (int sc = 0; sc < cs; ++sc) st_keep(outC + sc * kT + lane, c[sc], pol);
 }
 
 }  // namespace sym

@@ -246,6 +246,19 @@ class DeviceData:
                    layout=layout)
 
 
+def packed_source_elements(n: int) -> int:
+    """Entries of one dense n x n matrix that the packed layout stores (and that
+    a pack straight from page-locked host memory reads over PCIe): the upper
+    32-block triangle, diagonal 64-units without their (1,0) sub-tile."""
+    nb32 = (n + 31) // 32
+    ext = [min(32, n - 32 * k) for k in range(nb32)]
+    tot = 0
+    for bi in range(nb32):
+        for bj in range(bi, nb32):
+            tot += ext[bi] * ext[bj]
+    return tot
+
+
 def _upload_packed(src, n, device, pinned):
     """Dense host matrices -> packed symmetric stack on the device.  Page-locked
     sources are packed straight from host memory (only the upper triangle

@@ -11,6 +11,8 @@ caller asked to record.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 from typing import List, Optional, Union
 
@@ -190,6 +192,8 @@ def run_restarted(inst: ProblemInstance, config: SolverConfig,
     if metrics is None:
         f_star = criteria.f_star if criteria is not None else None
         metrics = diagnostics.metrics_from(engine._ctx.kkt(f_star), f_star)
+    if os.environ.get("RAPDB_STEP_PROFILE", "0") == "1":
+        stats["step_profile"] = engine._ctx.step_profile()
     return RunResult(solution=engine.last, average=engine.average(), trace=engine.trace,
                      restart_log=restart_log, iterations=engine.iters, evals=engine.evals_total,
                      converged=converged, status=status, metrics=metrics,

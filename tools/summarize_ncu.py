@@ -60,7 +60,7 @@ def full(rep, out, alg_bytes):
         1e9 if d["dram__bytes_read.sum"]["unit"] == "Gbyte" else 1e6 if d["dram__bytes_read.sum"]["unit"] == "Mbyte" else 1)
     wr = float(d["dram__bytes_write.sum"]["value"].replace(",", "")) * (
         1e9 if d["dram__bytes_write.sum"]["unit"] == "Gbyte" else 1e6 if d["dram__bytes_write.sum"]["unit"] == "Mbyte" else 1)
-    summ = {"report": rep, "kernel": "rapdb_solver_kernel OP_PROBE (one fused C1 sweep + g combine + U copy-out)",
+    summ = {"report": rep, "kernel": "rapdb_solver_kernel OP_PROBE (one fused C1 sweep: packed-symmetric stream + unit-partial reduction + g combine + U copy-out)",
             "duration_ms": t_ms, "dram_bytes_read": rd, "dram_bytes_write": wr,
             "dram_bytes_per_sweep": rd + wr, "algorithmic_bytes_per_sweep": alg_bytes,
             "traffic_over_algorithmic": (rd + wr) / alg_bytes if alg_bytes else None,

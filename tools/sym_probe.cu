@@ -105,11 +105,12 @@ __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict
     int s = warp;
     unsigned use = 0;
     const long long pstride = (long long)g.nbB * g.nbB * kB;
+    const uint64_t keep = evict_last_policy();
     for (long long k = warp; k < mine; k += ncw) {
       while (!try_wait(&full[s], use & 1)) {}
       const Unit un = units[u];
       consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
-                   Pt + a * pstride);
+                   Pt + a * pstride, keep);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
