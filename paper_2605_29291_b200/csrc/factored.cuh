@@ -17,28 +17,58 @@ namespace rapdb {
 __device__ __forceinline__ long long gwarp() { return (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); }
 __device__ __forceinline__ long long nwarps() { return (long long)gridDim.x * kWarps; }
 
+// sum_k val[k] * x[col[k]] over CSR row r, in stored order, no FMA; the CSR
+// arrays stream with an evict-first policy so the gathered x stays in L2
+__device__ __forceinline__ double csr_row_dot(const long long* __restrict__ ptr, const int* __restrict__ col,
+                                              const double* __restrict__ val, const double* x, long long r,
+                                              uint64_t ef) {
+  long long k = __ldg(ptr + r);
+  const long long k1 = __ldg(ptr + r + 1);
+  double s = 0.0;
+  for (; k + 8 <= k1; k += 8) {
+    int c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { c[t] = ld_stream(col + k + t, ef); v[t] = ld_stream(val + k + t, ef); }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) xv[t] = ldcg(x + c[t]);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s = __dadd_rn(s, __dmul_rn(v[t], xv[t]));
+  }
+  for (; k + 4 <= k1; k += 4) {
+    const int c0 = ld_stream(col + k, ef), c1 = ld_stream(col + k + 1, ef);
+    const int c2 = ld_stream(col + k + 2, ef), c3 = ld_stream(col + k + 3, ef);
+    const double v0 = ld_stream(val + k, ef), v1 = ld_stream(val + k + 1, ef);
+    const double v2 = ld_stream(val + k + 2, ef), v3 = ld_stream(val + k + 3, ef);
+    const double x0 = ldcg(x + c0), x1 = ldcg(x + c1), x2 = ldcg(x + c2), x3 = ldcg(x + c3);
+    s = __dadd_rn(s, __dmul_rn(v0, x0));
+    s = __dadd_rn(s, __dmul_rn(v1, x1));
+    s = __dadd_rn(s, __dmul_rn(v2, x2));
+    s = __dadd_rn(s, __dmul_rn(v3, x3));
+  }
+  for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(ld_stream(val + k, ef), ldcg(x + ld_stream(col + k, ef))));
+  return s;
+}
+
 // "Sweep" at x into parity par: W = R x (thread per row), A x - b into the
 // linear part of gval[par], chunk partials of c_i . x (warp per 1024 columns),
 // then (after a grid barrier) chunk partials of |W_i|^2 (warp per 1024 rows).
-__device__ bool sweep_factored(const KArgs& K, Sm& S, const double* x, int par) {
+__device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double* x, int par) {
   const DevProblem& P = K.P;
   const Work& w = K.w;
   const long long n = P.n;
   const int lane = threadIdx.x & 31;
   double* W = w.W + (long long)par * P.nr;
-  for (long long r = gtid(); r < P.nr; r += gstride()) {
-    const long long k0 = __ldg(P.r_ptr + r), k1 = __ldg(P.r_ptr + r + 1);
-    double s = 0.0;
-    for (long long k = k0; k < k1; ++k) s = fma(__ldg(P.r_val + k), ldcg(x + __ldg(P.r_col + k)), s);
-    W[r] = s;
-  }
+  // thread per CSR row, products summed in stored order without FMA (the
+  // operation order of scipy's csr_matvec, so W = R x matches the restatement
+  // bit for bit); the row's loads are issued in batches of 4 for MLP
+  const uint64_t ef = evict_first_policy();
+  const uint64_t el = sym::evict_last_policy();
+  for (long long r = gtid(); r < P.nr; r += gstride())
+    st_keep(W + r, csr_row_dot(P.r_ptr, P.r_col, P.r_val, x, r, ef), el);
   double* gv = w.gval + (long long)par * (P.m + 1);
-  for (long long j = gtid(); j < P.L; j += gstride()) {
-    const long long k0 = __ldg(P.a_ptr + j), k1 = __ldg(P.a_ptr + j + 1);
-    double s = 0.0;
-    for (long long k = k0; k < k1; ++k) s = fma(__ldg(P.a_val + k), ldcg(x + __ldg(P.a_col + k)), s);
-    gv[1 + P.mq + j] = s - __ldg(P.b + j);
-  }
+  for (long long j = gtid(); j < P.L; j += gstride())
+    gv[1 + P.mq + j] = csr_row_dot(P.a_ptr, P.a_col, P.a_val, x, j, ef) - __ldg(P.b + j);
   const long long items = (long long)(P.mq + 1) * P.nchx;
   for (long long it = gwarp(); it < items; it += nwarps()) {
     const long long i = it / P.nchx, ch = it - i * P.nchx;
@@ -86,24 +116,40 @@ __device__ void g_factored(const KArgs& K, int par) {
 }
 
 // out = sum_i w_i (R_i^T W_i + c_i) + A^T mu with w = (1, lam_1..lam_mq),
-// mu = lam[mq..]; lam is a global m-vector.  Pass 1 (column-parallel) adds
-// the dense c_i terms, pass 2 (warp per column) the R^T and A^T gathers.
-// The result is complete after the caller's grid barrier.
-__device__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, const double* lam, double* out) {
+// mu = lam[mq..]; lam is a global m-vector.  Pass 1 (element-parallel) adds
+// the dense c_i terms and scales the W-cache by its block weight,
+// Wl[r] = w_{blk(r)} W[r]; pass 2 gathers R^T Wl and A^T mu with 8 lanes per
+// column (4 columns per warp, 8 independent load chains per column), so the
+// ~65 nnz of a C3 column are fetched in ~8 dependent steps instead of ~3 per
+// lane-round.  The result is complete after the caller's grid barrier.
+__device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, const double* lam, double* out) {
   const DevProblem& P = K.P;
   const long long n = P.n;
   const int lane = threadIdx.x & 31;
   double* wq = S.stage;
+  double* Wl = K.w.wl;
+  const uint64_t ef = evict_first_policy();
+  const uint64_t el = sym::evict_last_policy();
   __syncthreads();
   for (int i = threadIdx.x; i <= P.mq; i += kThreads) wq[i] = i == 0 ? 1.0 : ldcg(lam + (i - 1));
   __syncthreads();
   for (long long j = gtid(); j < n; j += gstride()) {
     double acc = 0.0;
     int i = 0;
+    for (; i + 15 <= P.mq; i += 16) {   // 16 independent loads in flight per thread
+      double c[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double l = wq[i + k];
+        acc = (l != 0.0) ? acc + l * c[k] : acc;
+      }
+    }
     for (; i + 3 <= P.mq; i += 4) {
       double c[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) c[k] = __ldg(P.q + (long long)(i + k) * n + j);
+      for (int k = 0; k < 4; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const double l = wq[i + k];
@@ -112,25 +158,38 @@ __device__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, co
     }
     for (; i <= P.mq; ++i) {
       const double l = wq[i];
-      if (l != 0.0) acc = acc + l * __ldg(P.q + (long long)i * n + j);
+      if (l != 0.0) acc = acc + l * ld_stream(P.q + (long long)i * n + j, ef);
     }
     out[j] = acc;
   }
+  for (long long r = gtid(); r < P.nr; r += gstride())
+    st_keep(Wl + r, wq[ld_stream(P.rmat + r, ef)] * ldcg(Wpar + r), el);
   if (!gsync(K, S)) return false;
-  for (long long j = gwarp(); j < n; j += nwarps()) {
-    const long long k0 = __ldg(P.rt_ptr + j), k1 = __ldg(P.rt_ptr + j + 1);
-    double s = 0.0;
-    for (long long k = k0 + lane; k < k1; k += 32) {
-      const int r = __ldg(P.rt_row + k);
-      const double l = wq[__ldg(P.rmat + r)];
-      s = fma(__ldg(P.rt_val + k) * ldcg(Wpar + r), l, s);
+  const int sub = lane & 7, grp = lane >> 3;
+  for (long long jb = gwarp() * 4; jb < n; jb += nwarps() * 4) {
+    const long long j = jb + grp;
+    double s = 0.0, t = 0.0;
+    if (j < n) {
+      const long long k0 = __ldg(P.rt_ptr + j), k1 = __ldg(P.rt_ptr + j + 1);
+      long long k = k0 + sub;
+      for (; k + 8 < k1; k += 16) {
+        const int r0 = ld_stream(P.rt_row + k, ef), r1 = ld_stream(P.rt_row + k + 8, ef);
+        const double v0 = ld_stream(P.rt_val + k, ef), v1 = ld_stream(P.rt_val + k + 8, ef);
+        const double w0 = ldcg(Wl + r0), w1 = ldcg(Wl + r1);
+        s = fma(v0, w0, s);
+        s = fma(v1, w1, s);
+      }
+      if (k < k1) s = fma(ld_stream(P.rt_val + k, ef), ldcg(Wl + ld_stream(P.rt_row + k, ef)), s);
+      const long long a0 = __ldg(P.at_ptr + j), a1 = __ldg(P.at_ptr + j + 1);
+      for (long long k = a0 + sub; k < a1; k += 8)
+        t = fma(ld_stream(P.at_val + k, ef), ldcg(lam + P.mq + ld_stream(P.at_row + k, ef)), t);
     }
-    double t = 0.0;
-    const long long a0 = __ldg(P.at_ptr + j), a1 = __ldg(P.at_ptr + j + 1);
-    for (long long k = a0 + lane; k < a1; k += 32) t = fma(__ldg(P.at_val + k), ldcg(lam + P.mq + __ldg(P.at_row + k)), t);
-    s = warp_sum(s);
-    t = warp_sum(t);
-    if (lane == 0) out[j] = (ldcg(out + j) + s) + t;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    if (j < n && sub == 0) out[j] = (ldcg(out + j) + s) + t;
   }
   return true;
 }

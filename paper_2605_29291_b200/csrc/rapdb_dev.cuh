@@ -139,6 +139,7 @@ struct Work {
   double *H, *hx, *hxn, *hy;   // smoothed gap: dense H (n x n) and H-products
   double *W;                   // factored: [2][nr] W = R x at both parities
   double *pw2, *pcx;           // factored: chunk partials of |W_i|^2 and c_i . x
+  double *wl;                  // factored: [nr] block-weighted W-cache of the recombination
   double *Pt;                  // layout 1: per-unit partial products [nact][nbB][nbB][64]
   double* trace;
   SolverState* st;
@@ -256,5 +257,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+// streaming read-only loads that ask L2 to evict the line first (big
+// once-per-pass streams must not push small gathered vectors out of L2)
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+}
 
 }  // namespace rapdb

@@ -384,7 +384,7 @@ struct Layout {
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
-             B_W, B_PW2, B_PCX, B_PT, B_COUNT };
+             B_W, B_PW2, B_PCX, B_PT, B_WL, B_COUNT };
 static_assert(B_COUNT <= B_COUNT_MAX, "Layout::off too small");
 
 Layout layout_of(const rapdb_ctx* c) {
@@ -423,6 +423,7 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_PW2] = fac ? std::max(c->nchw, 1LL) * 8 : 8;
   sz[B_PCX] = fac ? (long long)(c->P.mq + 1) * c->P.nchx * 8 : 8;
   sz[B_PT] = packed ? std::max(1LL, (long long)c->P.nact) * c->sp.geom.nbB * c->sp.geom.nbB * sym::kB * 8 : 8;
+  sz[B_WL] = fac ? std::max(c->P.nr, 1LL) * 8 : 8;
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -963,6 +964,7 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.pw2 = D(B_PW2);
   w.pcx = D(B_PCX);
   w.Pt = D(B_PT);
+  w.wl = D(B_WL);
   w.trace = nullptr;
   w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);

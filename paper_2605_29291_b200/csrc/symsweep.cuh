@@ -114,9 +114,11 @@ __global__ void pack_kernel(Geom g, const Unit* __restrict__ units, const double
 
 // store that asks L2 to keep the line (the unit partials are re-read by the
 // reduction phase right after the stream; evict_last keeps them out of DRAM)
+#ifndef RAPDB_HAVE_ST_KEEP
 __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
 }
+#endif
 
 __device__ __forceinline__ uint64_t evict_last_policy() {
   uint64_t pol;

@@ -308,3 +308,98 @@ def grad_y_coupling(inst: ProblemInstance, z: Iterate):
     """(Ax - b, g(x)) (problem.py:220-223), on device."""
     _check_point(inst, z)
     return inst.eq_residual(z.x), inst.g_value(z.x)
+
+
+class DeviceDenseInstance:
+    """A dense QCQP of BASELINE configs 0-2's family whose Q stack is generated
+    ON THE DEVICE and packed there (never materialised on the host):
+    ``Q_i = 0.5 (B_i B_i^T + (B_i B_i^T)^T) + 0.1 I`` with ``B_i`` of shape n x r
+    and N(0, 1)/sqrt(n) entries drawn by torch's CUDA generator seeded with
+    (seed, i), fp64 DGEMM on the device; ``c_i ~ N(0,1)``, ``d_i ~ -U(1, 2)``,
+    ``d_0 = 0``, box [-box, box]^n, orthant cone, no equalities.  Same
+    distribution as ``instances.dense_qcqp`` but a different random stream (the
+    CounterRng instances stay the parity inputs); used for C2-scale
+    throughput runs, where the host instance would need 69 GB of host RAM.
+    Each rank of a sharded run generates only its own matrices.  Exposes the
+    ``ProblemInstance`` surface the solver layers use."""
+
+    def __init__(self, n: int, m: int, rank: int, seed: int = 0, box: float = 10.0, name: str = ""):
+        self.n, self.m, self.p, self.rank_r, self.seed = int(n), int(m), 0, int(rank), int(seed)
+        rng = np.random.default_rng(seed)
+        self.q = rng.standard_normal((m + 1, n))
+        self.r = np.concatenate([[0.0], -rng.uniform(1.0, 2.0, m)])
+        self.A = np.zeros((0, n))
+        self.b = np.zeros(0)
+        self.mu = 0.0
+        self.dual_set = None
+        self.name = name or f"device-dense n={n} m={m} r={rank}"
+        self.primal_set = Box(np.full(n, -box), np.full(n, box))
+        self.cone = NonnegOrthant(m)
+        self._dev = {}
+
+    def check_device_support(self):
+        return None
+
+    def zero_flags(self) -> np.ndarray:
+        return np.zeros(self.m + 1, dtype=np.uint8)
+
+    def generate_packed(self, device, k0: int, k1: int):
+        import torch
+        from . import _capi
+        n, r = self.n, self.rank_r
+        cnt = k1 - k0
+        spm = _capi.packed_doubles(n)
+        Qp = torch.empty((max(cnt, 1), spm), dtype=torch.float64, device=device)
+        chunk = max(1, min(cnt, (1 << 30) // (n * n * 8)))
+        stage = torch.empty((chunk, n, n), dtype=torch.float64, device=device)
+        gen = torch.Generator(device=device)
+        stream = torch.cuda.current_stream(device).cuda_stream
+        eye = 0.1 * torch.eye(n, dtype=torch.float64, device=device)
+        for c0 in range(0, cnt, chunk):
+            c = min(chunk, cnt - c0)
+            for j in range(c):
+                gen.manual_seed(self.seed * 1_000_003 + k0 + c0 + j)
+                B = torch.randn((n, r), generator=gen, dtype=torch.float64, device=device) / np.sqrt(n)
+                M = B @ B.T
+                stage[j] = 0.5 * (M + M.T) + eye
+            _capi.pack_symmetric(n, c, stage.data_ptr(), n, n * n, Qp[c0].data_ptr(), stream)
+        del stage
+        return Qp
+
+    def device_data(self, device=None, pinned_host=None, krange=None):
+        import torch
+        dev = torch.device("cuda", 0) if device is None else torch.device(device)
+        k0, k1 = krange if krange is not None else (0, self.m + 1)
+        key = str(dev) if (k0, k1) == (0, self.m + 1) else f"{dev}[{k0}:{k1}]"
+        if key not in self._dev:
+            t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+            n = self.n
+            self._dev[key] = DeviceData(n=n, m=self.m, p=0, ld=n + (n & 1), Q=self.generate_packed(dev, k0, k1),
+                                        q=t(self.q), r=t(self.r), A=None, b=None,
+                                        lower=t(self.primal_set.lower), upper=t(self.primal_set.upper), mu=0.0,
+                                        zero_flags=np.zeros(k1 - k0, dtype=np.uint8), device=dev,
+                                        layout="packed")
+        return self._dev[key]
+
+    def drop_device_data(self):
+        self._dev.clear()
+
+    def _evaluator(self):
+        from .engine import _Evaluator
+        ev = self._dev.get("_eval")
+        if ev is None:
+            ev = _Evaluator(self)
+            self._dev["_eval"] = ev
+        return ev
+
+    def f_value(self, x) -> float:
+        return float(self._evaluator().sweep(x)[1][0])
+
+    def g_value(self, x) -> np.ndarray:
+        return self._evaluator().sweep(x)[1][1:].cpu().numpy()
+
+    def eq_residual(self, x) -> np.ndarray:
+        return np.zeros(0)
+
+    def project_dual_cone(self, lam):
+        return np.maximum(np.asarray(lam, dtype=float), 0.0)

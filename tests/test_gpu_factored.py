@@ -135,7 +135,7 @@ def test_factored_shapes_vs_oracle(shape, nm):
     z = eng.last
     assert rel(z.x, res.x) <= 1e-8
     if arr.m:
-        assert rel(z.lam, res.lam) <= 1e-8
+        assert rel(z.lam, res.lam) <= 1e-8, rel(z.lam, res.lam)
     np.testing.assert_allclose(inst.g_value(z.x), O.FactoredProblem(arr).g(z.x), rtol=1e-10, atol=1e-10)
 
 

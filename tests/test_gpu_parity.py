@@ -295,6 +295,7 @@ def test_chunked_sweep_and_solver(monkeypatch, tile, stages, n):
     monkeypatch.setenv("RAPDB_TILE_BYTES", str(tile))
     monkeypatch.setenv("RAPDB_STAGES", str(stages))
     monkeypatch.setenv("RAPDB_ROW_TILE_MAX", "0")       # force column chunks
+    monkeypatch.setenv("RAPDB_LAYOUT", "rows")          # the row-major stack (packed: test_packed_layout.py)
     arr = instances.dense_qcqp(n, 7, 9, seed=21)
     inst = R.ProblemInstance.from_arrays(arr, validate=False)
     ev = inst._evaluator()
