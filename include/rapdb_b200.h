@@ -164,7 +164,8 @@ int rapdb_pack_symmetric(int n, long long count, const double* src, long long ld
  *   A     CSR [L x n] (a_ptr[L+1], a_col, a_val), A^T CSR [n x L], b [L]
  * All other pointers are device pointers.  No equality block (p = 0), the
  * dual set must be Unbounded, and the smoothed gap is not available (its
- * n x n H does not fit at this n): adaptive restarts need a dense instance. */
+ * n x n H does not fit at this n): adaptive restarts need a dense instance.
+ * Equivalent to rapdb_bind_factored_range over the whole instance.          */
 int rapdb_bind_factored(rapdb_ctx* ctx, int n, int mq, int L, long long nr,
                         const long long* r_ptr, const int* r_col, const double* r_val,
                         const long long* rt_ptr, const int* rt_row, const double* rt_val,
@@ -173,6 +174,22 @@ int rapdb_bind_factored(rapdb_ctx* ctx, int n, int mq, int L, long long nr,
                         const long long* a_ptr, const int* a_col, const double* a_val,
                         const long long* at_ptr, const int* at_row, const double* at_val,
                         const double* b, const double* lower, const double* upper, double mu);
+
+/* The same, holding only a constraint shard: blocks
+ * [fb0, fb1) of the mq+1 quadratic blocks (R rows, rblk with fb1-fb0+1
+ * entries, rmat LOCAL block ids, C and d rows fb0..fb1-1) and linear rows
+ * [l0, l1) of the L (A, A^T with local row ids, b).  mq and L are the global
+ * counts; x and the m multipliers are replicated.  The context exchanges the
+ * gradient partial (n) and g (m+1, zero outside this rank's rows) per trial. */
+int rapdb_bind_factored_range(rapdb_ctx* ctx, int n, int mq, int L, int fb0, int fb1, int l0, int l1,
+                              long long nr,
+                              const long long* r_ptr, const int* r_col, const double* r_val,
+                              const long long* rt_ptr, const int* rt_row, const double* rt_val,
+                              const int* rmat, const long long* rblk,
+                              const double* C, const double* d,
+                              const long long* a_ptr, const int* a_col, const double* a_val,
+                              const long long* at_ptr, const int* at_row, const double* at_val,
+                              const double* b, const double* lower, const double* upper, double mu);
 
 /* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
  * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */

@@ -47,7 +47,8 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_reinit", "rapdb_run", "rapdb_kkt", "rapdb_get_iterate", "rapdb_probe_sweep",
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
            "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x",
-           "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric"]
+           "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric",
+           "rapdb_bind_factored_range"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
@@ -117,6 +118,7 @@ def load(path: str = LIB_PATH):
     lib.rapdb_exchange_count.restype = LL
     lib.rapdb_step_profile.argtypes = [P, C.POINTER(D), C.POINTER(LL), I]
     lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 19 + [D]
+    lib.rapdb_bind_factored_range.argtypes = [P, I, I, I, I, I, I, I, LL] + [P] * 19 + [D]
     lib.rapdb_grad_x.argtypes = [P, P, P, P, P, P]
     _lib = lib
     return lib
@@ -220,8 +222,8 @@ class Context:
         self._set_stream()
         if getattr(data, "factored", False):
             rblk = np.ascontiguousarray(data.rblk, dtype=np.int64)
-            self._check(self.lib.rapdb_bind_factored(
-                self.h, data.n, data.mq, data.L, data.nr,
+            self._check(self.lib.rapdb_bind_factored_range(
+                self.h, data.n, data.mq, data.L, data.k0, data.k1, data.l0, data.l1, data.nr,
                 _ptr(data.r_ptr), _ptr(data.r_col), _ptr(data.r_val),
                 _ptr(data.rt_ptr), _ptr(data.rt_row), _ptr(data.rt_val),
                 _ptr(data.rmat), rblk.ctypes.data_as(C.c_void_p), _ptr(data.C), _ptr(data.d),

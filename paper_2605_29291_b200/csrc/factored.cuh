@@ -67,9 +67,9 @@ __device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double*
   for (long long r = gtid(); r < P.nr; r += gstride())
     st_keep(W + r, csr_row_dot(P.r_ptr, P.r_col, P.r_val, x, r, ef), el);
   double* gv = w.gval + (long long)par * (P.m + 1);
-  for (long long j = gtid(); j < P.L; j += gstride())
-    gv[1 + P.mq + j] = csr_row_dot(P.a_ptr, P.a_col, P.a_val, x, j, ef) - __ldg(P.b + j);
-  const long long items = (long long)(P.mq + 1) * P.nchx;
+  for (long long j = gtid(); j < P.Lloc; j += gstride())
+    gv[1 + P.mq + P.l0 + j] = csr_row_dot(P.a_ptr, P.a_col, P.a_val, x, j, ef) - __ldg(P.b + j);
+  const long long items = (long long)P.fnb * P.nchx;
   for (long long it = gwarp(); it < items; it += nwarps()) {
     const long long i = it / P.nchx, ch = it - i * P.nchx;
     const long long j0 = ch * 1024, j1 = min(j0 + 1024, n);
@@ -80,9 +80,9 @@ __device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double*
     if (lane == 0) w.pcx[it] = s;
   }
   if (!gsync(K, S)) return false;
-  const long long nchw = __ldg(P.wch + P.mq + 1);
+  const long long nchw = __ldg(P.wch + P.fnb);
   for (long long c = gwarp(); c < nchw; c += nwarps()) {
-    int lo = 0, hi = P.mq + 1;            // block of chunk c: wch[lo] <= c < wch[lo+1]
+    int lo = 0, hi = P.fnb;               // local block of chunk c: wch[lo] <= c < wch[lo+1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (__ldg(P.wch + mid) <= c) lo = mid; else hi = mid;
@@ -100,18 +100,27 @@ __device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double*
   return gsync(K, S);
 }
 
-// g_i (i = 0..mq, 0 = f) at parity par from the chunk partials: one warp per i
+// g_i (i = 0..mq, 0 = f) at parity par from the chunk partials: one warp per
+// local block; a sharded rank writes 0 for the entries it does not own (the
+// all-reduce of g is then exact: disjoint supports)
 __device__ void g_factored(const KArgs& K, int par) {
   const DevProblem& P = K.P;
   const int lane = threadIdx.x & 31;
   double* gv = K.w.gval + (long long)par * (P.m + 1);
-  for (long long i = gwarp(); i <= P.mq; i += nwarps()) {
+  for (long long i = gwarp(); i < P.fnb; i += nwarps()) {
     double sw = 0.0, sc = 0.0;
     for (long long c = __ldg(P.wch + i) + lane; c < __ldg(P.wch + i + 1); c += 32) sw += ldcg(K.w.pw2 + c);
     for (long long c = lane; c < P.nchx; c += 32) sc += ldcg(K.w.pcx + i * P.nchx + c);
     sw = warp_sum(sw);
     sc = warp_sum(sc);
-    if (lane == 0) gv[i] = 0.5 * sw + sc + __ldg(P.r + i);
+    if (lane == 0) gv[P.fb0 + i] = 0.5 * sw + sc + __ldg(P.r + i);
+  }
+  if (P.fnb < P.mq + 1 || P.Lloc < P.L) {
+    for (long long idx = gtid(); idx <= P.m; idx += gstride()) {
+      const bool mine = idx <= P.mq ? (idx >= P.fb0 && idx < P.fb0 + P.fnb)
+                                    : (idx - 1 - P.mq >= P.l0 && idx - 1 - P.mq < P.l0 + P.Lloc);
+      if (!mine) gv[idx] = 0.0;
+    }
   }
 }
 
@@ -131,12 +140,15 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
   const uint64_t ef = evict_first_policy();
   const uint64_t el = sym::evict_last_policy();
   __syncthreads();
-  for (int i = threadIdx.x; i <= P.mq; i += kThreads) wq[i] = i == 0 ? 1.0 : ldcg(lam + (i - 1));
+  for (int i = threadIdx.x; i < P.fnb; i += kThreads) {
+    const int gi = P.fb0 + i;             // global block id (0 = objective)
+    wq[i] = gi == 0 ? 1.0 : ldcg(lam + (gi - 1));
+  }
   __syncthreads();
   for (long long j = gtid(); j < n; j += gstride()) {
     double acc = 0.0;
     int i = 0;
-    for (; i + 15 <= P.mq; i += 16) {   // 16 independent loads in flight per thread
+    for (; i + 16 <= P.fnb; i += 16) {   // 16 independent loads in flight per thread
       double c[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
@@ -146,7 +158,7 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
         acc = (l != 0.0) ? acc + l * c[k] : acc;
       }
     }
-    for (; i + 3 <= P.mq; i += 4) {
+    for (; i + 4 <= P.fnb; i += 4) {
       double c[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
@@ -156,7 +168,7 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
         acc = (l != 0.0) ? acc + l * c[k] : acc;
       }
     }
-    for (; i <= P.mq; ++i) {
+    for (; i < P.fnb; ++i) {
       const double l = wq[i];
       if (l != 0.0) acc = acc + l * ld_stream(P.q + (long long)i * n + j, ef);
     }
@@ -182,7 +194,7 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
       if (k < k1) s = fma(ld_stream(P.rt_val + k, ef), ldcg(Wl + ld_stream(P.rt_row + k, ef)), s);
       const long long a0 = __ldg(P.at_ptr + j), a1 = __ldg(P.at_ptr + j + 1);
       for (long long k = a0 + sub; k < a1; k += 8)
-        t = fma(ld_stream(P.at_val + k, ef), ldcg(lam + P.mq + ld_stream(P.at_row + k, ef)), t);
+        t = fma(ld_stream(P.at_val + k, ef), ldcg(lam + P.mq + P.l0 + ld_stream(P.at_row + k, ef)), t);
     }
 #pragma unroll
     for (int o = 4; o >= 1; o >>= 1) {

@@ -105,7 +105,11 @@ struct DevProblem {
   const long long* rblk;                                            // [mq+2] first row of block i
   const long long* a_ptr; const int* a_col; const double* a_val;    // CSR A   [L x n]
   const long long* at_ptr; const int* at_row; const double* at_val; // CSR A^T [n x L]
-  const long long* wch;  // [mq+2] prefix count of 1024-row chunks of W per block
+  const long long* wch;  // [fnb+1] prefix count of 1024-row chunks of W per local block
+  // constraint sharding of a factored instance: this rank holds blocks
+  // [fb0, fb0+fnb) of the mq+1 (R, C, d local, rmat local ids) and linear rows
+  // [l0, l0+Lloc) of the L (A, A^T, b local); mq and L stay the global counts
+  int fb0, fnb, l0, Lloc;
 };
 
 struct DevParams {

@@ -421,7 +421,7 @@ Layout layout_of(const rapdb_ctx* c) {
   const bool fac = c->P.kind == 1;
   sz[B_W] = fac ? 2 * c->P.nr * 8 : 8;
   sz[B_PW2] = fac ? std::max(c->nchw, 1LL) * 8 : 8;
-  sz[B_PCX] = fac ? (long long)(c->P.mq + 1) * c->P.nchx * 8 : 8;
+  sz[B_PCX] = fac ? (long long)std::max(c->P.fnb, 1) * c->P.nchx * 8 : 8;
   sz[B_PT] = packed ? std::max(1LL, (long long)c->P.nact) * c->sp.geom.nbB * c->sp.geom.nbB * sym::kB * 8 : 8;
   sz[B_WL] = fac ? std::max(c->P.nr, 1LL) * 8 : 8;
   Layout L;
@@ -851,23 +851,41 @@ int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const 
                         const long long* a_ptr, const int* a_col, const double* a_val, const long long* at_ptr,
                         const int* at_row, const double* at_val, const double* b, const double* lower,
                         const double* upper, double mu) {
+  return rapdb_bind_factored_range(c, n, mq, L, 0, mq + 1, 0, L, nr, r_ptr, r_col, r_val, rt_ptr, rt_row, rt_val,
+                                   rmat, rblk, C, d, a_ptr, a_col, a_val, at_ptr, at_row, at_val, b, lower,
+                                   upper, mu);
+}
+
+int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int fb1, int l0, int l1, long long nr,
+                              const long long* r_ptr, const int* r_col, const double* r_val,
+                              const long long* rt_ptr, const int* rt_row, const double* rt_val,
+                              const int* rmat, const long long* rblk, const double* C, const double* d,
+                              const long long* a_ptr, const int* a_col, const double* a_val,
+                              const long long* at_ptr, const int* at_row, const double* at_val, const double* b,
+                              const double* lower, const double* upper, double mu) {
   if (!c) return RAPDB_EINPUT;
   if (n <= 0 || mq < 0 || L < 0 || nr < 0) return fail(c, RAPDB_EINPUT, "need n > 0, mq >= 0, L >= 0, nr >= 0");
-  if (c->nranks != 1 || c->split)
-    return fail(c, RAPDB_ECONFIG, "factored instances run on one rank (replicate across GPUs)");
-  if (!rblk || !C || !d || !lower || !upper || !rt_ptr || !at_ptr ||
+  if (fb0 < 0 || fb1 > mq + 1 || fb1 < fb0 || l0 < 0 || l1 > L || l1 < l0)
+    return fail(c, RAPDB_EINPUT, "bad local block / linear-row range");
+  const int fnb = fb1 - fb0, Lloc = l1 - l0;
+  const bool whole = fnb == mq + 1 && Lloc == L;
+  if (c->nranks == 1 && !whole && !c->split)
+    return fail(c, RAPDB_EINPUT, "a single-rank context must hold the whole instance (or be split)");
+  if (c->nranks > 1) c->split = 1;
+  if (!rblk || (fnb > 0 && (!C || !d)) || !lower || !upper || !rt_ptr || !at_ptr ||
       (nr > 0 && (!r_ptr || !r_col || !r_val || !rt_row || !rt_val || !rmat)) ||
-      (L > 0 && (!a_ptr || !a_col || !a_val || !at_row || !at_val || !b)))
+      (Lloc > 0 && (!a_ptr || !a_col || !a_val || !at_row || !at_val || !b)))
     return fail(c, RAPDB_EINPUT, "null data pointer");
-  if (rblk[0] != 0 || rblk[mq + 1] != nr) return fail(c, RAPDB_EINPUT, "rblk must run from 0 to nr");
-  std::vector<long long> ll(2 * (size_t)(mq + 2));
-  for (int i = 0; i <= mq; ++i) {
+  if (rblk[0] != 0 || rblk[fnb] != nr) return fail(c, RAPDB_EINPUT, "rblk must run from 0 to nr");
+  // d_ll: [fnb+1] local block row offsets, then [fnb+1] prefix counts of W chunks
+  std::vector<long long> ll(2 * (size_t)(fnb + 1));
+  for (int i = 0; i < fnb; ++i) {
     if (rblk[i + 1] < rblk[i]) return fail(c, RAPDB_EINPUT, "rblk must be nondecreasing");
     ll[i] = rblk[i];
-    ll[mq + 2 + i + 1] = ll[mq + 2 + i] + (rblk[i + 1] - rblk[i] + 1023) / 1024;
+    ll[fnb + 1 + i + 1] = ll[fnb + 1 + i] + (rblk[i + 1] - rblk[i] + 1023) / 1024;
   }
-  ll[mq + 1] = nr;
-  const long long nchw = ll[2 * (mq + 2) - 1];
+  ll[fnb] = nr;
+  const long long nchw = ll[2 * (fnb + 1) - 1];
   if (c->d_ll) cudaFree(c->d_ll);
   c->d_ll = nullptr;
   CK(cudaMalloc(&c->d_ll, ll.size() * sizeof(long long)));
@@ -878,12 +896,12 @@ int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const 
   CK(cudaMemset(c->d_ints, 0, 16));
   long long nnz_r = 0, nnz_a = 0;
   if (nr > 0) CK(cudaMemcpy(&nnz_r, r_ptr + nr, 8, cudaMemcpyDeviceToHost));
-  if (L > 0) CK(cudaMemcpy(&nnz_a, a_ptr + L, 8, cudaMemcpyDeviceToHost));
+  if (Lloc > 0) CK(cudaMemcpy(&nnz_a, a_ptr + Lloc, 8, cudaMemcpyDeviceToHost));
   // no streamed sweep: the ring degenerates to the multiplier staging area
   SweepPlan sp{};
   sp.TR = 1; sp.cpr = 1; sp.chunk = 2; sp.nstages = 1; sp.ncw = 1; sp.segmax = 1;
   sp.rc_cols = 1;   // the recombination ends warp-per-column: barrier before the primal step
-  sp.stage_bytes = align_up((long long)(mq + 1) * 8, 128);
+  sp.stage_bytes = align_up((long long)std::max(fnb, 1) * 8, 128);
   sp.xs_bytes = 0;
   sp.rows_total = 0;
   c->dyn_smem = (size_t)(sp.stage_bytes + 16);
@@ -905,9 +923,10 @@ int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const 
   P.Q = nullptr; P.q = C; P.r = d; P.A = nullptr; P.b = b; P.lo = lower; P.hi = upper; P.mu = mu;
   P.act = P.zero_list = P.seg_lo = P.seg_hi = P.cta_a0 = P.mat_slot = c->d_ints;
   P.kind = 1; P.mq = mq; P.nr = nr; P.L = L; P.nchx = (n + 1023) / 1024;
+  P.fb0 = fb0; P.fnb = fnb; P.l0 = l0; P.Lloc = Lloc;
   P.r_ptr = r_ptr; P.r_col = r_col; P.r_val = r_val;
   P.rt_ptr = rt_ptr; P.rt_row = rt_row; P.rt_val = rt_val;
-  P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (mq + 2);
+  P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (fnb + 1);
   P.a_ptr = a_ptr; P.a_col = a_col; P.a_val = a_val;
   P.at_ptr = at_ptr; P.at_row = at_row; P.at_val = at_val;
   c->P = P;
@@ -915,7 +934,7 @@ int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const 
   c->nchw = nchw;
   // one factored sweep: R (12 B/nnz + row pointers) streamed, W written and
   // re-read, C and A (+ b) read, x gathered once
-  c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * (mq + 1) * n + 12 * nnz_a + 16LL * L + 8 + 8LL * n;
+  c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * fnb * n + 12 * nnz_a + 16LL * Lloc + 8 + 8LL * n;
   c->bound = true;
   c->have_ws = false;
   return RAPDB_OK;

@@ -121,7 +121,10 @@ class ApdbEngine:
             self._ctx = _capi.Context(idx, shard.rank, shard.nranks)
             ctx = self._ctx
             ctx.set_exchange(lambda kind: shard.exchange(ctx.exchange_views(kind)), force_split=shard.split)
-            self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1))
+            if getattr(shard, "l0", None) is not None:
+                self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1), lrange=(shard.l0, shard.l1))
+            else:
+                self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1))
             ctx.bind(self._data, cfg, shard.k0, shard.k1)
         self._trace_buf = None
         self._res = None

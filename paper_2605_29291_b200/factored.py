@@ -80,14 +80,36 @@ class FactoredInstance:
         return None
 
     # -- device ---------------------------------------------------------------
-    def device_data(self, device=None, pinned_host=None, krange=None):
+    def shard_ranges(self, nranks: int):
+        """Constraint shards: contiguous quadratic
+        blocks balanced by R rows (block 0 = objective counts like any other)
+        and an even split of the linear rows; [(k0, k1, l0, l1)] per rank."""
+        nb = self.mq + 1
+        if nranks < 1 or nranks > nb:
+            raise ConfigurationError(f"cannot shard {nb} quadratic blocks over {nranks} ranks")
+        rows = np.diff(self.rblk).astype(float) + 1.0
+        cum = np.concatenate([[0.0], np.cumsum(rows)])
+        bounds = [0]
+        for r in range(1, nranks):
+            k = int(np.searchsorted(cum, cum[-1] * r / nranks, side="left"))
+            k = min(max(k, bounds[-1] + 1), nb - (nranks - r))
+            bounds.append(k)
+        bounds.append(nb)
+        return [(bounds[r], bounds[r + 1], self.L * r // nranks, self.L * (r + 1) // nranks)
+                for r in range(nranks)]
+
+    def device_data(self, device=None, pinned_host=None, krange=None, lrange=None):
+        """Upload (cached per device and shard).  krange = (k0, k1): quadratic
+        blocks held by this rank, lrange = (l0, l1): its linear rows."""
         import torch
-        if krange is not None and tuple(krange) != (0, self.m + 1):
-            raise ConfigurationError("factored instances are not constraint-sharded (run replicas)")
+        k0, k1 = krange if krange is not None else (0, self.mq + 1)
+        l0, l1 = lrange if lrange is not None else (0, self.L)
+        if krange is not None and lrange is None and tuple(krange) != (0, self.mq + 1):
+            raise ConfigurationError("a factored shard needs both its block range and its linear-row range")
         dev = torch.device("cuda", 0) if device is None else torch.device(device)
-        key = str(dev)
+        key = str(dev) if (k0, k1, l0, l1) == (0, self.mq + 1, 0, self.L) else f"{dev}[{k0}:{k1}|{l0}:{l1}]"
         if key not in self._dev:
-            self._dev[key] = FactoredDeviceData.upload(self, dev)
+            self._dev[key] = FactoredDeviceData.upload(self, dev, k0, k1, l0, l1)
         return self._dev[key]
 
     def drop_device_data(self):
@@ -127,8 +149,10 @@ class FactoredDeviceData:
         self.__dict__.update(kw)
 
     @classmethod
-    def upload(cls, inst: FactoredInstance, device):
+    def upload(cls, inst: FactoredInstance, device, k0=0, k1=None, l0=0, l1=None):
         import torch
+        k1 = inst.mq + 1 if k1 is None else k1
+        l1 = inst.L if l1 is None else l1
 
         def f64(a):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
@@ -142,21 +166,24 @@ class FactoredDeviceData:
         def csr(M):
             return i64(M.indptr), i32(M.indices), f64(M.data)
 
-        R = inst.R
+        r0, r1 = int(inst.rblk[k0]), int(inst.rblk[k1])
+        R = inst.R[r0:r1]
+        rblk = inst.rblk[k0:k1 + 1] - r0
         Rt = R.T.tocsr()
-        A = inst.A
+        A = inst.A[l0:l1]
         At = A.T.tocsr()
         nr = R.shape[0]
-        rmat = np.repeat(np.arange(inst.mq + 1, dtype=np.int32), np.diff(inst.rblk))
+        rmat = np.repeat(np.arange(k1 - k0, dtype=np.int32), np.diff(rblk))
         r_ptr, r_col, r_val = csr(R)
         rt_ptr, rt_row, rt_val = csr(Rt)
         a_ptr, a_col, a_val = csr(A)
         at_ptr, at_row, at_val = csr(At)
         one = lambda t: t if t.numel() else torch.zeros(1, dtype=t.dtype, device=device)
-        return cls(n=inst.n, m=inst.m, p=0, mq=inst.mq, L=inst.L, nr=nr, rblk=inst.rblk.copy(),
+        return cls(n=inst.n, m=inst.m, p=0, mq=inst.mq, L=inst.L, nr=nr, rblk=rblk.copy(),
+                   k0=k0, k1=k1, l0=l0, l1=l1,
                    r_ptr=r_ptr, r_col=one(r_col), r_val=one(r_val), rt_ptr=rt_ptr, rt_row=one(rt_row),
-                   rt_val=one(rt_val), rmat=one(i32(rmat)), C=f64(inst.C), d=f64(inst.d),
+                   rt_val=one(rt_val), rmat=one(i32(rmat)), C=one(f64(inst.C[k0:k1])), d=one(f64(inst.d[k0:k1])),
                    a_ptr=a_ptr, a_col=one(a_col), a_val=one(a_val), at_ptr=at_ptr, at_row=one(at_row),
-                   at_val=one(at_val), b=one(f64(inst.b)), lower=f64(inst.primal_set.lower),
+                   at_val=one(at_val), b=one(f64(inst.b[l0:l1])), lower=f64(inst.primal_set.lower),
                    upper=f64(inst.primal_set.upper), mu=inst.mu, device=device,
                    nnz_r=int(R.nnz), nnz_a=int(A.nnz))

@@ -34,6 +34,8 @@ class Shard:
     exchange: Optional[Callable[[list], None]] = None   # all-reduce(sum) of a list of device tensors
     force_split: bool = False
     name: str = ""
+    l0: Optional[int] = None      # factored instances: linear rows [l0, l1) of this rank
+    l1: Optional[int] = None
 
     @property
     def split(self) -> bool:
@@ -59,19 +61,26 @@ def plan(m: int, nranks: int, zero_flags: Optional[Sequence[bool]] = None) -> Li
     return [(bounds[r], bounds[r + 1]) for r in range(nranks)]
 
 
+def shard_ranges(inst, nranks: int):
+    """[(k0, k1, l0, l1)] per rank: matrix ranges balanced by streamed
+    matrices (dense; l0 = l1 = None) or the factored instance's own plan."""
+    if hasattr(inst, "shard_ranges"):
+        return inst.shard_ranges(nranks)
+    return [(k0, k1, None, None) for k0, k1 in plan(inst.m, nranks, inst.zero_flags().astype(bool))]
+
+
 def nccl_shard(inst, group=None) -> Shard:
     """This process's shard for the current torch.distributed (NCCL) group."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    zero = inst.zero_flags().astype(bool)
-    k0, k1 = plan(inst.m, world, zero)[rank]
+    k0, k1, l0, l1 = shard_ranges(inst, world)[rank]
 
     def allreduce(views):
         for v in views:
             dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
 
-    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl")
+    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl", l0=l0, l1=l1)
 
 
 class EmulatedCluster:
@@ -85,11 +94,10 @@ class EmulatedCluster:
         self.error: Optional[BaseException] = None
 
     def shards(self, inst) -> List[Shard]:
-        zero = inst.zero_flags().astype(bool)
         out = []
-        for r, (k0, k1) in enumerate(plan(inst.m, self.R, zero)):
+        for r, (k0, k1, l0, l1) in enumerate(shard_ranges(inst, self.R)):
             out.append(Shard(rank=r, nranks=self.R, k0=k0, k1=k1, force_split=True, name="emulated",
-                             exchange=(lambda views, rr=r: self._exchange(rr, views))))
+                             exchange=(lambda views, rr=r: self._exchange(rr, views)), l0=l0, l1=l1))
         return out
 
     def _exchange(self, rank, views):

@@ -146,3 +146,55 @@ def test_factored_rejects_unsupported(small):
         R.ApdbEngine(inst, R.SolverConfig(dual_ball=JointBall(5.0)), R.initial_iterate(inst))
     with pytest.raises(R.ConfigurationError):
         R.run_restarted(inst, R.SolverConfig(), R.AdaptiveRestart(warmup=5, check_period=5), budget=30)
+
+
+# ------------------------------------------------------- constraint sharding (section 8(e))
+
+def test_factored_forced_split_is_bitwise_identical(small):
+    """One rank in split mode (kernel stops at every exchange point, host
+    'all-reduces' a single buffer) == the fused single-launch run."""
+    from paper_2605_29291_b200.sharding import Shard
+    arr, inst, _ = small
+    cfg = R.SolverConfig(mode="yx", nonmonotone=True)
+    fused = R.run_restarted(inst, cfg, R.FixedRestart(40), budget=120)
+    calls = []
+    shard = Shard(rank=0, nranks=1, k0=0, k1=arr.mq + 1, l0=0, l1=arr.L, force_split=True,
+                  exchange=lambda views: calls.append(len(views)))
+    split = R.run_restarted(inst, cfg, R.FixedRestart(40), budget=120, shard=shard)
+    assert calls
+    np.testing.assert_array_equal(trace_arr(split.trace), trace_arr(fused.trace))
+    np.testing.assert_array_equal(split.solution.x, fused.solution.x)
+    np.testing.assert_array_equal(split.solution.lam, fused.solution.lam)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("nm", [False, True])
+def test_factored_emulated_shards(small, nranks, nm):
+    """R ranks, each holding a block range and a linear-row range, exchanging
+    the gradient partial and g per trial: same accepted steps as the
+    unsharded device run, iterates to 1e-12, and the oracle to 1e-9."""
+    from paper_2605_29291_b200.sharding import EmulatedCluster
+    arr, inst, _ = small
+    cfg = R.SolverConfig(mode="yx", nonmonotone=nm)
+    iters = 80
+    ref = R.ApdbEngine(inst, cfg, R.initial_iterate(inst))
+    ref.run_block(iters)
+    tr_ref = trace_arr(ref.trace)
+    tr_o, res_o = oracle_trace(O.FactoredProblem(arr), nm, iters)
+    cluster = EmulatedCluster(nranks)
+    shards = cluster.shards(inst)
+    assert [s.k0 for s in shards][0] == 0 and shards[-1].k1 == arr.mq + 1
+    assert shards[0].l0 == 0 and shards[-1].l1 == arr.L
+
+    def body(shard):
+        eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst), shard=shard)
+        eng.run_block(iters)
+        return trace_arr(eng.trace), eng.last
+
+    for tr, z in cluster.run(inst, body):
+        np.testing.assert_array_equal(tr[:, 5], tr_ref[:, 5])
+        np.testing.assert_allclose(tr[:, 1:5], tr_ref[:, 1:5], rtol=1e-12)
+        assert rel(z.x, ref.last.x) <= 1e-12
+        assert rel(z.lam, ref.last.lam) <= 1e-11
+        np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
+        np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)

@@ -68,3 +68,23 @@ def test_config_validation_and_defaults():
 def test_budget_validation():
     with pytest.raises(ConfigurationError):
         restarts.run_restarted(None, SolverConfig(), budget=0)
+
+
+def test_factored_shard_ranges_cover_and_balance():
+    from paper_2605_29291_b200 import instances
+    from paper_2605_29291_b200.factored import FactoredInstance
+    arr = instances.factored_qcqp(n=500, mq=9, rows=40, nnz_row=4, lin_rows=101, lin_nnz=3, seed=1)
+    inst = FactoredInstance.from_arrays(arr)
+    for R_ in (1, 2, 3, 5, 10):
+        rr = inst.shard_ranges(R_)
+        assert len(rr) == R_
+        assert rr[0][0] == 0 and rr[-1][1] == arr.mq + 1 and rr[0][2] == 0 and rr[-1][3] == arr.L
+        for a, b in zip(rr, rr[1:]):
+            assert a[1] == b[0] and a[3] == b[2]
+        assert all(k1 > k0 for k0, k1, _, _ in rr)
+        sizes = [k1 - k0 for k0, k1, _, _ in rr]
+        assert max(sizes) - min(sizes) <= 1
+    import pytest
+    from paper_2605_29291_b200.errors import ConfigurationError
+    with pytest.raises(ConfigurationError):
+        inst.shard_ranges(arr.mq + 2)
