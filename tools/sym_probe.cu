@@ -55,7 +55,7 @@ __global__ void dense_mv(const double* D, int n, long long nmat, const double* x
 
 __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict__ units, const double* __restrict__ Qp,
                                                   int nmat, const double* __restrict__ x, double* __restrict__ Pt,
-                                                  int ns, int slot_bytes, int xs_bytes) {
+                                                  int ns, int slot_bytes, int xs_bytes, int pf, int nocomp) {
   extern __shared__ __align__(128) unsigned char sm[];
   double* xs = reinterpret_cast<double*>(sm);
   unsigned char* ring = sm + xs_bytes;
@@ -82,9 +82,30 @@ __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       long long a = b / g.upm;
       int u = (int)(b - a * g.upm);
+      // L2 prefetch cursor pf units ahead of the ring
+      long long pa = a;
+      int pu = u;
+      for (int t = 0; t < pf; ++t) {
+        if (t < mine) {
+          const Unit un = units[pu];
+          int rs, cs;
+          const unsigned by = (unsigned)unit_subtiles(g, un.bi, un.bj, rs, cs) * kTD * 8;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(Qp + pa * mat_doubles + (long long)un.off * kTD), "r"(by) : "memory");
+        }
+        pu += G;
+        while (pu >= g.upm) { pu -= g.upm; ++pa; }
+      }
       int s = 0;
       unsigned use = 0;
       for (long long k = 0; k < mine; ++k) {
+        if (pf > 0 && k + pf < mine) {
+          const Unit un = units[pu];
+          int rs, cs;
+          const unsigned by = (unsigned)unit_subtiles(g, un.bi, un.bj, rs, cs) * kTD * 8;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(Qp + pa * mat_doubles + (long long)un.off * kTD), "r"(by) : "memory");
+          pu += G;
+          while (pu >= g.upm) { pu -= g.upm; ++pa; }
+        }
         if (use > 0) while (!try_wait(&empty[s], (use - 1) & 1)) {}
         const Unit un = units[u];
         int rs, cs;
@@ -109,8 +130,10 @@ __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict
     for (long long k = warp; k < mine; k += ncw) {
       while (!try_wait(&full[s], use & 1)) {}
       const Unit un = units[u];
-      consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
-                   Pt + a * pstride, keep);
+      // nocomp 1: no compute (pure stream); 2: compute, partials of every
+      // matrix into matrix 0's slots (L2-resident: no DRAM write traffic)
+      if (nocomp != 1) consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
+                   Pt + (nocomp == 2 ? 0 : a) * pstride, keep);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
@@ -150,6 +173,8 @@ int main(int argc, char** argv) {
   const int nmat = argc > 2 ? atoi(argv[2]) : 201;
   const int reps = argc > 3 ? atoi(argv[3]) : 20;
   int ns = argc > 4 ? atoi(argv[4]) : 0;
+  const int pf = argc > 5 ? atoi(argv[5]) : 0;
+  const int nocomp = argc > 6 ? atoi(argv[6]) : 0;
   const Geom g = make_geom(n);
   std::vector<Unit> hu(g.upm);
   fill_units(g, hu.data());
@@ -184,7 +209,7 @@ int main(int argc, char** argv) {
   float msa = 0, msb = 0;
   for (int it = 0; it < reps + 2; ++it) {
     cudaEventRecord(e0);
-    phase_a<<<nsm, 288, smem>>>(g, units, Qp, nmat, x, Pt, ns, slot, xs_bytes);
+    phase_a<<<nsm, 288, smem>>>(g, units, Qp, nmat, x, Pt, ns, slot, xs_bytes, pf, nocomp);
     cudaEventRecord(e1);
     phase_b<<<nsm * 4, 256>>>(g, nmat, Pt, U);
     cudaEventRecord(e2);
@@ -209,7 +234,7 @@ int main(int argc, char** argv) {
   float msd;
   cudaEventElapsedTime(&msd, e0, e1);
   msd /= 5;
-  printf("n=%d nmat=%d ns=%d smem=%d  packed %.3f GB (dense %.3f GB, Pt %.1f MB)\n", n, nmat, ns, smem,
+  printf("pf=%d n=%d nmat=%d ns=%d smem=%d  packed %.3f GB (dense %.3f GB, Pt %.1f MB)\n", pf, n, nmat, ns, smem,
          packed_b / 1e9, dense_b / 1e9, pt_b / 1e6);
   printf("phaseA %.4f ms (%.1f GB/s packed)  phaseB %.4f ms  total %.4f ms  dense-equiv %.1f GB/s\n", msa,
          packed_b / msa / 1e6, msb, msa + msb, dense_b / (msa + msb) / 1e6);
