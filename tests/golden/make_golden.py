@@ -283,11 +283,32 @@ def c1_fixtures():
     save("c1_200", arrays, meta)
 
 
+def scaled_fixtures(name, cfg_name, scale, cases, snaps=(1, 2, 5, 10, 20, 50, 100, 150, 200)):
+    """200-iteration traces of the REAL reference on a BASELINE config
+    (C4 at full size, C2 at reduced scale: the full C2 stack is 69 GB)."""
+    arr = instances.config_instance(cfg_name, scale=scale)
+    t0 = time.time()
+    inst = ref_instance(arr)
+    print(name, "instance", time.time() - t0, flush=True)
+    arrays = {"Q_checksum": np.array([float(np.sum(arr.Q[i])) for i in range(arr.m + 1)])}
+    meta = {"instance": f"instances.config_instance({cfg_name!r}, scale={scale!r})", "cases": {},
+            "n": arr.n, "m": arr.m}
+    for key, case in cases.items():
+        out, wall = run_case(inst, case, set(snaps))
+        for k, v in out.items():
+            arrays[f"{key}/{k}"] = v
+        meta["cases"][key] = dict(case, wall_s=wall)
+        print(name, key, wall, flush=True)
+    save(name, arrays, meta)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     ap.add_argument("--factored", action="store_true")
+    ap.add_argument("--c4", action="store_true")
+    ap.add_argument("--c2s", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
         small_fixtures()
@@ -295,3 +316,11 @@ if __name__ == "__main__":
         factored_fixtures()
     if a.c1:
         c1_fixtures()
+    if a.c4:   # BASELINE C4 at full size (N = 4000, n = 4001): nm and mono, no restart in 200
+        scaled_fixtures("c4_200", "C4", None,
+                        {"nm": dict(nm=True, policy={"kind": "fixed", "period": 500}, budget=200),
+                         "mono": dict(nm=False, policy={"kind": "fixed", "period": 500}, budget=200)})
+    if a.c2s:  # BASELINE C2's generator at 1/4 scale (n = 1024, m = 128, rank 64)
+        scaled_fixtures("c2s_200", "C2", 0.25,
+                        {"nm": dict(nm=True, policy={"kind": "none"}, budget=200),
+                         "mono": dict(nm=False, policy={"kind": "none"}, budget=200)})

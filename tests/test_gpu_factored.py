@@ -198,3 +198,22 @@ def test_factored_emulated_shards(small, nranks, nm):
         assert rel(z.lam, ref.last.lam) <= 1e-11
         np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
         np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+
+
+@pytest.mark.slow
+def test_c3_full_size_first_iterations():
+    """BASELINE C3 at full size (n = 10^6, 64 factored constraints, 5e5
+    linear rows): the first 3 accepted iterations (11 test evaluations, incl.
+    the initial backtracking from tau_bar) against the oracle's factored
+    restatement -- identical backtrack counts and step sizes to rounding,
+    iterates to 1e-9.  (~1 min of CPU oracle time.)"""
+    arr = instances.factored_qcqp()
+    inst = FactoredInstance.from_arrays(arr)
+    tr_o, res_o = oracle_trace(O.FactoredProblem(arr), False, 3)
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=False), R.initial_iterate(inst))
+    eng.run_block(3)
+    tr = trace_arr(eng.trace)
+    np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
+    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-12)
+    assert rel(eng.last.x, res_o.x) <= 1e-9
+    assert rel(eng.last.lam, res_o.lam) <= 1e-9

@@ -398,3 +398,41 @@ def test_smoothed_gap_kats():
     inst = inst_from(a["Q"], a["q"], a["r"], a["lower"], a["upper"])
     gap, _ = smoothed_gap(inst, R.Iterate(np.zeros(2), np.zeros(0), np.zeros(1)), 0.04, subsolver_tol=1e-11)
     assert gap > 1.0
+
+
+# ------------------------------------------------- BASELINE configs at scale
+
+def _first_200(g, arr, key, nm, tol=1e-9):
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.initial_iterate(inst))
+    snaps = [int(k) for k in g[f"{key}/snap_iters"]]
+    done = 0
+    for idx, k in enumerate(snaps):
+        eng.run_block(k - done)
+        done = k
+        z = eng.last
+        assert rel(z.x, g[f"{key}/snap_x"][idx]) <= tol, k
+        assert rel(z.lam, g[f"{key}/snap_lam"][idx]) <= tol, k
+    np.testing.assert_array_equal(trace_arr(eng.trace)[:, TAU], g[f"{key}/trace"][:, TAU])
+
+
+@pytest.mark.parametrize("key,nm", [("nm", True), ("mono", False)])
+def test_c4_first_200(key, nm):
+    """BASELINE C4 at full size (KML epigraph, N = 4000, n = 4001) against the
+    real reference's first 200 iterations (tests/golden/c4_200.npz)."""
+    g = load_golden("c4_200")
+    arr = instances.config_instance("C4")
+    np.testing.assert_allclose([float(np.sum(arr.Q[i])) for i in range(arr.m + 1)], g["Q_checksum"], rtol=1e-12)
+    _first_200(g, arr, key, nm)
+
+
+@pytest.mark.parametrize("key,nm", [("nm", True), ("mono", False)])
+def test_c2_scaled_first_200(key, nm):
+    """BASELINE C2's generator at 1/4 scale (n = 1024, m = 128, rank 64)
+    against the real reference (the full 69 GB stack does not fit the
+    reference's host)."""
+    g = load_golden("c2s_200")
+    arr = instances.config_instance("C2", scale=0.25)
+    np.testing.assert_allclose([float(np.sum(arr.Q[i])) for i in range(0, arr.m + 1, 16)],
+                               g["Q_checksum"][::16], rtol=1e-12)
+    _first_200(g, arr, key, nm)
