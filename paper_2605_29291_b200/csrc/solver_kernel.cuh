@@ -250,6 +250,13 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
     double sx = 0.0, sy = 0.0;
     int kk = 0;
+    for (; kk + 16 <= nbB; kk += 16) {   // 16 x 512 B in flight per warp (the reads are DRAM-bound)
+      double2 t[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) { sx += t[q].x; sy += t[q].y; }
+    }
     for (; kk + 4 <= nbB; kk += 4) {
       const double2 t0 = __ldcg(pp + (kk + 0) * 32), t1 = __ldcg(pp + (kk + 1) * 32);
       const double2 t2 = __ldcg(pp + (kk + 2) * 32), t3 = __ldcg(pp + (kk + 3) * 32);

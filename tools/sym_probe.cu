@@ -145,6 +145,121 @@ __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict
   }
 }
 
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Stream + reduction fused: unit partials go to a ring of W matrix slots
+// (L2-resident), a reducer warp per CTA reduces matrix a once all its units
+// are written (cnt[a]) and publishes red[a]; writers of matrix a >= W wait for
+// red[a - W] (slot reuse).  Counters are cumulative over sweeps (epoch E).
+__global__ void __launch_bounds__(288, 1) phase_fused(Geom g, const Unit* __restrict__ units,
+                                                      const double* __restrict__ Qp, int nmat,
+                                                      const double* __restrict__ x, double* __restrict__ Pt,
+                                                      int ns, int slot_bytes, int xs_bytes, int W, int* cnt,
+                                                      int* red, int E, double* __restrict__ U) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  double* xs = reinterpret_cast<double*>(sm);
+  unsigned char* ring = sm + xs_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (long long)ns * slot_bytes);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(1));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int j = threadIdx.x; j < g.nbB * kB; j += blockDim.x) xs[j] = j < g.n ? x[j] : 0.0;
+  __syncthreads();
+  const long long total = (long long)nmat * g.upm;
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
+  const int ncw = ns < 7 ? ns : 7;
+  const long long mat_doubles = g.spm * kTD;
+  const long long pstride = (long long)g.nbB * g.nbB * kB;
+  const int cnt_done = (E + 1) * g.upm, red_done = (E + 1) * g.nbB;
+  if (warp == 8) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      long long a = b / g.upm;
+      int u = (int)(b - a * g.upm);
+      int s = 0;
+      unsigned use = 0;
+      for (long long k = 0; k < mine; ++k) {
+        if (use > 0) while (!try_wait(&empty[s], (use - 1) & 1)) {}
+        const Unit un = units[u];
+        int rs, cs;
+        const unsigned bytes = (unsigned)unit_subtiles(g, un.bi, un.bj, rs, cs) * kTD * 8;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(su32(ring + (long long)s * slot_bytes)), "l"(Qp + a * mat_doubles + (long long)un.off * kTD),
+                     "r"(bytes), "r"(su32(&full[s])), "l"(pol) : "memory");
+        u += G;
+        while (u >= g.upm) { u -= g.upm; ++a; }
+        if (++s == ns) { s = 0; ++use; }
+      }
+    }
+  } else if (warp < ncw) {
+    long long gi = b + (long long)warp * G;
+    long long a = gi / g.upm;
+    int u = (int)(gi - a * g.upm);
+    int s = warp;
+    unsigned use = 0;
+    const uint64_t keep = evict_last_policy();
+    for (long long k = warp; k < mine; k += ncw) {
+      while (!try_wait(&full[s], use & 1)) {}
+      const Unit un = units[u];
+      if (a >= W) while (ld_acquire(red + (a - W)) < red_done) __nanosleep(32);   // slot reuse
+      consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
+                   Pt + (a % W) * pstride, keep);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+        __threadfence();
+        atomicAdd(cnt + a, 1);
+      }
+      u += ncw * G;
+      while (u >= g.upm) { u -= g.upm; ++a; }
+      s += ncw;
+      while (s >= ns) { s -= ns; ++use; }
+    }
+  } else if (warp == 7) {
+    // reducer: items t = a * nbB + B, round-robin over CTAs, in increasing t
+    const int nbB = g.nbB;
+    for (long long t = b; t < (long long)nmat * nbB; t += G) {
+      const long long a = t / nbB;
+      const int B = (int)(t - a * nbB);
+      while (ld_acquire(cnt + a) < cnt_done) __nanosleep(64);
+      const double2* p = reinterpret_cast<const double2*>(Pt + ((a % W) * nbB + B) * (long long)nbB * kB) + lane;
+      double sx = 0.0, sy = 0.0;
+      int K = 0;
+      for (; K + 8 <= nbB; K += 8) {
+        double2 tt[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tt[q] = __ldcg(p + (K + q) * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { sx += tt[q].x; sy += tt[q].y; }
+      }
+      for (; K < nbB; ++K) { const double2 t2 = __ldcg(p + K * 32); sx += t2.x; sy += t2.y; }
+      const int r = B * kB + 2 * lane;
+      if (r < g.n) U[a * g.n + r] = sx;
+      if (r + 1 < g.n) U[a * g.n + r + 1] = sy;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(red + a, 1);
+      }
+    }
+  }
+}
+
 __global__ void phase_b(Geom g, int nmat, const double* __restrict__ Pt, double* __restrict__ U) {
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -207,6 +322,35 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   float msa = 0, msb = 0;
+  const int W = argc > 7 ? atoi(argv[7]) : 0;
+  if (W > 0) {   // fused stream + reduction with a W-matrix partial ring
+    int *cnt, *red;
+    CK(cudaMalloc(&cnt, nmat * 4));
+    CK(cudaMalloc(&red, nmat * 4));
+    CK(cudaMemset(cnt, 0, nmat * 4));
+    CK(cudaMemset(red, 0, nmat * 4));
+    CK(cudaFuncSetAttribute(phase_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int Wr = W < nmat ? W : nmat;
+    for (int it = 0; it < reps + 2; ++it) {
+      cudaEventRecord(e0);
+      phase_fused<<<nsm, 288, smem>>>(g, units, Qp, nmat, x, Pt, ns, slot, xs_bytes, Wr, cnt, red, it, U);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float a_;
+      cudaEventElapsedTime(&a_, e0, e1);
+      if (it >= 2) msa += a_;
+    }
+    CK(cudaGetLastError());
+    msa /= reps;
+    std::vector<double> hU((long long)nmat * n), hR((long long)nmat * n);
+    CK(cudaMemcpy(hU.data(), U, hU.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hR.data(), Uref, hR.size() * 8, cudaMemcpyDeviceToHost));
+    double err = 0, mx = 0;
+    for (size_t i = 0; i < hU.size(); ++i) { err = fmax(err, fabs(hU[i] - hR[i])); mx = fmax(mx, fabs(hR[i])); }
+    printf("fused W=%d n=%d nmat=%d ns=%d: %.4f ms (%.1f GB/s packed, %.1f dense-equiv)  max|err| %.3e (max|u| %.3e)\n",
+           Wr, n, nmat, ns, msa, packed_b / msa / 1e6, dense_b / msa / 1e6, err, mx);
+    return 0;
+  }
   for (int it = 0; it < reps + 2; ++it) {
     cudaEventRecord(e0);
     phase_a<<<nsm, 288, smem>>>(g, units, Qp, nmat, x, Pt, ns, slot, xs_bytes, pf, nocomp);
