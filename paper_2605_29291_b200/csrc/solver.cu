@@ -344,6 +344,7 @@ struct rapdb_ctx {
   int* d_ints = nullptr;
   long long* d_ll = nullptr;   // factored: rblk and W-chunk prefix tables
   sym::Unit* d_units = nullptr;  // packed layout: unit table
+  SolverState* h_state = nullptr;  // page-locked copy of the device state (+ abort flag)
   long long ws_bytes = 0;
   long long stage_cap = 0;  // doubles available in the staging area
   bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
@@ -513,7 +514,10 @@ int wait_stream(rapdb_ctx* c) {
       c->err = msg;
       return RAPDB_EDEVICE;
     }
-    std::this_thread::sleep_for(std::chrono::microseconds(100));
+    // spin for the first 2 ms (a sharded run comes back here at every
+    // exchange point, typically after tens of microseconds), then back off
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2))
+      std::this_thread::sleep_for(std::chrono::microseconds(100));
   }
   cudaEventDestroy(ev);
   return RAPDB_OK;
@@ -525,9 +529,13 @@ int read_state(rapdb_ctx* c, SolverState* st) {
     const int wr = wait_stream(c);   // poll first: a pageable D2H copy would block behind a hung kernel
     if (wr) return wr;
   }
-  CK(cudaMemcpyAsync(st, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(&ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (!c->h_state) CK(cudaMallocHost(&c->h_state, sizeof(SolverState) + 64));
+  int* h_ab = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_state) + sizeof(SolverState));
+  CK(cudaMemcpyAsync(c->h_state, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(h_ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  *st = *c->h_state;
+  ab = *h_ab;
   if (ab) {
     int info[20] = {0};
     cudaMemcpy(info, c->w.abort_flag, sizeof(info), cudaMemcpyDeviceToHost);
@@ -625,6 +633,7 @@ void rapdb_destroy(rapdb_ctx* c) {
   if (c->d_ints) cudaFree(c->d_ints);
   if (c->d_ll) cudaFree(c->d_ll);
   if (c->d_units) cudaFree(c->d_units);
+  if (c->h_state) cudaFreeHost(c->h_state);
   delete c;
 }
 
