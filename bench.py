@@ -55,7 +55,8 @@ def parse():
                     help="with N>1: independent replicas instead of constraint sharding")
     ap.add_argument("--shard", action="store_true",
                     help="force the constraint-sharded (NCCL exchange) path even with one rank")
-    ap.add_argument("--cpu-sample-iters", type=int, default=2)
+    ap.add_argument("--cpu-sample-iters", type=int, default=24,
+                    help="accepted C1 iterations per CPU sample (~0.25 s each on 16 cores)")
     ap.add_argument("--skip-cpu", action="store_true")
     return ap.parse_args()
 

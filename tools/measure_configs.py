@@ -28,6 +28,9 @@ if name == "C2":
 elif name == "C3":
     arr = instances.factored_qcqp()
     inst = R.FactoredInstance.from_arrays(arr)
+elif name == "C3f":   # C3 with x0 ~ U(-0.01, 0.01): the BASELINE C3 (x0 ~ U(-1, 1)) is infeasible
+    arr = instances.factored_qcqp(x0_scale=0.01)
+    inst = R.FactoredInstance.from_arrays(arr)
 else:
     arr = instances.config_instance(name)
     inst = R.ProblemInstance.from_arrays(arr, validate=False)
