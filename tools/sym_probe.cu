@@ -260,6 +260,99 @@ __global__ void __launch_bounds__(288, 1) phase_fused(Geom g, const Unit* __rest
   }
 }
 
+// Half-unit ring: 16 KB slots, each unit's sub-rows in consecutive slots;
+// slot tags make any distance between a warp's slots safe (a wait starts only
+// once the producer has tagged the slot with the expected sequence number).
+__global__ void __launch_bounds__(256, 1) phase_half(Geom g, const Unit* __restrict__ units,
+                                                     const double* __restrict__ Qp, int nmat,
+                                                     const double* __restrict__ x, double* __restrict__ Pt,
+                                                     int ns, int slot_bytes, int xs_bytes) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ unsigned tag[64];
+  double* xs = reinterpret_cast<double*>(sm);
+  unsigned char* ring = sm + xs_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (long long)ns * slot_bytes);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[s])), "r"(1));
+      tag[s] = 0xffffffffu;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int j = threadIdx.x; j < g.nbB * kB; j += blockDim.x) xs[j] = j < g.n ? x[j] : 0.0;
+  __syncthreads();
+  const long long total = (long long)nmat * g.upm;
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
+  const int ncw = 7;
+  const long long mat_doubles = g.spm * kTD;
+  const long long pstride = (long long)g.nbB * g.nbB * kB;
+  volatile unsigned* vtag = tag;
+  if (warp == 7) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      long long a = b / g.upm;
+      int u = (int)(b - a * g.upm);
+      unsigned q = 0;
+      int s = 0;
+      unsigned use = 0;
+      for (long long k = 0; k < mine; ++k) {
+        const Unit un = units[u];
+        int rs, cs;
+        unit_subtiles(g, un.bi, un.bj, rs, cs);
+        const bool diag = un.bi == un.bj;
+        const double* base = Qp + a * mat_doubles + (long long)un.off * kTD;
+        for (int h = 0; h < rs; ++h) {
+          int first, count;
+          unit_half(diag, rs, cs, h, first, count);
+          if (use > 0) while (!try_wait(&empty[s], (use - 1) & 1)) {}
+          vtag[s] = q;
+          const unsigned bytes = (unsigned)count * kTD * 8;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                       ::"r"(su32(ring + (long long)s * slot_bytes)), "l"(base + (long long)first * kTD),
+                       "r"(bytes), "r"(su32(&full[s])), "l"(pol) : "memory");
+          ++q;
+          if (++s == ns) { s = 0; ++use; }
+        }
+        u += G;
+        while (u >= g.upm) { u -= g.upm; ++a; }
+      }
+    }
+  } else {
+    // every consumer walks the CTA's unit sequence to track slot numbers
+    long long a = b / g.upm;
+    int u = (int)(b - a * g.upm);
+    unsigned q = 0;
+    const uint64_t keep = evict_last_policy();
+    HalfState hs;
+    for (long long k = 0; k < mine; ++k) {
+      const Unit un = units[u];
+      const int rs = (2 * un.bi + 1 < g.nb32) ? 2 : 1;
+      if ((int)(k % ncw) == warp) {
+        for (int h = 0; h < rs; ++h) {
+          const unsigned qq = q + h;
+          const int s = (int)(qq % ns);
+          while (vtag[s] != qq) {}
+          while (!try_wait(&full[s], (qq / ns) & 1)) {}
+          consume_half(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj, h,
+                       Pt + a * pstride, keep, hs);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+        }
+      }
+      q += rs;
+      u += G;
+      while (u >= g.upm) { u -= g.upm; ++a; }
+    }
+  }
+}
+
 __global__ void phase_b(Geom g, int nmat, const double* __restrict__ Pt, double* __restrict__ U) {
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -323,6 +416,34 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   float msa = 0, msb = 0;
   const int W = argc > 7 ? atoi(argv[7]) : 0;
+  if (W < 0) {   // half-unit ring (16 KB slots)
+    const int hslot = 2 * kTD * 8;
+    const int hns = -W;
+    const int hsmem = xs_bytes + hns * hslot + 2 * hns * 8;
+    CK(cudaFuncSetAttribute(phase_half, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
+    for (int it = 0; it < reps + 2; ++it) {
+      cudaEventRecord(e0);
+      phase_half<<<nsm, 256, hsmem>>>(g, units, Qp, nmat, x, Pt, hns, hslot, xs_bytes);
+      cudaEventRecord(e1);
+      phase_b<<<nsm * 4, 256>>>(g, nmat, Pt, U);
+      cudaEventRecord(e2);
+      CK(cudaEventSynchronize(e2));
+      float a_, b_;
+      cudaEventElapsedTime(&a_, e0, e1);
+      cudaEventElapsedTime(&b_, e1, e2);
+      if (it >= 2) { msa += a_; msb += b_; }
+    }
+    CK(cudaGetLastError());
+    msa /= reps; msb /= reps;
+    std::vector<double> hU((long long)nmat * n), hR((long long)nmat * n);
+    CK(cudaMemcpy(hU.data(), U, hU.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hR.data(), Uref, hR.size() * 8, cudaMemcpyDeviceToHost));
+    double err = 0, mx = 0;
+    for (size_t i = 0; i < hU.size(); ++i) { err = fmax(err, fabs(hU[i] - hR[i])); mx = fmax(mx, fabs(hR[i])); }
+    printf("half ns=%d n=%d nmat=%d: phaseA %.4f ms (%.1f GB/s packed)  phaseB %.4f  total %.4f ms  max|err| %.3e (max|u| %.3e)\n",
+           hns, n, nmat, msa, packed_b / msa / 1e6, msb, msa + msb, err, mx);
+    return 0;
+  }
   if (W > 0) {   // fused stream + reduction with a W-matrix partial ring
     int *cnt, *red;
     CK(cudaMalloc(&cnt, nmat * 4));
