@@ -793,6 +793,7 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   if (e != cudaSuccess) return cuda_fail(c, e, "occupancy");
   if (occ < 1) return fail(c, RAPDB_EDEVICE, "solver kernel cannot be resident");
   c->G = c->nsm * occ;
+  if (c->G > 256) c->G = 256;   // get_totals keeps <= 8 partials per lane
   const int G = c->G;
   // row partition of the streamed rows over CTAs and the segment tables
   const long long R = (long long)act.size() * n;

@@ -94,8 +94,14 @@ __device__ __forceinline__ void get_totals(const KArgs& K, Sm& S, const int (&sl
   const int G = gridDim.x;
   for (int k = w; k < NK; k += kWarps) {
     const double* p = K.w.part + (long long)slots[k] * G;
+    // all of a lane's partials in flight at once (G <= 8 * 32), summed in
+    // index order: one L2 round trip instead of G / 32 dependent ones
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = (lane + 32 * t < G) ? ldcg(p + lane + 32 * t) : 0.0;
     double s = 0.0;
-    for (int i = lane; i < G; i += 32) s += ldcg(p + i);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += v[t];
     s = warp_sum(s);
     if (lane == 0) S.tot[slots[k]] = s;
   }
@@ -669,6 +675,20 @@ __device__ void recombine_cols(const KArgs& K, Sm& S, const double* Upar, const 
       if (lm == 0 && P.k0 == 0 && l1 > 0) {
         acc = ldcg(Upar + j) + __ldg(P.q + j);
         lm = 1;
+      }
+      for (; lm + 7 < l1; lm += 8) {     // 16 loads in flight per lane
+        double u[8], qq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          u[k] = ldcg(Upar + (long long)(lm + k) * n + j);
+          qq[k] = __ldg(P.q + (long long)(P.k0 + lm + k) * n + j);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double l = lam_s[P.k0 + lm + k - 1];
+          const double t = l * (u[k] + qq[k]);
+          acc = (l != 0.0) ? acc + t : acc;
+        }
       }
       for (; lm + 3 < l1; lm += 4) {
         double u[4], qq[4];

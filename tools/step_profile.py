@@ -18,12 +18,13 @@ inst = R.ProblemInstance.from_arrays(arr, validate=False)
 crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
 cfg = R.SolverConfig(mode="yx", nonmonotone=nm)
 pol = R.FixedRestart(500)
-for k in range(2):
+for k in range(int(os.environ.get("REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = R.run_restarted(inst, cfg, pol, budget=1000 if nm else 50_000, criteria=crit)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    print(f"solve {k}: {dt * 1e3:.1f} ms wall, kernel {res.device_stats['kernel_ms']:.1f} ms", flush=True)
 print(f"{name} {'nm' if nm else 'mono'}: {res.iterations} it, {res.evals} evals, {dt * 1e3:.1f} ms "
       f"({res.iterations / dt:.1f} it/s), kernel {res.device_stats['kernel_ms']:.1f} ms, "
       f"sweeps {res.device_stats['sweeps']} in {res.device_stats['sweep_ns'] / 1e6:.1f} ms")
