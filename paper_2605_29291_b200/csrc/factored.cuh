@@ -177,27 +177,31 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
   for (long long r = gtid(); r < P.nr; r += gstride())
     st_keep(Wl + r, wq[ld_stream(P.rmat + r, ef)] * ldcg(Wpar + r), el);
   if (!gsync(K, S)) return false;
-  const int sub = lane & 7, grp = lane >> 3;
-  for (long long jb = gwarp() * 4; jb < n; jb += nwarps() * 4) {
+  // 2 lanes per column (16 columns per warp): at the persistent kernel's 8
+  // warps per SM this beats 8 lanes (0.51 vs 0.71 ms for the C3 R^T gather,
+  // tools/csr_probe.cu); each lane keeps 2 gathers in flight
+  constexpr int LW = 2;
+  const int sub = lane & (LW - 1), grp = lane / LW;
+  for (long long jb = gwarp() * (32 / LW); jb < n; jb += nwarps() * (32 / LW)) {
     const long long j = jb + grp;
     double s = 0.0, t = 0.0;
     if (j < n) {
       const long long k0 = __ldg(P.rt_ptr + j), k1 = __ldg(P.rt_ptr + j + 1);
       long long k = k0 + sub;
-      for (; k + 8 < k1; k += 16) {
-        const int r0 = ld_stream(P.rt_row + k, ef), r1 = ld_stream(P.rt_row + k + 8, ef);
-        const double v0 = ld_stream(P.rt_val + k, ef), v1 = ld_stream(P.rt_val + k + 8, ef);
+      for (; k + LW < k1; k += 2 * LW) {
+        const int r0 = ld_stream(P.rt_row + k, ef), r1 = ld_stream(P.rt_row + k + LW, ef);
+        const double v0 = ld_stream(P.rt_val + k, ef), v1 = ld_stream(P.rt_val + k + LW, ef);
         const double w0 = ldcg(Wl + r0), w1 = ldcg(Wl + r1);
         s = fma(v0, w0, s);
         s = fma(v1, w1, s);
       }
       if (k < k1) s = fma(ld_stream(P.rt_val + k, ef), ldcg(Wl + ld_stream(P.rt_row + k, ef)), s);
       const long long a0 = __ldg(P.at_ptr + j), a1 = __ldg(P.at_ptr + j + 1);
-      for (long long k = a0 + sub; k < a1; k += 8)
+      for (long long k = a0 + sub; k < a1; k += LW)
         t = fma(ld_stream(P.at_val + k, ef), ldcg(lam + P.mq + P.l0 + ld_stream(P.at_row + k, ef)), t);
     }
 #pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) {
+    for (int o = LW / 2; o >= 1; o >>= 1) {
       s += __shfl_xor_sync(0xffffffffu, s, o);
       t += __shfl_xor_sync(0xffffffffu, t, o);
     }

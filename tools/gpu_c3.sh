@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_factored.py -q -p no:cacheprovider -x 2>&1 | grep -E "passed|failed|Error|assert" | head
+timeout 900 python -m pytest tests/test_gpu_factored.py -q -p no:cacheprovider -x 2>&1 | tail -2
 python tools/profile_grad.py C3 2
-timeout 900 python tools/measure_configs.py C3 2000 mono > gpurun_out/m_c3.json 2> gpurun_out/m_c3.err; tail -2 gpurun_out/m_c3.err; cat gpurun_out/m_c3.json
+timeout 900 python tools/measure_configs.py C3f 30000 mono > gpurun_out/m_c3f.json 2> gpurun_out/m_c3f.err; tail -2 gpurun_out/m_c3f.err; cut -c1-300 gpurun_out/m_c3f.json; python -c "import json; d=json.load(open('gpurun_out/m_c3f.json')); print(d['step_profile_ms'], d['sweep_ms_each'])"

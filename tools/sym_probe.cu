@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(288, 1) phase_fused(Geom g, const Unit* __rest
       if (lane == 0) {
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
         __threadfence();
-        atomicAdd(cnt + a, 1);
+        atomicAdd(cnt + (a * 8 + (b & 7)) * 32, 1);   // 8 sub-counters per matrix, one 128-B line each
       }
       u += ncw * G;
       while (u >= g.upm) { u -= g.upm; ++a; }
@@ -236,7 +236,13 @@ __global__ void __launch_bounds__(288, 1) phase_fused(Geom g, const Unit* __rest
     for (long long t = b; t < (long long)nmat * nbB; t += G) {
       const long long a = t / nbB;
       const int B = (int)(t - a * nbB);
-      while (ld_acquire(cnt + a) < cnt_done) __nanosleep(64);
+      for (;;) {
+        int c = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c += ld_acquire(cnt + (a * 8 + q) * 32);
+        if (c >= cnt_done) break;
+        __nanosleep(64);
+      }
       const double2* p = reinterpret_cast<const double2*>(Pt + ((a % W) * nbB + B) * (long long)nbB * kB) + lane;
       double sx = 0.0, sy = 0.0;
       int K = 0;
@@ -446,9 +452,9 @@ int main(int argc, char** argv) {
   }
   if (W > 0) {   // fused stream + reduction with a W-matrix partial ring
     int *cnt, *red;
-    CK(cudaMalloc(&cnt, nmat * 4));
+    CK(cudaMalloc(&cnt, nmat * 8 * 32 * 4));
     CK(cudaMalloc(&red, nmat * 4));
-    CK(cudaMemset(cnt, 0, nmat * 4));
+    CK(cudaMemset(cnt, 0, nmat * 8 * 32 * 4));
     CK(cudaMemset(red, 0, nmat * 4));
     CK(cudaFuncSetAttribute(phase_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int Wr = W < nmat ? W : nmat;
