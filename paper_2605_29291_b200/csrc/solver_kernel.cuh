@@ -154,13 +154,33 @@ __device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par) {
   const long long items = (long long)P.p + P.nzero;
   for (long long it = (long long)blockIdx.x * kWarps + warp; it < items; it += (long long)gridDim.x * kWarps) {
     const double* vec = it < P.p ? P.A + it * n : P.q + (long long)(P.k0 + __ldg(P.zero_list + (it - P.p))) * n;
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(__ldg(vec + j), S.xs[j], s);
-    s = warp_sum(s);
+    // 4 independent chains per lane (8 loads in flight), combined in fixed order
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = lane;
+    for (; j + 96 < n; j += 128) {
+      const double a0 = __ldg(vec + j), a1 = __ldg(vec + j + 32), a2 = __ldg(vec + j + 64), a3 = __ldg(vec + j + 96);
+      s0 = fma(a0, S.xs[j], s0);
+      s1 = fma(a1, S.xs[j + 32], s1);
+      s2 = fma(a2, S.xs[j + 64], s2);
+      s3 = fma(a3, S.xs[j + 96], s3);
+    }
+    for (; j < n; j += 32) s0 = fma(__ldg(vec + j), S.xs[j], s0);
+    double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
       if (it < P.p) K.w.eqv[(long long)par * P.p + it] = s - __ldg(P.b + it);
       else K.w.zq[it - P.p] = s;
     }
+  }
+}
+
+// sub-phase timing of the packed sweep on CTA 0 (step-profile slots 36..38:
+// x staging, stream, reduce+tail)
+__device__ __forceinline__ void sub_time(Sm& S, int slot, unsigned long long& t) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long now = globaltimer();
+    if (now > t) S.st->step_ns[slot] += (double)(now - t);
+    S.st->step_cnt[slot] += 1;
+    t = now;
   }
 }
 
@@ -175,10 +195,26 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   const sym::Geom& g = sp.geom;
   const int n = P.n;
   const int xlen = g.nbB * sym::kB;
-  for (int j = threadIdx.x; j < xlen; j += kThreads) S.xs[j] = (j < n) ? ldcg(xsrc + j) : 0.0;
+  unsigned long long tsub = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) tsub = globaltimer();
+  // stage x (zero padded): all of a thread's loads in flight at once
+  for (int j0 = threadIdx.x; j0 < xlen; j0 += 8 * kThreads) {
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = j0 + t * kThreads;
+      v[t] = (j < n) ? ldcg(xsrc + j) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = j0 + t * kThreads;
+      if (j < xlen) S.xs[j] = v[t];
+    }
+  }
   // generic-proxy use of the ring (dual staging) before the bulk copies below
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  sub_time(S, 36, tsub);
   const int G = gridDim.x, b = blockIdx.x;
   const long long total = (long long)P.nact * g.upm;
   const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
@@ -246,6 +282,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   }
   S.pseq = base + (unsigned)mine;
   if (!gsync(K, S)) return;   // aborted: the caller's barrier reports it
+  sub_time(S, 37, tsub);
   // phase B: u = sum_K Pt[a][B][K] (K order), U-cache rows, block x.u and q.x
   const int nbB = g.nbB;
   const long long items = (long long)P.nact * nbB;
@@ -256,7 +293,14 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
     double sx = 0.0, sy = 0.0;
     int kk = 0;
-    for (; kk + 16 <= nbB; kk += 16) {   // 16 x 512 B in flight per warp (the reads are DRAM-bound)
+    for (; kk + 32 <= nbB; kk += 32) {   // 32 x 512 B in flight per warp
+      double2 t[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) { sx += t[q].x; sy += t[q].y; }
+    }
+    for (; kk + 16 <= nbB; kk += 16) {
       double2 t[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
@@ -297,6 +341,8 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     }
   }
   sweep_tail(K, S, par);
+  __syncthreads();
+  sub_time(S, 38, tsub);
 }
 
 __device__ __noinline__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
