@@ -212,6 +212,16 @@ int rapdb_reinit(rapdb_ctx* ctx, int source, const double* x, const double* v,
  * a device buffer of max_iters * RAPDB_TRACE_COLS doubles (row-major).        */
 int rapdb_run(rapdb_ctx* ctx, const rapdb_run_args* args, double* trace, rapdb_run_result* out);
 
+/* Extragradient baseline (egm.py:37-77) from the
+ * current point (set it with rapdb_reinit: the projection Pi of egm.py:52):
+ * K iterations of z~ = Pi(z - s F(z)), z+ = Pi(z - s F(z~)), two sweeps each,
+ * stopping early when |z| > 1e8 (1 + |z0|).  Afterwards rapdb_get_iterate
+ * returns the last point (which 0) and the plain average (which 1).  trace:
+ * device buffer of (K / trace_every) rows (iter, |z|), or NULL with
+ * trace_every = 0.                                                          */
+int rapdb_egm(rapdb_ctx* ctx, double stepsize, long long K, int trace_every, double* trace,
+              long long* iterations, int* diverged);
+
 /* kkt_residual at the current iterate (diagnostics.py:96-113); out[8] host   */
 int rapdb_kkt(rapdb_ctx* ctx, int has_f_star, double f_star, double* out);
 

@@ -48,14 +48,15 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
            "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x",
            "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric",
-           "rapdb_bind_factored_range"]
+           "rapdb_bind_factored_range", "rapdb_egm"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
               "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
               "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
               "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN",
-              "DONE", "sweep:stage_x", "sweep:stream", "sweep:reduce"]
+              "E_INIT", "E_GX", "E_HALF", "E_HSWEEP", "E_HGLOC", "E_GXH", "E_PLUS", "E_PSWEEP", "E_PGLOC",
+              "E_POST", "DONE"] + [""] * 14 + ["sweep:stage_x", "sweep:stream", "sweep:reduce", ""]
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
@@ -120,6 +121,7 @@ def load(path: str = LIB_PATH):
     lib.rapdb_step_profile.argtypes = [P, C.POINTER(D), C.POINTER(LL), I]
     lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 19 + [D]
     lib.rapdb_bind_factored_range.argtypes = [P, I, I, I, I, I, I, I, LL] + [P] * 19 + [D]
+    lib.rapdb_egm.argtypes = [P, D, LL, I, P, C.POINTER(LL), C.POINTER(I)]
     lib.rapdb_grad_x.argtypes = [P, P, P, P, P, P]
     _lib = lib
     return lib
@@ -211,9 +213,9 @@ class Context:
 
     def step_profile(self):
         """{step name: (total device ms, calls)} accumulated since bind."""
-        ns = (C.c_double * 40)()
-        cnt = (C.c_longlong * 40)()
-        self._check(self.lib.rapdb_step_profile(self.h, ns, cnt, 40))
+        ns = (C.c_double * 64)()
+        cnt = (C.c_longlong * 64)()
+        self._check(self.lib.rapdb_step_profile(self.h, ns, cnt, 64))
         return {name: (ns[i] / 1e6, int(cnt[i])) for i, name in enumerate(STEP_NAMES) if cnt[i]}
 
     # -- binding -----------------------------------------------------------
@@ -283,6 +285,19 @@ class Context:
         self._check(self.lib.rapdb_kkt(self.h, 0 if f_star is None else 1,
                                        0.0 if f_star is None else float(f_star), out))
         return list(out)
+
+    def egm(self, stepsize: float, K: int, trace_every: int = 0):
+        """Extragradient iterations from the current point (egm.py:37-77);
+        returns (iterations, diverged, trace rows (iter, |z|) as a host array)."""
+        torch = self.torch
+        rows = (K // trace_every) if trace_every > 0 else 0
+        tr = torch.zeros((max(rows, 1), 2), dtype=torch.float64, device=self.device)
+        it = C.c_longlong()
+        dv = C.c_int()
+        self._set_stream()
+        self._check(self.lib.rapdb_egm(self.h, float(stepsize), int(K), int(trace_every),
+                                       _ptr(tr) if rows else None, C.byref(it), C.byref(dv)))
+        return int(it.value), bool(dv.value), tr[:rows].cpu().numpy()
 
     def get_iterate(self, which: int):
         torch = self.torch

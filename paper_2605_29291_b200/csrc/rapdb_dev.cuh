@@ -44,10 +44,11 @@ enum Slot {
   S_PHIV, S_PHIL,                               // Phi at a (re)start point
   S_AVG_V, S_AVG_L,                             // ball norms of an average point
   S_GAPQ,                                       // z'Hz in the smoothed-gap subsolver
+  S_EGM_X, S_EGM_V, S_EGM_L,                    // EGM: |x|^2, |v|^2, |lam|^2 of a point
   NSLOT
 };
 
-enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5, OP_GRAD = 6 };
+enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5, OP_GRAD = 6, OP_EGM = 7 };
 enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
                  ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6, ST_EXCHANGE = 7, ST_RUNNING = 8 };
 
@@ -63,8 +64,8 @@ struct SolverState {
   double tau, tau_start, slack, sigma, alpha_n, beta_n, phi_new, theta;
   long long call_done;     // accepted iterations in the current rapdb_run call
   int step, ret, kret, xkind, evals, rsrc, rwarm, pad2;
-  double step_ns[40];      // device time per state-machine step (CTA 0, globaltimer)
-  long long step_cnt[40];
+  double step_ns[64];      // device time per state-machine step (CTA 0, globaltimer); 60..62: sweep sub-phases
+  long long step_cnt[64];
 };
 
 // steps of the resumable op state machine
@@ -76,6 +77,7 @@ enum Step {
   R_POINT, R_SWEEP, R_GLOCAL, R_CACHE, R_GXPART, R_GXCACHE, R_FINISH,
   G_CAND, G_GLOCAL, G_HPART, G_SOLVE,
   P_SWEEP, P_OUT, P_GRAD, P_GFIN,
+  E_INIT, E_GX, E_HALF, E_HSWEEP, E_HGLOC, E_GXH, E_PLUS, E_PSWEEP, E_PGLOC, E_POST,
   DONE
 };
 // exchange kinds: what the host must all-reduce (sum) across ranks before resuming
@@ -160,6 +162,9 @@ struct RunCfg {
 
   double eps, eps_kkt, eps_feas, f_star;
   double xi, tol;                  // smoothed gap
+  double egm_s;                    // EGM stepsize
+  long long egm_K;                 // EGM iterations
+  int egm_trace_every, egm_pad;
   const double* warm;              // smoothed gap subsolver warm start (or null)
   const double* in_x; const double* in_v; const double* in_lam;   // explicit points
   double* out_x; double* out_v; double* out_lam; double* out_u; double* out_g;

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "egm.cuh"
 #include "gap.cuh"
 #include "rapdb_b200.h"
 #include "solver_ops.cuh"
@@ -186,6 +187,9 @@ __device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
       }
       return DONE;
     }
+    case E_INIT: case E_GX: case E_HALF: case E_HSWEEP: case E_HGLOC:
+    case E_GXH: case E_PLUS: case E_PSWEEP: case E_PGLOC: case E_POST:
+      return egm_step(K, S, step, xk);
     default:
       return kAbort;
   }
@@ -214,7 +218,7 @@ __device__ void drive(const KArgs& K, Sm& S) {
       bcn[3] = (int)S.pseq;
     }
     const int next = run_step(K, S, step, xk);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && step < 40) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && step < 60) {
       const unsigned long long t1 = globaltimer();
       if (t1 > t0) st.step_ns[step] += (double)(t1 - t0);
       st.step_cnt[step] += 1;
@@ -310,6 +314,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
         case OP_KKT: s_st.step = K_GXPART; s_st.kret = DONE; break;
         case OP_GAP: s_st.step = G_CAND; break;
         case OP_PROBE: case OP_GRAD: s_st.step = P_SWEEP; break;
+        case OP_EGM: s_st.step = E_INIT; break;
         default: s_st.step = DONE; break;
       }
     } else {
@@ -594,7 +599,7 @@ int rapdb_step_profile(rapdb_ctx* c, double* ns, long long* counts, int nsteps) 
   SolverState st;
   int r = read_state(c, &st);
   if (r) return r;
-  for (int i = 0; i < nsteps && i < 40; ++i) {
+  for (int i = 0; i < nsteps && i < 64; ++i) {
     ns[i] = st.step_ns[i];
     counts[i] = st.step_cnt[i];
   }
@@ -1024,6 +1029,31 @@ int rapdb_reinit(rapdb_ctx* c, int source, const double* x, const double* v, con
   if (r) return r;
   SolverState st;
   return read_state(c, &st);
+}
+
+int rapdb_egm(rapdb_ctx* c, double stepsize, long long K, int trace_every, double* trace, long long* iterations,
+              int* diverged) {
+  if (!c || !iterations || !diverged) return RAPDB_EINPUT;
+  if (!(stepsize >= 0.0)) return fail(c, RAPDB_ECONFIG, "stepsize must be nonnegative");
+  if (K < 1) return fail(c, RAPDB_ECONFIG, "need K >= 1");
+  if (trace_every < 0 || (trace_every > 0 && !trace)) return fail(c, RAPDB_EINPUT, "trace_every needs a trace buffer");
+  RunCfg rc{};
+  rc.op = OP_EGM;
+  rc.egm_s = stepsize;
+  rc.egm_K = K;
+  rc.egm_trace_every = trace_every;
+  Work saved = c->w;
+  c->w.trace = trace_every > 0 ? trace : nullptr;
+  int r = launch(c, rc);
+  c->w = saved;
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  if (r) return r;
+  if (st.status == ST_ABORT) return fail(c, RAPDB_EDEVICE, "EGM op aborted");
+  *iterations = st.call_done;
+  *diverged = st.fail_iter ? 1 : 0;
+  return RAPDB_OK;
 }
 
 int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_result* out) {

@@ -173,7 +173,7 @@ __device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par) {
   }
 }
 
-// sub-phase timing of the packed sweep on CTA 0 (step-profile slots 36..38:
+// sub-phase timing of the packed sweep on CTA 0 (step-profile slots 60..62:
 // x staging, stream, reduce+tail)
 __device__ __forceinline__ void sub_time(Sm& S, int slot, unsigned long long& t) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -214,7 +214,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   // generic-proxy use of the ring (dual staging) before the bulk copies below
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  sub_time(S, 36, tsub);
+  sub_time(S, 60, tsub);
   const int G = gridDim.x, b = blockIdx.x;
   const long long total = (long long)P.nact * g.upm;
   const long long mine = total > b ? (total - 1 - b) / G + 1 : 0;
@@ -282,7 +282,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   }
   S.pseq = base + (unsigned)mine;
   if (!gsync(K, S)) return;   // aborted: the caller's barrier reports it
-  sub_time(S, 37, tsub);
+  sub_time(S, 61, tsub);
   // phase B: u = sum_K Pt[a][B][K] (K order), U-cache rows, block x.u and q.x
   const int nbB = g.nbB;
   const long long items = (long long)P.nact * nbB;
@@ -342,7 +342,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   }
   sweep_tail(K, S, par);
   __syncthreads();
-  sub_time(S, 38, tsub);
+  sub_time(S, 62, tsub);
 }
 
 __device__ __noinline__ void sweep(const KArgs& K, Sm& S, const double* xsrc, int par) {
