@@ -163,3 +163,44 @@ def ball_code(ball):
     if isinstance(ball, SplitBall):
         return 2, float(ball.radius_v), float(ball.radius_lam)
     raise ConfigurationError(f"dual ball {type(ball).__name__} is not supported")
+
+
+# ---- JSON descriptors (geometry.py:376-421 of the reference) --------------
+def set_to_json(s) -> dict:
+    if isinstance(s, Box):
+        return {"type": "box", "lower": list(s.lower), "upper": list(s.upper)}
+    from .errors import ConfigurationError
+    raise ConfigurationError(f"primal set {type(s).__name__} is not built on the device path")
+
+
+def set_from_json(d: dict):
+    from .errors import ConfigurationError, InputError
+    try:
+        kind = d["type"]
+        if kind == "box":
+            return Box(np.asarray(d["lower"], float), np.asarray(d["upper"], float))
+    except (KeyError, TypeError) as exc:
+        raise InputError(f"bad set descriptor {d!r}: {exc}") from exc
+    if kind in ("ball", "simplex", "nonneg_lineq"):
+        raise ConfigurationError(f"primal set type {kind!r} is not built on the device path")
+    raise InputError(f"unknown set type {kind!r}")
+
+
+def cone_to_json(c) -> dict:
+    if isinstance(c, NonnegOrthant):
+        return {"type": "orthant", "dim": c.dim}
+    from .errors import ConfigurationError
+    raise ConfigurationError(f"cone {type(c).__name__} is not built on the device path")
+
+
+def cone_from_json(d: dict):
+    from .errors import ConfigurationError, InputError
+    try:
+        kind = d["type"]
+        if kind == "orthant":
+            return NonnegOrthant(int(d["dim"]))
+    except (KeyError, TypeError) as exc:
+        raise InputError(f"bad cone descriptor {d!r}: {exc}") from exc
+    if kind in ("soc", "product"):
+        raise ConfigurationError(f"cone type {kind!r} is not built on the device path")
+    raise InputError(f"unknown cone type {kind!r}")

@@ -403,3 +403,97 @@ class DeviceDenseInstance:
 
     def project_dual_cone(self, lam):
         return np.maximum(np.asarray(lam, dtype=float), 0.0)
+
+
+# ---------------------------------------------------------------------------
+# The reference's problem JSON (problem.py:318-389): dense matrices as nested
+# lists, sparse ones as {"format": "csr", ...}; sets and cones as descriptors.
+
+def _matrix_to_json(M):
+    M = np.asarray(M)
+    if M.ndim == 2 and M.size and np.count_nonzero(M) < 0.25 * M.size:
+        import scipy.sparse as sp
+        S = sp.csr_matrix(M)
+        return {"format": "csr", "shape": list(S.shape), "indptr": S.indptr.tolist(),
+                "indices": S.indices.tolist(), "data": S.data.tolist()}
+    return M.tolist()
+
+
+def _matrix_from_json(obj, shape):
+    if isinstance(obj, dict):
+        if obj.get("format") != "csr":
+            raise InputError(f"unknown matrix format {obj.get('format')!r}")
+        import scipy.sparse as sp
+        return sp.csr_matrix((obj["data"], obj["indices"], obj["indptr"]),
+                             shape=tuple(obj.get("shape", shape))).toarray()
+    return np.asarray(obj, dtype=float).reshape(shape)
+
+
+def to_json_dict(inst: ProblemInstance) -> dict:
+    from .geometry import cone_to_json, set_to_json
+    out = {
+        "n": inst.n, "m": inst.m, "p": inst.p,
+        "Q": [_matrix_to_json(inst.Q[i]) for i in range(inst.m + 1)],
+        "q": [v.tolist() for v in inst.q],
+        "r": inst.r.tolist(),
+        "A": np.asarray(inst.A).tolist(),
+        "b": inst.b.tolist(),
+        "primal_set": set_to_json(inst.primal_set),
+        "cone": cone_to_json(inst.cone),
+        "mu": inst.mu,
+    }
+    if inst.name:
+        out["name"] = inst.name
+    return out
+
+
+def from_json_dict(d: dict, validate: bool = True) -> ProblemInstance:
+    from .geometry import cone_from_json, set_from_json
+    if "dual_set" in d:
+        raise ConfigurationError("minimax dual_set instances are not built on the device path")
+    try:
+        n, m, p = int(d["n"]), int(d["m"]), int(d["p"])
+        return ProblemInstance(
+            n=n, m=m, p=p,
+            Q=[_matrix_from_json(M, (n, n)) for M in d["Q"]],
+            q=[np.asarray(v, dtype=float) for v in d["q"]],
+            r=np.asarray(d["r"], dtype=float),
+            A=np.asarray(d["A"], dtype=float).reshape(p, n),
+            b=np.asarray(d["b"], dtype=float),
+            primal_set=set_from_json(d["primal_set"]),
+            cone=cone_from_json(d["cone"]),
+            mu=float(d.get("mu", 0.0)),
+            name=str(d.get("name", "")),
+            validate=validate)
+    except (KeyError, TypeError, ValueError) as exc:
+        if isinstance(exc, (InputError, ConfigurationError)):
+            raise
+        raise InputError(f"malformed problem description: {exc}") from exc
+
+
+def save(inst: ProblemInstance, path: str):
+    import json
+    with open(path, "w") as fh:
+        json.dump(to_json_dict(inst), fh)
+
+
+def load(path: str, validate: bool = True) -> ProblemInstance:
+    """Read a problem written by the reference's ``rapdb.problem.save``."""
+    import json
+    with open(path) as fh:
+        return from_json_dict(json.load(fh), validate=validate)
+
+
+def save_stack(inst: ProblemInstance, path: str):
+    """Binary form for multi-GB instances (the JSON is impractical at C1/C2
+    sizes): one .npz with the (m+1, n, n) stack and the vectors."""
+    np.savez(path, n=inst.n, m=inst.m, p=inst.p, Q=inst.Q, q=inst.q, r=inst.r, A=inst.A, b=inst.b,
+             lower=inst.primal_set.lower, upper=inst.primal_set.upper, mu=inst.mu, name=inst.name)
+
+
+def load_stack(path: str, validate: bool = False) -> ProblemInstance:
+    z = np.load(path, allow_pickle=False)
+    return ProblemInstance(n=int(z["n"]), m=int(z["m"]), p=int(z["p"]), Q=z["Q"], q=z["q"], r=z["r"],
+                           A=z["A"], b=z["b"], primal_set=Box(z["lower"], z["upper"]),
+                           cone=NonnegOrthant(int(z["m"])), mu=float(z["mu"]), name=str(z["name"]),
+                           validate=validate)
