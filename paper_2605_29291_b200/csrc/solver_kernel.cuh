@@ -319,6 +319,14 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       const double2 t = __ldcg(pp + kk * 32);
       sx += t.x; sy += t.y;
     }
+    // the item's partials are dead until the next sweep rewrites them: drop
+    // the L2 lines without writing them back to DRAM
+    __syncwarp();
+    {
+      const char* base = reinterpret_cast<const char*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB);
+      for (int L = lane; L < nbB * 4; L += 32)
+        asm volatile("discard.global.L2 [%0], 128;" :: "l"(base + (long long)L * 128) : "memory");
+    }
     const int lm = __ldg(P.act + a);
     const double* qa = P.q + (long long)(P.k0 + lm) * n;
     const int r = B * sym::kB + 2 * lane;
@@ -341,6 +349,25 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     }
   }
   sweep_tail(K, S, par);
+  // The next sweep streams the same units in the same order and only starts
+  // after the trial's control steps (tens of microseconds of latency-bound
+  // work during which HBM would idle): prefetch this CTA's first units of it
+  // into L2 now (fire-and-forget bulk prefetches, no shared memory involved).
+  if (warp == kConsumerWarps && lane == 0 && sp.l2pf > 0) {
+    long long a = b / upm;
+    int u = (int)(b - a * upm);
+    const long long lim = min(mine, (long long)sp.l2pf);
+    for (long long k = 0; k < lim; ++k) {
+      const sym::Unit un = units[u];
+      int rs, cs;
+      const unsigned bytes = (unsigned)sym::unit_subtiles(gg, un.bi, un.bj, rs, cs) * sym::kTD * 8u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   :: "l"(Qst + (long long)__ldg(act + a) * mat_doubles + (long long)un.off * sym::kTD), "r"(bytes)
+                   : "memory");
+      u += G;
+      while (u >= upm) { u -= upm; ++a; }
+    }
+  }
   __syncthreads();
   sub_time(S, 62, tsub);
 }

@@ -13,8 +13,12 @@ from paper_2605_29291_b200 import _capi, instances  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-arr = instances.config_instance(name)
-inst = R.ProblemInstance.from_arrays(arr, validate=False)
+if name == "C2":   # device-generated: the host instance takes minutes and 69 GB
+    inst = R.DeviceDenseInstance(4096, 512, 256)
+    arr = inst
+else:
+    arr = instances.config_instance(name)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
 ev = inst._evaluator()
 x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, arr.n)).cuda()
 for _ in range(2):
