@@ -50,18 +50,20 @@ __device__ __forceinline__ double csr_row_dot(const long long* __restrict__ ptr,
   return s;
 }
 
-// "Sweep" at x into parity par: W = R x (thread per row), A x - b into the
-// linear part of gval[par], chunk partials of c_i . x (warp per 1024 columns),
-// then (after a grid barrier) chunk partials of |W_i|^2 (warp per 1024 rows).
-__device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double* x, int par) {
-  const DevProblem& P = K.P;
-  const Work& w = K.w;
+// "Sweep" at x into parity par, part A: W = R x (thread per row), A x - b
+// into the linear part of gval[par], chunk partials of c_i . x (warp per 1024
+// columns).  Part B (after a grid barrier / kernel boundary): chunk partials
+// of |W_i|^2 (warp per 1024 rows).  Both run inside the persistent kernel
+// (sweep_factored) or as high-occupancy standalone kernels launched by the
+// host at a stop (fac_sweep_*_kernel, the default: the gathers are latency
+// bound and 8 warps per SM starve them -- tools/csr_probe.cu).
+__device__ __forceinline__ void fac_sweep_a(const DevProblem& P, const Work& w, const double* x, int par) {
   const long long n = P.n;
   const int lane = threadIdx.x & 31;
   double* W = w.W + (long long)par * P.nr;
   // thread per CSR row, products summed in stored order without FMA (the
   // operation order of scipy's csr_matvec, so W = R x matches the restatement
-  // bit for bit); the row's loads are issued in batches of 4 for MLP
+  // bit for bit); the row's loads are issued in batches for MLP
   const uint64_t ef = evict_first_policy();
   const uint64_t el = sym::evict_last_policy();
   for (long long r = gtid(); r < P.nr; r += gstride())
@@ -79,7 +81,11 @@ __device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double*
     s = warp_sum(s);
     if (lane == 0) w.pcx[it] = s;
   }
-  if (!gsync(K, S)) return false;
+}
+
+__device__ __forceinline__ void fac_sweep_b(const DevProblem& P, const Work& w, int par) {
+  const int lane = threadIdx.x & 31;
+  const double* W = w.W + (long long)par * P.nr;
   const long long nchw = __ldg(P.wch + P.fnb);
   for (long long c = gwarp(); c < nchw; c += nwarps()) {
     int lo = 0, hi = P.fnb;               // local block of chunk c: wch[lo] <= c < wch[lo+1]
@@ -97,6 +103,12 @@ __device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double*
     s = warp_sum(s);
     if (lane == 0) w.pw2[c] = s;
   }
+}
+
+__device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double* x, int par) {
+  fac_sweep_a(K.P, K.w, x, par);
+  if (!gsync(K, S)) return false;
+  fac_sweep_b(K.P, K.w, par);
   return gsync(K, S);
 }
 
@@ -125,26 +137,22 @@ __device__ void g_factored(const KArgs& K, int par) {
 }
 
 // out = sum_i w_i (R_i^T W_i + c_i) + A^T mu with w = (1, lam_1..lam_mq),
-// mu = lam[mq..]; lam is a global m-vector.  Pass 1 (element-parallel) adds
+// mu = lam[mq..]; lam is a global m-vector.  Part A (element-parallel) adds
 // the dense c_i terms and scales the W-cache by its block weight,
-// Wl[r] = w_{blk(r)} W[r]; pass 2 gathers R^T Wl and A^T mu with 8 lanes per
-// column (4 columns per warp, 8 independent load chains per column), so the
-// ~65 nnz of a C3 column are fetched in ~8 dependent steps instead of ~3 per
-// lane-round.  The result is complete after the caller's grid barrier.
-__device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, const double* lam, double* out) {
-  const DevProblem& P = K.P;
-  const long long n = P.n;
-  const int lane = threadIdx.x & 31;
-  double* wq = S.stage;
-  double* Wl = K.w.wl;
-  const uint64_t ef = evict_first_policy();
-  const uint64_t el = sym::evict_last_policy();
-  __syncthreads();
-  for (int i = threadIdx.x; i < P.fnb; i += kThreads) {
+// Wl[r] = w_{blk(r)} W[r]; part B gathers R^T Wl and A^T mu (2 lanes per
+// column).  wq: the fnb block weights, staged in shared memory by the caller.
+__device__ __forceinline__ void fac_wq(const DevProblem& P, const double* lam, double* wq, int nthreads) {
+  for (int i = threadIdx.x; i < P.fnb; i += nthreads) {
     const int gi = P.fb0 + i;             // global block id (0 = objective)
     wq[i] = gi == 0 ? 1.0 : ldcg(lam + (gi - 1));
   }
-  __syncthreads();
+}
+
+__device__ __forceinline__ void fac_gx_a(const DevProblem& P, const Work& w, const double* Wpar, const double* wq,
+                                         double* out) {
+  const long long n = P.n;
+  const uint64_t ef = evict_first_policy();
+  const uint64_t el = sym::evict_last_policy();
   for (long long j = gtid(); j < n; j += gstride()) {
     double acc = 0.0;
     int i = 0;
@@ -175,12 +183,17 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
     out[j] = acc;
   }
   for (long long r = gtid(); r < P.nr; r += gstride())
-    st_keep(Wl + r, wq[ld_stream(P.rmat + r, ef)] * ldcg(Wpar + r), el);
-  if (!gsync(K, S)) return false;
-  // 2 lanes per column (16 columns per warp): at the persistent kernel's 8
-  // warps per SM this beats 8 lanes (0.51 vs 0.71 ms for the C3 R^T gather,
-  // tools/csr_probe.cu); each lane keeps 2 gathers in flight
-  constexpr int LW = 2;
+    st_keep(w.wl + r, wq[ld_stream(P.rmat + r, ef)] * ldcg(Wpar + r), el);
+}
+
+// LW lanes per column: 2 is best at the persistent kernel's 8 warps per SM,
+// 8 in a standalone kernel with 8 CTAs per SM (tools/csr_probe.cu)
+template <int LW>
+__device__ __forceinline__ void fac_gx_b(const DevProblem& P, const Work& w, const double* lam, double* out) {
+  const long long n = P.n;
+  const int lane = threadIdx.x & 31;
+  const uint64_t ef = evict_first_policy();
+  const double* Wl = w.wl;
   const int sub = lane & (LW - 1), grp = lane / LW;
   for (long long jb = gwarp() * (32 / LW); jb < n; jb += nwarps() * (32 / LW)) {
     const long long j = jb + grp;
@@ -207,7 +220,37 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
     }
     if (j < n && sub == 0) out[j] = (ldcg(out + j) + s) + t;
   }
+}
+
+__device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, const double* lam,
+                                                double* out) {
+  double* wq = S.stage;
+  __syncthreads();
+  fac_wq(K.P, lam, wq, kThreads);
+  __syncthreads();
+  fac_gx_a(K.P, K.w, Wpar, wq, out);
+  if (!gsync(K, S)) return false;
+  fac_gx_b<2>(K.P, K.w, lam, out);
   return true;
+}
+
+// ---- standalone kernels the host launches at a factored stop (fq requests):
+// same device code, any grid (blockDim = kThreads), many CTAs per SM
+__global__ void __launch_bounds__(kThreads) fac_sweep_a_kernel(DevProblem P, Work w, const double* x, int par) {
+  fac_sweep_a(P, w, x, par);
+}
+__global__ void __launch_bounds__(kThreads) fac_sweep_b_kernel(DevProblem P, Work w, int par) {
+  fac_sweep_b(P, w, par);
+}
+__global__ void __launch_bounds__(kThreads) fac_gx_a_kernel(DevProblem P, Work w, const double* Wpar,
+                                                           const double* lam, double* out) {
+  extern __shared__ double wq_s[];
+  fac_wq(P, lam, wq_s, kThreads);
+  __syncthreads();
+  fac_gx_a(P, w, Wpar, wq_s, out);
+}
+__global__ void __launch_bounds__(kThreads) fac_gx_b_kernel(DevProblem P, Work w, const double* lam, double* out) {
+  fac_gx_b<8>(P, w, lam, out);
 }
 
 }  // namespace rapdb

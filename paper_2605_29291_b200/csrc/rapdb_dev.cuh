@@ -64,6 +64,11 @@ struct SolverState {
   double tau, tau_start, slack, sigma, alpha_n, beta_n, phi_new, theta;
   long long call_done;     // accepted iterations in the current rapdb_run call
   int step, ret, kret, xkind, evals, rsrc, rwarm, pad2;
+  // factored, host-assisted: request for the host to run the high-occupancy
+  // factored kernels at this stop: fq[0] = 0 none, 1 sweep (fq[1] = parity,
+  // fq[2] = x source: 0 w.x[par], 1 rc.in_x), 2 gradient(s) (fq[1] = count,
+  // then per request: parity, multiplier id, output id; factored.cuh)
+  int fq[8];
   double step_ns[64];      // device time per state-machine step (CTA 0, globaltimer); 60..62: sweep sub-phases
   long long step_cnt[64];
 };
@@ -160,6 +165,7 @@ struct RunCfg {
   int metrics_every, criterion, has_f_star, fixed_period, fixed_point, warm_tau, stop_at_fixed;
   int op, src, reset_inner, reps;
   int split;               // exit at exchange points (sharded runs) instead of continuing
+  int fac_host;            // factored: sweeps / gradients run as host-launched kernels (stops)
   int resume;              // continue the saved op at st.step
 
   double eps, eps_kkt, eps_feas, f_star;

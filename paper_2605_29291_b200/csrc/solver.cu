@@ -231,6 +231,11 @@ __device__ void drive(const KArgs& K, Sm& S) {
     }
     if (threadIdx.x == 0) st.step = next;
     __syncthreads();
+    if (st.fq[0] != 0) {   // host-assisted factored work (and maybe an exchange) at this stop
+      if (threadIdx.x == 0) { st.xkind = K.rc.split ? xk : X_NONE; st.status = ST_EXCHANGE; }
+      __syncthreads();
+      return;
+    }
     if (xk != X_NONE) {
       if (K.rc.split) {   // the host all-reduces the buffer and relaunches
         if (threadIdx.x == 0) { st.xkind = xk; st.status = ST_EXCHANGE; }
@@ -297,6 +302,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
   S.pseq = 0;
   if (threadIdx.x == 0) {
     s_st = *K.w.st;
+    s_st.fq[0] = 0;   // the host served the previous stop's request
     for (int s = 0; s < K.sp.nstages; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.empty[s], 1);   // each ring slot is consumed by exactly one warp
@@ -356,6 +362,7 @@ struct rapdb_ctx {
   long long sweep_bytes = 0;  // algorithmic bytes of one sweep (the roofline numerator)
   long long nchw = 0;       // factored: 1024-row chunks of W over all blocks
   int split = 0;            // sharded: stop at exchange points
+  int fac_host = 0;         // factored: sweeps / gradients as host-launched high-occupancy kernels
   rapdb_exchange_fn xcb = nullptr;
   void* xuser = nullptr;
   long long exchanges = 0;
@@ -461,6 +468,36 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   return RAPDB_OK;
 }
 
+// A factored stop: run the requested sweep / gradient(s) as standalone
+// kernels (8 CTAs per SM) on the context's stream, then the op resumes.
+int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
+  const DevProblem& P = c->P;
+  const Work& w = c->w;
+  const int grid = c->nsm * 8;
+  const long long n = P.n, np = (long long)P.p + P.m;
+  if (st.fq[0] == 1) {
+    const int par = st.fq[1];
+    const double* x = st.fq[2] ? rc.in_x : w.x + (long long)par * n;
+    fac_sweep_a_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, x, par);
+    fac_sweep_b_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, par);
+    g_launches += 2;
+  } else if (st.fq[0] == 2) {
+    for (int k = 0; k < st.fq[1] && k < 2; ++k) {
+      const int par = st.fq[2 + 3 * k], lid = st.fq[3 + 3 * k], oid = st.fq[4 + 3 * k];
+      const double* lam = lid == 0 ? w.ytr + P.p : lid == 1 ? w.y + P.p : lid == 2 ? w.y + np + P.p : rc.in_lam;
+      double* out = oid == 0 ? w.gxs : w.gxb + (long long)st.ig_new * n;
+      const double* Wpar = w.W + (long long)par * P.nr;
+      fac_gx_a_kernel<<<grid, kThreads, (size_t)std::max(P.fnb, 1) * 8, c->stream>>>(P, w, Wpar, lam, out);
+      fac_gx_b_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, lam, out);
+      g_launches += 2;
+    }
+  } else {
+    return fail(c, RAPDB_EDEVICE, "unknown factored request");
+  }
+  CK(cudaGetLastError());
+  return RAPDB_OK;
+}
+
 // Launch an op.  Single-rank contexts run it to completion in one launch
 // (asynchronous).  Sharded contexts ("split") stop at every exchange point:
 // the registered callback all-reduces the buffer rapdb_exchange_buffers names
@@ -470,16 +507,23 @@ int launch(rapdb_ctx* c, RunCfg rc) {
   if (c->P.kind == 1 && c->prm.ball != 0)
     return fail(c, RAPDB_ECONFIG, "factored instances support the unbounded dual set only");
   rc.split = c->split;
+  rc.fac_host = c->fac_host;
   rc.resume = 0;
   int r = launch_once(c, rc);
-  if (r || !c->split) return r;
+  if (r || (!c->split && !c->fac_host)) return r;
   for (;;) {
     r = read_state(c, &c->last_st);
     if (r) return r;
     if (c->last_st.status != ST_EXCHANGE) return RAPDB_OK;
-    if (!c->xcb) return fail(c, RAPDB_ECONFIG, "sharded context has no exchange callback");
-    if (c->xcb(c->xuser, c->last_st.xkind) != 0) return fail(c, RAPDB_EDEVICE, "exchange callback failed");
-    ++c->exchanges;
+    if (c->last_st.fq[0] != 0) {
+      r = serve_factored(c, rc, c->last_st);
+      if (r) return r;
+    }
+    if (c->split && c->last_st.xkind != X_NONE) {
+      if (!c->xcb) return fail(c, RAPDB_ECONFIG, "sharded context has no exchange callback");
+      if (c->xcb(c->xuser, c->last_st.xkind) != 0) return fail(c, RAPDB_EDEVICE, "exchange callback failed");
+      ++c->exchanges;
+    }
     rc.resume = 1;
     r = launch_once(c, rc);
     if (r) return r;
@@ -846,6 +890,7 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   c->P = P;
   c->sp = sp;
   c->sweep_bytes = R * (long long)n * 8;
+  c->fac_host = 0;
   if (layout == 1) {
     // the unit table rides in its own allocation (8-byte entries)
     if (c->d_units) cudaFree(c->d_units);
@@ -951,6 +996,8 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   c->P = P;
   c->sp = sp;
   c->nchw = nchw;
+  const char* env_fh = std::getenv("RAPDB_FAC_HOST");
+  c->fac_host = (env_fh && env_fh[0] == '0') ? 0 : 1;
   // one factored sweep: R (12 B/nnz + row pointers) streamed, W written and
   // re-read, C and A (+ b) read, x gathered once
   c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * fnb * n + 12 * nnz_a + 16LL * Lloc + 8 + 8LL * n;

@@ -26,7 +26,16 @@ __device__ __forceinline__ bool sweep_sync(const KArgs& K, Sm& S, const double* 
   unsigned long long t0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer();
   bool ok;
-  if (K.P.kind == 1) {
+  if (K.P.kind == 1 && K.rc.fac_host) {   // the host runs the sweep kernels at the next stop
+    if (threadIdx.x == 0) {
+      SolverState& st = *S.st;
+      st.fq[0] = 1;
+      st.fq[1] = par;
+      st.fq[2] = xsrc == K.rc.in_x ? 1 : 0;
+    }
+    __syncthreads();
+    ok = true;
+  } else if (K.P.kind == 1) {
     ok = sweep_factored(K, S, xsrc, par);
   } else {
     sweep(K, S, xsrc, par);
@@ -71,6 +80,22 @@ __device__ __forceinline__ void g_local(const KArgs& K, int par) {
 __device__ __forceinline__ bool gx_part(const KArgs& K, Sm& S, int par, const double* lam_g, const double* lam_s,
                                         double* out) {
   const DevProblem& P = K.P;
+  if (P.kind == 1 && K.rc.fac_host) {   // queue it for the host (factored.cuh, fac_gx_*)
+    if (threadIdx.x == 0) {
+      SolverState& st = *S.st;
+      const int np = P.p + P.m;
+      const int lid = lam_g == K.w.ytr + P.p ? 0 : lam_g == K.w.y + P.p ? 1 : lam_g == K.w.y + np + P.p ? 2 : 3;
+      const int oid = out == K.w.gxs ? 0 : 1;
+      const int k = st.fq[0] == 2 ? st.fq[1] : 0;
+      st.fq[0] = 2;
+      st.fq[1] = k + 1;
+      st.fq[2 + 3 * k] = par;
+      st.fq[3 + 3 * k] = lid;
+      st.fq[4 + 3 * k] = oid;
+    }
+    __syncthreads();
+    return true;
+  }
   if (P.kind == 1) return recombine_factored(K, S, K.w.W + (long long)par * P.nr, lam_g, out);
   const double* U = K.w.U + (long long)par * P.nloc * P.n;
   if (K.sp.rc_cols) recombine_cols(K, S, U, lam_s, out);
