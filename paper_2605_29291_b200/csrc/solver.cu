@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -388,6 +389,37 @@ int cuda_fail(rapdb_ctx* c, cudaError_t e, const char* where) {
 
 long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+// Small per-context device tables are stream-ordered allocations (no device
+// synchronisation on free: a context is created and destroyed per solve), and
+// the page-locked state readback buffers are pooled across contexts.
+cudaError_t table_alloc(void** p, size_t bytes, cudaStream_t s) { return cudaMallocAsync(p, bytes, s); }
+void table_free(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+std::mutex g_pin_mu;
+std::vector<void*> g_pin_pool;
+
+void* pinned_get(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_pool.empty()) {
+      void* p = g_pin_pool.back();
+      g_pin_pool.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, std::max<size_t>(bytes, 4096)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void pinned_put(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_pool.push_back(p);
+}
+
 constexpr int B_COUNT_MAX = 32;
 
 struct Layout {
@@ -578,7 +610,11 @@ int read_state(rapdb_ctx* c, SolverState* st) {
     const int wr = wait_stream(c);   // poll first: a pageable D2H copy would block behind a hung kernel
     if (wr) return wr;
   }
-  if (!c->h_state) CK(cudaMallocHost(&c->h_state, sizeof(SolverState) + 64));
+  if (!c->h_state) {
+    static_assert(sizeof(SolverState) + 64 <= 4096, "pinned state buffer");
+    c->h_state = static_cast<SolverState*>(pinned_get(sizeof(SolverState) + 64));
+    if (!c->h_state) return fail(c, RAPDB_EDEVICE, "cudaMallocHost failed");
+  }
   int* h_ab = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_state) + sizeof(SolverState));
   CK(cudaMemcpyAsync(c->h_state, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(h_ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -679,10 +715,10 @@ int rapdb_create(int device, int rank, int nranks, rapdb_ctx** out) {
 
 void rapdb_destroy(rapdb_ctx* c) {
   if (!c) return;
-  if (c->d_ints) cudaFree(c->d_ints);
-  if (c->d_ll) cudaFree(c->d_ll);
-  if (c->d_units) cudaFree(c->d_units);
-  if (c->h_state) cudaFreeHost(c->h_state);
+  table_free(c->d_ints, c->stream);
+  table_free(c->d_ll, c->stream);
+  table_free(c->d_units, c->stream);
+  pinned_put(c->h_state);
   delete c;
 }
 
@@ -877,10 +913,11 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   };
   const size_t o_act = put(act), o_zl = put(zl), o_lo = put(seg_lo), o_hi = put(seg_hi),
                o_a0 = put(cta_a0), o_slot = put(slot);
-  if (c->d_ints) cudaFree(c->d_ints);
+  table_free(c->d_ints, c->stream);
   c->d_ints = nullptr;
-  CK(cudaMalloc(&c->d_ints, ints.size() * sizeof(int)));
-  CK(cudaMemcpy(c->d_ints, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(table_alloc(reinterpret_cast<void**>(&c->d_ints), ints.size() * sizeof(int), c->stream));
+  CK(cudaMemcpyAsync(c->d_ints, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   DevProblem P{};
   P.n = n; P.m = m; P.p = p; P.k0 = k0; P.k1 = k1; P.nloc = nloc;
   P.nact = (int)act.size(); P.nzero = (int)zl.size(); P.ld = ld;
@@ -893,12 +930,13 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   c->fac_host = 0;
   if (layout == 1) {
     // the unit table rides in its own allocation (8-byte entries)
-    if (c->d_units) cudaFree(c->d_units);
+    table_free(c->d_units, c->stream);
     c->d_units = nullptr;
     std::vector<sym::Unit> hu(sp.geom.upm);
     sym::fill_units(sp.geom, hu.data());
-    CK(cudaMalloc(&c->d_units, hu.size() * sizeof(sym::Unit)));
-    CK(cudaMemcpy(c->d_units, hu.data(), hu.size() * sizeof(sym::Unit), cudaMemcpyHostToDevice));
+    CK(table_alloc(reinterpret_cast<void**>(&c->d_units), hu.size() * sizeof(sym::Unit), c->stream));
+    CK(cudaMemcpyAsync(c->d_units, hu.data(), hu.size() * sizeof(sym::Unit), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     c->sp.units = c->d_units;
     c->sweep_bytes = (long long)act.size() * sp.geom.spm * sym::kTD * 8;   // packed bytes streamed
   }
@@ -950,14 +988,15 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   }
   ll[fnb] = nr;
   const long long nchw = ll[2 * (fnb + 1) - 1];
-  if (c->d_ll) cudaFree(c->d_ll);
+  table_free(c->d_ll, c->stream);
   c->d_ll = nullptr;
-  CK(cudaMalloc(&c->d_ll, ll.size() * sizeof(long long)));
-  CK(cudaMemcpy(c->d_ll, ll.data(), ll.size() * sizeof(long long), cudaMemcpyHostToDevice));
-  if (c->d_ints) cudaFree(c->d_ints);
+  CK(table_alloc(reinterpret_cast<void**>(&c->d_ll), ll.size() * sizeof(long long), c->stream));
+  CK(cudaMemcpyAsync(c->d_ll, ll.data(), ll.size() * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  table_free(c->d_ints, c->stream);
   c->d_ints = nullptr;
-  CK(cudaMalloc(&c->d_ints, 16));
-  CK(cudaMemset(c->d_ints, 0, 16));
+  CK(table_alloc(reinterpret_cast<void**>(&c->d_ints), 16, c->stream));
+  CK(cudaMemsetAsync(c->d_ints, 0, 16, c->stream));
   long long nnz_r = 0, nnz_a = 0;
   if (nr > 0) CK(cudaMemcpy(&nnz_r, r_ptr + nr, 8, cudaMemcpyDeviceToHost));
   if (Lloc > 0) CK(cudaMemcpy(&nnz_a, a_ptr + Lloc, 8, cudaMemcpyDeviceToHost));

@@ -13,11 +13,13 @@ from paper_2605_29291_b200.engine import ApdbEngine  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 nm = len(sys.argv) > 2 and sys.argv[2] == "nm"
+mode = sys.argv[3] if len(sys.argv) > 3 else "yx"
+pol_name = sys.argv[4] if len(sys.argv) > 4 else "fixed"
 arr = instances.config_instance(name)
 inst = R.ProblemInstance.from_arrays(arr, validate=False)
 crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
-cfg = R.SolverConfig(mode="yx", nonmonotone=nm)
-pol = R.FixedRestart(500)
+cfg = R.SolverConfig(mode=mode, nonmonotone=nm)
+pol = R.FixedRestart(500) if pol_name == "fixed" else R.AdaptiveRestart()
 for k in range(int(os.environ.get("REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
