@@ -181,6 +181,9 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2605_29291_b200 import instances
+    if args.config == "C2":
+        emit({"impl": "reference", "unavailable": "C2's 69 GB dense stack does not fit the CPU reference's host"})
+        return
     arr = instances.config_instance(args.config)
     from oracle import rapdb_oracle as O
     P = O.Problem.from_arrays(arr)
@@ -238,8 +241,15 @@ def main():
     from paper_2605_29291_b200 import _capi, instances
     from paper_2605_29291_b200.sharding import nccl_shard
 
-    arr = instances.config_instance(args.config)
-    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    device_generated = args.config == "C2"
+    if device_generated:
+        # the C2 host instance needs ~69 GB of host RAM and minutes of BLAS:
+        # generate and pack the stack on the device (same distribution)
+        inst = R.DeviceDenseInstance(4096, 512, 256, seed=0, name="C2 (device-generated)")
+        arr = inst
+    else:
+        arr = instances.config_instance(args.config)
+        inst = R.ProblemInstance.from_arrays(arr, validate=False)
     cfg = R.SolverConfig(mode="yx", nonmonotone=False)
     pol = R.FixedRestart(500)
     crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
@@ -315,8 +325,12 @@ def main():
         _, _, probe_ms = ev.ctx.probe_sweep(xprobe, reps=10)
 
     # ---- e2e through the public API with host-resident inputs -----------
-    inst.pin_host()
-    inst.drop_device_data()
+    if device_generated:
+        e2e_block = {"unavailable": "device-generated instance: its inputs never exist on the host"}
+    else:
+        e2e_block = None
+        inst.pin_host()
+        inst.drop_device_data()
     torch.cuda.synchronize()
     nloc = arr.m + 1 if shard is None else shard.k1 - shard.k0
     if layout == "packed" and os.environ.get("RAPDB_PACK_STAGED", "0") != "1":
@@ -328,7 +342,7 @@ def main():
         q_bytes = nloc * arr.n * arr.n * 8
     h2d = q_bytes + inst.q.nbytes + inst.r.nbytes + 2 * arr.n * 8 + inst.A.nbytes + inst.b.nbytes
     e2e_iters, e2e_s, d2h = 0, 0.0, 0
-    for _ in range(args.steps):
+    for _ in range(0 if device_generated else args.steps):
         inst.drop_device_data()
         barrier()
         t0 = time.perf_counter()
@@ -340,7 +354,7 @@ def main():
         d2h = (2 * (arr.n + arr.m + arr.p) * 8 + r.device_stats["run_launches"] * 0
                + r.iterations * 11 * 8 + 8 * 8)
     e2e_s = max_over_ranks(e2e_s)
-    e2e_value = (e2e_iters if sharded else sum_over_ranks(e2e_iters)) / e2e_s
+    e2e_value = (e2e_iters if sharded else sum_over_ranks(e2e_iters)) / e2e_s if e2e_s > 0 else None
 
     # non-monotone variant: fixed 1000-iteration budget (it/s only)
     inst.device_data(dev, krange=krange)
@@ -354,7 +368,7 @@ def main():
     out = None
     if rank == 0:
         cpu = None
-        if not args.skip_cpu and ws == 1:
+        if not args.skip_cpu and ws == 1 and not device_generated:
             v_cpu, dt_cpu, _ = oracle_sample(arr, args.cpu_sample_iters)
             cpu = {"value": v_cpu, "unit": UNIT, "cores": blas_threads(), "kind": "port",
                    "sample": f"{args.cpu_sample_iters} accepted mono-yx iterations of C1 after the first "
@@ -372,7 +386,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded CounterRng, BASELINE config 1 shapes; random instance, no dataset)",
+            "data": ("synthetic (device-generated, BASELINE config 2 shapes and distribution)" if device_generated
+                     else f"synthetic (seeded CounterRng, BASELINE {args.config} shapes; random instance, no dataset)"),
             "config": config_block(arr, args.config, "yx monotone + FixedRestart(500) (rapdb-yx)",
                                    {"parallelism": (f"constraint-sharded over {ws} GPU(s), NCCL all-reduce per trial"
                                                     if sharded else ("replicas only" if ws > 1 else "single GPU")),
@@ -395,8 +410,8 @@ def main():
                          "standalone_sweep_gbs": None if probe_ms is None else sweep_bytes / (probe_ms / 1e3) / 1e9,
                          "frac_of_8tbs": achieved / 8000.0},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "time_to_kkt_ms": 1e3 * e2e_s / args.steps},
+            "e2e": e2e_block or {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                                 "d2h_bytes_per_step": int(d2h), "time_to_kkt_ms": 1e3 * e2e_s / args.steps},
             "nonmonotone": {"iters_per_s": rnm.iterations / tn, "iterations": rnm.iterations,
                             "evals": rnm.evals, "budget": 1000, "final_kkt": rnm.metrics.kkt_residual},
             "gpu_launches": int(launches),

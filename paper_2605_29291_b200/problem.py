@@ -333,6 +333,7 @@ class DeviceDenseInstance:
         self.mu = 0.0
         self.dual_set = None
         self.name = name or f"device-dense n={n} m={m} r={rank}"
+        self.meta = {"rank": int(rank), "seed": int(seed), "generator": "torch CUDA normal + fp64 DGEMM"}
         self.primal_set = Box(np.full(n, -box), np.full(n, box))
         self.cone = NonnegOrthant(m)
         self._dev = {}
