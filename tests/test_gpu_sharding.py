@@ -98,3 +98,44 @@ def test_emulated_shards_adaptive_gap():
     for res in cluster.run(inst, body):
         np.testing.assert_array_equal(trace_arr(res.trace)[:200, TAU], g["yx_nm_ada/trace"][:200, TAU])
         assert [e.iteration for e in res.restart_log][:len(meaningful)] == meaningful
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_emulated_shards_kml_zero_objective_and_equality(nranks):
+    """C4's structure (all-zero Q_0 never streamed, one equality row, a free
+    epigraph variable) sharded: the zero matrix lands on rank 0's range."""
+    g = load_golden("kml_small")
+    arr = instances.kml_epigraph(N=120, d=10)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    cluster = EmulatedCluster(nranks)
+
+    def body(shard):
+        return R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(500),
+                               budget=3000, criteria=crit(1e-6), shard=shard)
+
+    for res in cluster.run(inst, body):
+        tr = trace_arr(res.trace)
+        np.testing.assert_array_equal(tr[:200, TAU], g["nm_fixed500/trace"][:200, TAU])
+        assert res.iterations == int(g["nm_fixed500/iterations"])
+
+
+def test_emulated_shards_factored_xy():
+    """xy mode (two gradient exchanges per trial) on a sharded factored instance."""
+    from conftest import FACTORED_SMALL
+    from paper_2605_29291_b200.factored import FactoredInstance
+    arr = instances.factored_qcqp(**FACTORED_SMALL)
+    inst = FactoredInstance.from_arrays(arr)
+    cfg = R.SolverConfig(mode="xy", nonmonotone=True)
+    ref = R.ApdbEngine(inst, cfg, R.initial_iterate(inst))
+    ref.run_block(60)
+    cluster = EmulatedCluster(2)
+
+    def body(shard):
+        eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst), shard=shard)
+        eng.run_block(60)
+        return trace_arr(eng.trace), eng.last
+
+    for tr, z in cluster.run(inst, body):
+        np.testing.assert_array_equal(tr[:, 5], trace_arr(ref.trace)[:, 5])
+        np.testing.assert_allclose(tr[:, 1:5], trace_arr(ref.trace)[:, 1:5], rtol=1e-12)
+        assert rel(z.x, ref.last.x) <= 1e-11
