@@ -1,7 +1,9 @@
 // solver_kernel.cuh -- the persistent, cooperative rAPDB kernel (sm_100a, fp64).
 //
-// One CTA per SM (288 threads: 8 consumer warps + 1 TMA-bulk producer warp,
-// ~200 KB of shared memory for the Q-tile ring).  A launch executes one "op":
+// One CTA per SM (256 threads: 7 consumer warps + 1 TMA-bulk producer warp --
+// two warps per SM sub-partition, so the register cap is 255 and the sweeps do
+// not spill; ~210 KB of shared memory for the Q-tile ring).  A launch executes
+// one "op":
 //   OP_RUN    accepted iterations with device-side backtracking, KKT cadence,
 //             termination and fixed restarts  (engine.py:198-259 inside
 //             restarts.py:111-161);
@@ -9,7 +11,9 @@
 //             (engine.py:102-136);
 //   OP_KKT    kkt_residual at the current iterate (diagnostics.py:96-113);
 //   OP_GET    engine.last / engine.average() (engine.py:262-272);
-//   OP_PROBE  one (or reps) fused Q sweeps at a given x, for KATs and timing.
+//   OP_PROBE  one (or reps) fused Q sweeps at a given x, for KATs and timing;
+//   OP_GAP    the smoothed duality gap (gap.cuh); OP_GRAD grad_x Phi at a point;
+//   OP_EGM    extragradient iterations (egm.cuh).
 //
 // Phases inside an op are separated by a software grid barrier (the launch is
 // cooperative, so all CTAs are co-resident).  Every cross-CTA sum is a
@@ -729,7 +733,7 @@ __device__ __forceinline__ double recombine_local(const KArgs& K, const double* 
 }
 
 // recombine_local for every column, for many matrices: each CTA takes 32-column
-// blocks, its 9 warps take contiguous chunks of the local matrices, and warp 0
+// blocks, its 8 warps take contiguous chunks of the local matrices, and warp 0
 // adds the chunk partials in warp order (fixed order -> deterministic).  The
 // per-thread variant above leaves all but n threads idle and is latency-bound
 // for m in the hundreds (C1: 24 us -> ~4 us per trial).

@@ -16,7 +16,9 @@
 // all-reduces (sums) the named buffer and relaunches the kernel, which resumes
 // at the next step (all loop state lives in SolverState).  With one rank the
 // partial already is the total and the kernel just continues (a grid barrier
-// where the consumer mapping differs).  Single-GPU runs never leave the kernel.
+// where the consumer mapping differs).  Single-GPU dense runs never leave the
+// kernel; factored runs also stop at each sweep / gradient so the host can run
+// them as high-occupancy kernels (SolverState::fq, factored.cuh).
 #pragma once
 #include "factored.cuh"
 
