@@ -191,3 +191,27 @@ def test_nearly_symmetric_input_uses_upper_triangle(monkeypatch):
     asym = np.abs(arr.Q - np.transpose(arr.Q, (0, 2, 1))) @ np.abs(x)
     assert np.all(np.abs(us["rows"] - us["packed"]) <= asym + 1e-13 * (1 + np.max(np.abs(us["rows"]))))
     assert np.max(asym) <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,p", [(1, 1, 0), (33, 2, 0), (65, 3, 1), (130, 4, 2), (257, 1, 0)])
+def test_packed_solver_ragged_vs_oracle(n, m, p, monkeypatch):
+    """Whole solves on ragged n (edge units with one sub-row / column, padded
+    sub-tiles) with equality rows: accepted steps identical to the oracle."""
+    from oracle import rapdb_oracle as O
+    monkeypatch.setenv("RAPDB_LAYOUT", "packed")
+    arr = instances.dense_qcqp(n, m, max(1, min(6, n)), seed=11 + n)
+    if p:
+        rng = np.random.default_rng(n)
+        arr.A = rng.standard_normal((p, n))
+        arr.b = arr.A @ rng.uniform(-0.1, 0.1, n)
+        arr.p = p
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    P = O.Problem.from_arrays(arr)
+    for nm in (False, True):
+        ref = O.run_restarted(P, O.Options(mode="yx", nonmonotone=nm), O.Policy("fixed", period=40), budget=100)
+        res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=nm), R.FixedRestart(40), budget=100)
+        a = np.array([[t.tau_start, t.tau, t.evals_iter] for t in res.trace])
+        b = np.array([[t.tau_start, t.tau, t.evals_iter] for t in ref.trace])
+        np.testing.assert_array_equal(a, b)
+        assert np.linalg.norm(res.solution.x - ref.x) <= 1e-9 * (1 + np.linalg.norm(ref.x))
