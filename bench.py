@@ -397,7 +397,12 @@ def main():
                                     "final_kkt": results[-1].metrics.kkt_residual}),
             "time_to_kkt_ms": t_ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per sweep (dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                         "OP_PROBE sweep launch, ncu --set full, profiles/ncu_summary.json); "
+                                         "achieved counts the same sweep bytes over the solve launch",
+                         "traffic_over_algorithmic": (traffic / sweep_bytes) if traffic else None,
+                         "peak_source": peak_src,
                          "kernel": "rapdb_solver_kernel (whole launch: sweeps + all other phases)",
                          "layout": layout,
                          "bytes_per_launch_def": ("sweeps x packed-symmetric stack bytes "
