@@ -55,6 +55,8 @@ def parse():
                     help="with N>1: independent replicas instead of constraint sharding")
     ap.add_argument("--shard", action="store_true",
                     help="force the constraint-sharded (NCCL exchange) path even with one rank")
+    ap.add_argument("--p2p", action="store_true",
+                    help="sharded runs exchange in-kernel over NVLink peer memory instead of NCCL")
     ap.add_argument("--cpu-sample-iters", type=int, default=24,
                     help="accepted C1 iterations per CPU sample (~0.25 s each on 16 cores)")
     ap.add_argument("--skip-cpu", action="store_true")
@@ -257,6 +259,7 @@ def main():
     if sharded:
         shard = nccl_shard(inst)
         shard.force_split = True
+        shard.p2p = bool(args.p2p)
     krange = None if shard is None else (shard.k0, shard.k1)
 
     def solve(c=cfg, budget=50_000, criteria=crit):

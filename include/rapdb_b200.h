@@ -100,6 +100,25 @@ int rapdb_exchange_buffers(rapdb_ctx* ctx, int kind, double** buf0, long long* c
 /* number of exchanges performed by this context so far */
 long long rapdb_exchange_count(const rapdb_ctx* ctx);
 
+/* In-kernel exchange over NVLink peer memory (dense shards; opt-in): each
+ * rank allocates a zeroed device region of rapdb_peer_region_bytes(ctx)
+ * bytes (rapdb_region_alloc), shares it with the other ranks (CUDA IPC handles:
+ * rapdb_ipc_handle / rapdb_ipc_open / rapdb_ipc_close), and passes the R
+ * device pointers (regions[rank] = its own) to rapdb_set_peer_exchange.  The
+ * per-trial gradient / g exchanges then run inside the persistent kernel:
+ * push the partial into slot `rank` of every peer, release-signal every peer,
+ * acquire all R signals, sum the R slots in rank order -- no host round trip.
+ * The smoothed gap's H still goes through the exchange callback.          */
+long long rapdb_peer_region_bytes(rapdb_ctx* ctx);
+/* a zeroed device allocation of its own (an IPC handle names a whole
+ * allocation, so the region must not live inside a pooled block)           */
+int rapdb_region_alloc(long long bytes, void** dptr);
+int rapdb_region_free(void* dptr);
+int rapdb_ipc_handle(const void* dptr, unsigned char* handle64);
+int rapdb_ipc_open(const unsigned char* handle64, void** dptr);
+int rapdb_ipc_close(void* dptr);
+int rapdb_set_peer_exchange(rapdb_ctx* ctx, void* const* regions);
+
 /* cumulative device time (ns, CTA 0 globaltimer) and call counts per step of
  * the op state machine (step ids: rapdb_dev.cuh enum Step), for profiling */
 int rapdb_step_profile(rapdb_ctx* ctx, double* ns, long long* counts, int nsteps);

@@ -48,7 +48,9 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_smoothed_gap", "rapdb_launch_count", "rapdb_set_exchange", "rapdb_exchange_buffers",
            "rapdb_exchange_count", "rapdb_step_profile", "rapdb_bind_factored", "rapdb_grad_x",
            "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric",
-           "rapdb_bind_factored_range", "rapdb_egm"]
+           "rapdb_bind_factored_range", "rapdb_egm", "rapdb_peer_region_bytes", "rapdb_ipc_handle",
+           "rapdb_ipc_open", "rapdb_ipc_close", "rapdb_set_peer_exchange", "rapdb_region_alloc",
+           "rapdb_region_free"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
@@ -79,6 +81,41 @@ def pack_symmetric(n: int, count: int, src_ptr: int, ld: int, mat_stride: int, d
                                        C.c_void_p(dst_ptr), C.c_void_p(stream_ptr))
     if code != 0:
         raise DeviceError(f"rapdb_pack_symmetric failed (code {code})")
+
+
+def ipc_handle(dptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    if load().rapdb_ipc_handle(C.c_void_p(int(dptr)), buf) != 0:
+        raise DeviceError("cudaIpcGetMemHandle failed")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = C.c_void_p()
+    if load().rapdb_ipc_open(handle, C.byref(out)) != 0:
+        raise DeviceError("cudaIpcOpenMemHandle failed")
+    return int(out.value)
+
+
+def ipc_close(dptr: int) -> None:
+    load().rapdb_ipc_close(C.c_void_p(int(dptr)))
+
+
+class PeerRegion:
+    """A zeroed cudaMalloc'd region (freed with the object)."""
+
+    def __init__(self, nbytes: int):
+        out = C.c_void_p()
+        if load().rapdb_region_alloc(int(nbytes), C.byref(out)) != 0:
+            raise DeviceError("peer region allocation failed")
+        self.ptr = int(out.value)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                load().rapdb_region_free(C.c_void_p(self.ptr))
+        except Exception:   # interpreter shutdown
+            pass
 
 
 def load(path: str = LIB_PATH):
@@ -122,6 +159,14 @@ def load(path: str = LIB_PATH):
     lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 19 + [D]
     lib.rapdb_bind_factored_range.argtypes = [P, I, I, I, I, I, I, I, LL] + [P] * 19 + [D]
     lib.rapdb_egm.argtypes = [P, D, LL, I, P, C.POINTER(LL), C.POINTER(I)]
+    lib.rapdb_peer_region_bytes.argtypes = [P]
+    lib.rapdb_peer_region_bytes.restype = LL
+    lib.rapdb_ipc_handle.argtypes = [P, C.c_char_p]
+    lib.rapdb_ipc_open.argtypes = [C.c_char_p, C.POINTER(P)]
+    lib.rapdb_ipc_close.argtypes = [P]
+    lib.rapdb_region_alloc.argtypes = [LL, C.POINTER(P)]
+    lib.rapdb_region_free.argtypes = [P]
+    lib.rapdb_set_peer_exchange.argtypes = [P, C.POINTER(P)]
     lib.rapdb_grad_x.argtypes = [P, P, P, P, P, P]
     _lib = lib
     return lib
@@ -207,6 +252,14 @@ class Context:
                 off = b.value - base
                 out.append(self.ws[off:off + 8 * cnt.value].view(self.torch.float64))
         return out
+
+    def peer_region_bytes(self) -> int:
+        return int(self.lib.rapdb_peer_region_bytes(self.h))
+
+    def set_peer_exchange(self, regions):
+        """regions: R device pointers (ints), this rank's own at index rank."""
+        arr = (C.c_void_p * len(regions))(*[C.c_void_p(int(r)) for r in regions])
+        self._check(self.lib.rapdb_set_peer_exchange(self.h, arr))
 
     def exchange_count(self):
         return int(self.lib.rapdb_exchange_count(self.h))

@@ -63,6 +63,7 @@ struct SolverState {
   // resumable control (the kernel may exit at an exchange point and resume)
   double tau, tau_start, slack, sigma, alpha_n, beta_n, phi_new, theta;
   long long call_done;     // accepted iterations in the current rapdb_run call
+  unsigned long long xgen; // in-kernel peer exchanges done by this context (generation counter)
   int step, ret, kret, xkind, evals, rsrc, rwarm, pad2;
   // factored, host-assisted: request for the host to run the high-occupancy
   // factored kernels at this stop: fq[0] = 0 none, 1 sweep (fq[1] = parity,
@@ -166,6 +167,7 @@ struct RunCfg {
   int op, src, reset_inner, reps;
   int split;               // exit at exchange points (sharded runs) instead of continuing
   int fac_host;            // factored: sweeps / gradients run as host-launched kernels (stops)
+  int p2p;                 // sharded dense: exchanges in-kernel over peer memory (PeerX)
   int resume;              // continue the saved op at st.step
 
   double eps, eps_kkt, eps_feas, f_star;
@@ -178,12 +180,25 @@ struct RunCfg {
   double* out_x; double* out_v; double* out_lam; double* out_u; double* out_g;
 };
 
+// In-kernel constraint-shard exchange over NVLink peer memory: every rank
+// owns a region [2 sets][R slots][S doubles] + [R flags]; rank r pushes its
+// partial into slot r of set (gen & 1) of every peer, signals flag r of every
+// peer with the generation, waits for all R flags of its own region, and sums
+// its R slots in rank order -- the same bits on every rank.
+struct PeerX {
+  double* const* slots;            // [R] base of each rank's region (device pointers, peers mapped)
+  unsigned long long* const* flags; // [R] each rank's flag array (R x 16 words apart)
+  long long S;                     // doubles per slot
+  int rank, R;
+};
+
 struct KArgs {
   DevProblem P;
   DevParams prm;
   SweepPlan sp;
   Work w;
   RunCfg rc;
+  PeerX px;
 };
 
 // ---------------------------------------------------------------- primitives

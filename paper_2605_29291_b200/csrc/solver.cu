@@ -237,6 +237,14 @@ __device__ void drive(const KArgs& K, Sm& S) {
       __syncthreads();
       return;
     }
+    if (xk != X_NONE && K.rc.p2p && xk != X_H) {   // in-kernel exchange over NVLink peer memory
+      if (!peer_exchange(K, S, xk)) {
+        if (threadIdx.x == 0) { st.status = ST_ABORT; st.step = DONE; }
+        __syncthreads();
+        return;
+      }
+      continue;
+    }
     if (xk != X_NONE) {
       if (K.rc.split) {   // the host all-reduces the buffer and relaunches
         if (threadIdx.x == 0) { st.xkind = xk; st.status = ST_EXCHANGE; }
@@ -364,6 +372,9 @@ struct rapdb_ctx {
   long long nchw = 0;       // factored: 1024-row chunks of W over all blocks
   int split = 0;            // sharded: stop at exchange points
   int fac_host = 0;         // factored: sweeps / gradients as host-launched high-occupancy kernels
+  int p2p = 0;              // sharded dense: in-kernel exchanges over peer memory
+  PeerX px{};
+  void* d_px = nullptr;     // device tables of the peer region pointers
   rapdb_exchange_fn xcb = nullptr;
   void* xuser = nullptr;
   long long exchanges = 0;
@@ -490,6 +501,7 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   K.sp = c->sp;
   K.w = c->w;
   K.rc = rc;
+  K.px = c->px;
   CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
   CK(cudaMemsetAsync(c->w.abort_flag, 0, 128, c->stream));
   void* args[] = {&K};
@@ -540,6 +552,7 @@ int launch(rapdb_ctx* c, RunCfg rc) {
     return fail(c, RAPDB_ECONFIG, "factored instances support the unbounded dual set only");
   rc.split = c->split;
   rc.fac_host = c->fac_host;
+  rc.p2p = c->p2p;
   rc.resume = 0;
   int r = launch_once(c, rc);
   if (r || (!c->split && !c->fac_host)) return r;
@@ -674,6 +687,77 @@ int rapdb_exchange_buffers(rapdb_ctx* c, int kind, double** b0, long long* n0, d
 
 long long rapdb_exchange_count(const rapdb_ctx* c) { return c ? c->exchanges : -1; }
 
+// ---- in-kernel peer exchange (sharded dense contexts) ---------------------
+namespace {
+long long peer_slot_doubles(const rapdb_ctx* c) { return 2LL * c->P.n + c->P.m + 1; }
+}
+
+long long rapdb_peer_region_bytes(rapdb_ctx* c) {
+  if (!c || !c->bound || c->P.kind != 0) return -1;
+  const long long R = c->nranks, S = peer_slot_doubles(c);
+  return 2 * R * S * 8 + R * 16 * 8;
+}
+
+int rapdb_region_alloc(long long bytes, void** out) {
+  if (bytes <= 0 || !out) return RAPDB_EINPUT;
+  if (cudaMalloc(out, (size_t)bytes) != cudaSuccess) return RAPDB_EDEVICE;
+  if (cudaMemset(*out, 0, (size_t)bytes) != cudaSuccess) return RAPDB_EDEVICE;
+  return cudaDeviceSynchronize() == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+int rapdb_region_free(void* p) {
+  if (!p) return RAPDB_EINPUT;
+  return cudaFree(p) == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+int rapdb_ipc_handle(const void* dptr, unsigned char* out) {
+  if (!dptr || !out) return RAPDB_EINPUT;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)) != cudaSuccess) return RAPDB_EDEVICE;
+  static_assert(sizeof(h) <= 64, "ipc handle");
+  std::memcpy(out, &h, sizeof(h));
+  return RAPDB_OK;
+}
+
+int rapdb_ipc_open(const unsigned char* handle, void** out) {
+  if (!handle || !out) return RAPDB_EINPUT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+int rapdb_ipc_close(void* p) {
+  if (!p) return RAPDB_EINPUT;
+  return cudaIpcCloseMemHandle(p) == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+int rapdb_set_peer_exchange(rapdb_ctx* c, void* const* regions) {
+  if (!c || !regions) return RAPDB_EINPUT;
+  if (!c->bound || c->P.kind != 0) return fail(c, RAPDB_ECONFIG, "peer exchange needs a bound dense context");
+  const int R = c->nranks;
+  const long long S = peer_slot_doubles(c);
+  std::vector<void*> tab(2 * (size_t)R);
+  for (int r = 0; r < R; ++r) {
+    if (!regions[r] || (reinterpret_cast<uintptr_t>(regions[r]) & 127)) return fail(c, RAPDB_EINPUT, "bad peer region");
+    tab[r] = regions[r];
+    tab[R + r] = static_cast<char*>(regions[r]) + 2 * R * S * 8;
+  }
+  table_free(c->d_px, c->stream);
+  c->d_px = nullptr;
+  CK(table_alloc(&c->d_px, tab.size() * sizeof(void*), c->stream));
+  CK(cudaMemcpyAsync(c->d_px, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  PeerX px{};
+  px.slots = reinterpret_cast<double* const*>(c->d_px);
+  px.flags = reinterpret_cast<unsigned long long* const*>(static_cast<void**>(c->d_px) + R);
+  px.S = S;
+  px.rank = c->rank;
+  px.R = R;
+  c->px = px;
+  c->p2p = 1;
+  return RAPDB_OK;
+}
+
 int rapdb_step_profile(rapdb_ctx* c, double* ns, long long* counts, int nsteps) {
   if (!c || !ns || !counts || !c->have_ws) return RAPDB_EINPUT;
   SolverState st;
@@ -718,6 +802,7 @@ void rapdb_destroy(rapdb_ctx* c) {
   table_free(c->d_ints, c->stream);
   table_free(c->d_ll, c->stream);
   table_free(c->d_units, c->stream);
+  table_free(c->d_px, c->stream);
   pinned_put(c->h_state);
   delete c;
 }

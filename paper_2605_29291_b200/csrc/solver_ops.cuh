@@ -53,6 +53,70 @@ __device__ __forceinline__ bool sweep_sync(const KArgs& K, Sm& S, const double* 
 
 constexpr int kAbort = -1;
 
+// ---------------------------------------------------------------- peer exchange
+// The in-kernel replacement of the host all-reduce at an exchange point
+// (sharded dense runs with peer regions attached, KArgs::px): push this
+// rank's partial into slot `rank` of every peer over NVLink, fence, signal
+// every peer's flag `rank` with the generation, wait for all R flags of the
+// own region, then sum the R slots in rank order (identical bits on every
+// rank).  Double-buffered by generation parity: a rank can be at most one
+// exchange ahead of any peer (it cannot finish exchange k+1 before every peer
+// has signalled k+1, i.e. finished reading exchange k).
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ bool peer_exchange(const KArgs& K, Sm& S, int xk) {
+  const PeerX& px = K.px;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const long long n = K.P.n, m = K.P.m;
+  double* b0 = w.gxs;
+  long long n0 = n;
+  double* b1 = nullptr;
+  long long n1 = 0;
+  if (xk == X_G) { b0 = w.gval + (long long)(st.cur ^ 1) * (m + 1); n0 = m + 1; }
+  else if (xk == X_GX2) { b1 = w.gxb + (long long)st.ig_new * n; n1 = n; }
+  const long long tot = n0 + n1;
+  if (!gsync(K, S)) return false;                 // the partial is complete on this rank
+  if (threadIdx.x == 0) st.xgen += 1;
+  __syncthreads();
+  const unsigned long long gen = st.xgen;
+  const long long set = (long long)(gen & 1ull) * px.R * px.S;
+  for (long long j = gtid(); j < tot; j += gstride()) {
+    const double v = j < n0 ? ldcg(b0 + j) : ldcg(b1 + (j - n0));
+    for (int r = 0; r < px.R; ++r) px.slots[r][set + (long long)px.rank * px.S + j] = v;
+  }
+  __threadfence_system();
+  if (!gsync(K, S)) return false;                 // every CTA's pushes are fenced
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int r = 0; r < px.R; ++r) st_release_sys(px.flags[r] + (long long)px.rank * 16, gen);
+  if (threadIdx.x == 0) {                         // wait for every peer's push of this generation
+    const long long t0 = clock64();
+    for (int r = 0; r < px.R; ++r) {
+      while (ld_acquire_sys(px.flags[px.rank] + (long long)r * 16) < gen) {
+        if (*(volatile int*)K.w.abort_flag) { S.flag[0] = 1; break; }
+        if (clock64() - t0 > 60000000000ll) { atomicExch(K.w.abort_flag, 5); S.flag[0] = 1; break; }
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (S.flag[0]) return false;
+  const double* mine = px.slots[px.rank] + set;
+  for (long long j = gtid(); j < tot; j += gstride()) {
+    double s = ldcg(mine + j);
+    for (int r = 1; r < px.R; ++r) s += ldcg(mine + (long long)r * px.S + j);
+    if (j < n0) b0[j] = s; else b1[j - n0] = s;
+  }
+  return gsync(K, S);                             // consumers read the sums next
+}
+
 __device__ __forceinline__ BallScale ball_from_slots(const KArgs& K, Sm& S, int sv, int sl) {
   if (!K.prm.ball) return BallScale{1.0, 1.0, 0, 0};
   const int s2[2] = {sv, sl};

@@ -126,6 +126,8 @@ class ApdbEngine:
             else:
                 self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1))
             ctx.bind(self._data, cfg, shard.k0, shard.k1)
+            if getattr(shard, "p2p", False) and not getattr(self._data, "factored", False):
+                shard.attach_peer_exchange(ctx)
         self._trace_buf = None
         self._res = None
         self.iters = 0

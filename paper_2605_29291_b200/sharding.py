@@ -36,6 +36,38 @@ class Shard:
     name: str = ""
     l0: Optional[int] = None      # factored instances: linear rows [l0, l1) of this rank
     l1: Optional[int] = None
+    p2p: bool = False             # dense: exchange in-kernel over NVLink peer memory (opt-in)
+    group: object = None          # torch.distributed group for the peer-region handshake
+    _peer: object = None          # [(region, opened peer pointers)] kept alive by the shard
+
+    def attach_peer_exchange(self, ctx):
+        """Allocate this rank's zeroed exchange region, swap CUDA IPC handles
+        with the other ranks (torch.distributed object all-gather) and hand the
+        R pointers to the context (rapdb_set_peer_exchange)."""
+        from . import _capi
+        region = _capi.PeerRegion(ctx.peer_region_bytes())
+        if self.nranks == 1:
+            ptrs = [region.ptr]
+            opened = []
+        else:
+            import torch.distributed as dist
+            allh = [None] * self.nranks
+            dist.all_gather_object(allh, _capi.ipc_handle(region.ptr), group=self.group)
+            ptrs, opened = [], []
+            for r, hr in enumerate(allh):
+                if r == self.rank:
+                    ptrs.append(region.ptr)
+                else:
+                    p = _capi.ipc_open(hr)
+                    opened.append(p)
+                    ptrs.append(p)
+            dist.barrier(group=self.group)
+        ctx.set_peer_exchange(ptrs)
+        # every engine gets a fresh region (its flags restart at generation 0);
+        # earlier regions stay mapped so engines created before remain valid
+        if self._peer is None:
+            self._peer = []
+        self._peer.append((region, opened))
 
     @property
     def split(self) -> bool:
@@ -80,7 +112,8 @@ def nccl_shard(inst, group=None) -> Shard:
         for v in views:
             dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
 
-    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl", l0=l0, l1=l1)
+    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl", l0=l0, l1=l1,
+                 group=group)
 
 
 class EmulatedCluster:

@@ -139,3 +139,24 @@ def test_emulated_shards_factored_xy():
         np.testing.assert_array_equal(tr[:, 5], trace_arr(ref.trace)[:, 5])
         np.testing.assert_allclose(tr[:, 1:5], trace_arr(ref.trace)[:, 1:5], rtol=1e-12)
         assert rel(z.x, ref.last.x) <= 1e-11
+
+
+@pytest.mark.parametrize("mode,policy", [("yx", "fixed"), ("xy", "fixed"), ("yx", "adaptive")])
+def test_peer_exchange_single_rank_is_bitwise_identical(mode, policy):
+    """The in-kernel NVLink exchange path (push to every peer's slot, release
+    / acquire generation flags, rank-ordered sum) with one rank: it must leave
+    every result bit-identical to the fused run (the sum of one slot).  The
+    smoothed gap's H still goes through the host callback (adaptive case)."""
+    arr = instances.dense_qcqp(150, 9, 12, seed=4)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    pol = R.FixedRestart(40) if policy == "fixed" else R.AdaptiveRestart(warmup=30, check_period=60)
+    fused = _solve(inst, None, mode, True, pol, 300, 1e-9)
+    calls = []
+    shard = Shard(rank=0, nranks=1, k0=0, k1=arr.m + 1, force_split=True, p2p=True,
+                  exchange=lambda views: calls.append(len(views)))
+    peer = _solve(inst, shard, mode, True, pol, 300, 1e-9)
+    if policy == "fixed":
+        assert not calls, "gradient / g exchanges must not leave the kernel"
+    np.testing.assert_array_equal(trace_arr(peer.trace)[:, :7], trace_arr(fused.trace)[:, :7])
+    np.testing.assert_array_equal(peer.solution.x, fused.solution.x)
+    np.testing.assert_array_equal(peer.solution.lam, fused.solution.lam)

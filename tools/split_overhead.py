@@ -36,7 +36,8 @@ def nccl(views):
 
 for label, shard in [("fused", None),
                      ("split-noop", Shard(0, 1, 0, arr.m + 1, exchange=noop, force_split=True)),
-                     ("split-nccl", Shard(0, 1, 0, arr.m + 1, exchange=nccl, force_split=True))]:
+                     ("split-nccl", Shard(0, 1, 0, arr.m + 1, exchange=nccl, force_split=True)),
+                     ("peer-p2p", Shard(0, 1, 0, arr.m + 1, exchange=nccl, force_split=True, p2p=True))]:
     for rep in range(2):
         calls[0] = 0
         torch.cuda.synchronize()
