@@ -32,6 +32,50 @@ __device__ double hval(long long a, long long r, long long c) {
   return (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5 + (r == c ? 2.0 : 0.0);
 }
 
+
+// Experiment only (nocomp == 3): consume_unit that skips the R writes of odd
+// block columns and the C writes of odd block rows -- the partial-write volume
+// and transpose count a 2x2 "super-unit" scheme would have (results wrong).
+__device__ __forceinline__ void consume_unit_halfw(const Geom& g, const double* __restrict__ tile,
+                                                   const double* __restrict__ xs, int bi, int bj,
+                                                   double* __restrict__ Pa, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  int rs, cs;
+  unit_subtiles(g, bi, bj, rs, cs);
+  const double* xr = xs + bi * kB;
+  const double* xc = xs + bj * kB;
+  const long long nbB = g.nbB;
+  if (bi == bj) { consume_unit(g, tile, xs, bi, bj, Pa, pol); return; }
+  double c[2] = {0.0, 0.0};
+  double* outR = Pa + ((long long)bi * nbB + bj) * kB;
+  for (int sr = 0; sr < rs; ++sr) {
+    double v[32];
+#pragma unroll
+    for (int r = 0; r < kT; ++r) v[r] = 0.0;
+    for (int sc = 0; sc < cs; ++sc) {
+      const double* T = tile + (sr * cs + sc) * kTD;
+      const double xj = xc[sc * kT + lane];
+      const double* xi = xr + sr * kT;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < kT; r += 2) {
+        const double2 xx = *reinterpret_cast<const double2*>(xi + r);
+        const double q0 = T[r * kT + lane], q1 = T[(r + 1) * kT + lane];
+        v[r] = fma(q0, xj, v[r]);
+        v[r + 1] = fma(q1, xj, v[r + 1]);
+        c0 = fma(q0, xx.x, c0);
+        c1 = fma(q1, xx.y, c1);
+      }
+      c[sc] = c[sc] + (c0 + c1);
+    }
+    if (!(bj & 1)) st_keep(outR + sr * kT + lane, transpose_reduce(v), pol);
+    else if (v[0] == 12345.678) outR[0] = v[1];
+  }
+  double* outC = Pa + ((long long)bj * nbB + bi) * kB;
+  if (!(bi & 1)) for (int sc = 0; sc < cs; ++sc) st_keep(outC + sc * kT + lane, c[sc], pol);
+  else if (c[0] == 12345.678) outC[0] = c[1];
+}
+
 __global__ void gen_dense(double* D, int n, long long nmat) {
   const long long tot = nmat * n * (long long)n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
@@ -132,7 +176,9 @@ __global__ void __launch_bounds__(288, 1) phase_a(Geom g, const Unit* __restrict
       const Unit un = units[u];
       // nocomp 1: no compute (pure stream); 2: compute, partials of every
       // matrix into matrix 0's slots (L2-resident: no DRAM write traffic)
-      if (nocomp != 1) consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
+      if (nocomp == 3) consume_unit_halfw(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs,
+                                          un.bi, un.bj, Pt + a * pstride, keep);
+      else if (nocomp != 1) consume_unit(g, reinterpret_cast<const double*>(ring + (long long)s * slot_bytes), xs, un.bi, un.bj,
                    Pt + (nocomp == 2 ? 0 : a) * pstride, keep);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
