@@ -933,6 +933,12 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
     sp.chunk = (int)ld;
     sp.stage_bytes = 4LL * sym::kTD * 8;
     sp.xs_bytes = align_up((long long)sp.geom.nbB * sym::kB * 8, 128);
+    // x does not fit next to a 2-slot ring (n > ~19 500), or forced: every
+    // consumer warp loads its unit's two 64-entry x blocks instead
+    const long long budget0 = (long long)c->optin - 16384 - 2048;
+    const char* env_xg = std::getenv("RAPDB_XGLOBAL");
+    sp.xglobal = (env_xg && env_xg[0] == '1') || sp.xs_bytes + 2 * sp.stage_bytes + 256 > budget0;
+    if (sp.xglobal) sp.xs_bytes = align_up((long long)kConsumerWarps * 128 * 8, 128);
     const char* env_pf = std::getenv("RAPDB_L2PF");
     // L2 prefetch of the next sweep's first units: measured neutral at 8 and
     // harmful beyond (C1 1598 -> 1460 it/s at 64 units), so off by default

@@ -151,7 +151,7 @@ __device__ __forceinline__ double rowdot(const double* row, const double* xs, lo
 // barrier per tile, so the ring keeps nstages*stage_bytes of HBM reads in
 // flight per SM; chunk partials of a row are summed in chunk order.
 // equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
-__device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par) {
+__device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par, const double* xg = nullptr) {
   const DevProblem& P = K.P;
   const int n = P.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -161,14 +161,16 @@ __device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par) {
     // 4 independent chains per lane (8 loads in flight), combined in fixed order
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int j = lane;
+    // x from shared memory, or from global memory when it is too long (xg)
+    auto xv = [&](int jj) { return xg ? ldcg(xg + jj) : S.xs[jj]; };
     for (; j + 96 < n; j += 128) {
       const double a0 = __ldg(vec + j), a1 = __ldg(vec + j + 32), a2 = __ldg(vec + j + 64), a3 = __ldg(vec + j + 96);
-      s0 = fma(a0, S.xs[j], s0);
-      s1 = fma(a1, S.xs[j + 32], s1);
-      s2 = fma(a2, S.xs[j + 64], s2);
-      s3 = fma(a3, S.xs[j + 96], s3);
+      s0 = fma(a0, xv(j), s0);
+      s1 = fma(a1, xv(j + 32), s1);
+      s2 = fma(a2, xv(j + 64), s2);
+      s3 = fma(a3, xv(j + 96), s3);
     }
-    for (; j < n; j += 32) s0 = fma(__ldg(vec + j), S.xs[j], s0);
+    for (; j < n; j += 32) s0 = fma(__ldg(vec + j), xv(j), s0);
     double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
       if (it < P.p) K.w.eqv[(long long)par * P.p + it] = s - __ldg(P.b + it);
@@ -201,8 +203,9 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   const int xlen = g.nbB * sym::kB;
   unsigned long long tsub = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) tsub = globaltimer();
-  // stage x (zero padded): all of a thread's loads in flight at once
-  for (int j0 = threadIdx.x; j0 < xlen; j0 += 8 * kThreads) {
+  // stage x (zero padded): all of a thread's loads in flight at once; with a
+  // very long x (sp.xglobal) each consumer warp loads its unit's two x blocks
+  for (int j0 = threadIdx.x; j0 < (sp.xglobal ? 0 : xlen); j0 += 8 * kThreads) {
     double v[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -272,8 +275,21 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     for (long long k = warp; k < mine; k += ncw) {
       if (!mbar_wait(&fullb[s], use & 1, abort_flag)) break;
       const sym::Unit un = units[u];
-      sym::consume_unit(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xs,
-                        un.bi, un.bj, Pt + a * pstride, keep);
+      if (sp.xglobal) {   // this unit's x blocks into the warp's 128-entry buffer
+        double* xw = S.xs + warp * 128;
+        const int r0 = un.bi * sym::kB, c0 = un.bj * sym::kB;
+        xw[lane] = r0 + lane < n ? ldcg(xsrc + r0 + lane) : 0.0;
+        xw[32 + lane] = r0 + 32 + lane < n ? ldcg(xsrc + r0 + 32 + lane) : 0.0;
+        xw[64 + lane] = c0 + lane < n ? ldcg(xsrc + c0 + lane) : 0.0;
+        xw[96 + lane] = c0 + 32 + lane < n ? ldcg(xsrc + c0 + 32 + lane) : 0.0;
+        __syncwarp();
+        sym::consume_unit_x(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xw, xw + 64,
+                            un.bi, un.bj, Pt + a * pstride, keep);
+        __syncwarp();
+      } else {
+        sym::consume_unit(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xs,
+                          un.bi, un.bj, Pt + a * pstride, keep);
+      }
       // generic-proxy reads of the slot before the producer's next bulk write
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -336,14 +352,16 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     const int r = B * sym::kB + 2 * lane;
     double xu = 0.0, qx = 0.0;
     if (r < n) {
+      const double x0 = sp.xglobal ? ldcg(xsrc + r) : xs[r];
       U[(long long)lm * n + r] = sx;
-      xu = xs[r] * sx;
-      qx = __ldg(qa + r) * xs[r];
+      xu = x0 * sx;
+      qx = __ldg(qa + r) * x0;
     }
     if (r + 1 < n) {
+      const double x1 = sp.xglobal ? ldcg(xsrc + r + 1) : xs[r + 1];
       U[(long long)lm * n + r + 1] = sy;
-      xu = xu + xs[r + 1] * sy;
-      qx = qx + __ldg(qa + r + 1) * xs[r + 1];
+      xu = xu + x1 * sy;
+      qx = qx + __ldg(qa + r + 1) * x1;
     }
     xu = warp_sum(xu);
     qx = warp_sum(qx);
@@ -352,7 +370,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       K.w.segqx[it] = qx;
     }
   }
-  sweep_tail(K, S, par);
+  sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr);
   // The next sweep streams the same units in the same order and only starts
   // after the trial's control steps (tens of microseconds of latency-bound
   // work during which HBM would idle): prefetch this CTA's first units of it

@@ -157,14 +157,13 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ T, const do
 
 // One unit held in shared memory (tile) -> its slots of Pt.  xs: staged x,
 // zero padded to nbB * 64.  Pa: Pt + a * nbB * nbB * 64 (this matrix).
-__device__ __forceinline__ void consume_unit(const Geom& g, const double* __restrict__ tile,
-                                             const double* __restrict__ xs, int bi, int bj,
-                                             double* __restrict__ Pa, uint64_t pol) {
+// xr / xc: the 64 entries of x at block rows Bi / Bj (shared memory)
+__device__ __forceinline__ void consume_unit_x(const Geom& g, const double* __restrict__ tile,
+                                               const double* __restrict__ xr, const double* __restrict__ xc,
+                                               int bi, int bj, double* __restrict__ Pa, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   int rs, cs;
   unit_subtiles(g, bi, bj, rs, cs);
-  const double* xr = xs + bi * kB;
-  const double* xc = xs + bj * kB;
   const long long nbB = g.nbB;
   if (bi == bj) {
     // (0,0): D00 x0 (C-way, symmetric);  (0,1): row part -> rows 0..31,
@@ -216,6 +215,12 @@ __device__ __forceinline__ void consume_unit(const Geom& g, const double* __rest
   }
   double* outC = Pa + ((long long)bj * nbB + bi) * kB;
   for (int sc = 0; sc < cs; ++sc) st_keep(outC + sc * kT + lane, c[sc], pol);
+}
+
+__device__ __forceinline__ void consume_unit(const Geom& g, const double* __restrict__ tile,
+                                             const double* __restrict__ xs, int bi, int bj,
+                                             double* __restrict__ Pa, uint64_t pol) {
+  consume_unit_x(g, tile, xs + bi * kB, xs + bj * kB, bi, bj, Pa, pol);
 }
 
 // ---- half-unit streaming: a unit's sub-rows travel as separate ring slots

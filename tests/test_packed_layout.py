@@ -215,3 +215,40 @@ def test_packed_solver_ragged_vs_oracle(n, m, p, monkeypatch):
         b = np.array([[t.tau_start, t.tau, t.evals_iter] for t in ref.trace])
         np.testing.assert_array_equal(a, b)
         assert np.linalg.norm(res.solution.x - ref.x) <= 1e-9 * (1 + np.linalg.norm(ref.x))
+
+
+@pytest.mark.gpu
+def test_xglobal_mode_is_bitwise_identical(monkeypatch):
+    """Long-x fallback (each consumer warp loads its unit's two x blocks
+    instead of staging all of x in shared memory), forced at a small n: the
+    same arithmetic on the same values -> bit-identical solves."""
+    arr = instances.dense_qcqp(333, 6, 9, seed=12)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RAPDB_XGLOBAL", flag)
+        inst = R.ProblemInstance.from_arrays(arr, validate=False)
+        out[flag] = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(50),
+                                    budget=150)
+    a, b = out["0"], out["1"]
+    np.testing.assert_array_equal(np.array([[t.tau, t.evals_iter] for t in a.trace]),
+                                  np.array([[t.tau, t.evals_iter] for t in b.trace]))
+    np.testing.assert_array_equal(a.solution.x, b.solution.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_long_x_instance_vs_oracle():
+    """n = 20 500 (x no longer fits in shared memory next to the ring: the
+    automatic long-x path), first 4 iterations against the oracle."""
+    from oracle import rapdb_oracle as O
+    arr = instances.dense_qcqp(20_500, 1, 3, seed=2)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    P = O.Problem.from_arrays(arr)
+    eng = O.Engine(P, O.Options(mode="yx", nonmonotone=False), *O.initial_point(P))
+    for _ in range(4):
+        eng.step()
+    dev = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=False), R.initial_iterate(inst))
+    dev.run_block(4)
+    np.testing.assert_array_equal(np.array([[t.tau_start, t.tau, t.evals_iter] for t in dev.trace]),
+                                  np.array([[t.tau_start, t.tau, t.evals_iter] for t in eng.trace]))
+    assert np.linalg.norm(dev.last.x - eng.x) <= 1e-9 * (1 + np.linalg.norm(eng.x))
