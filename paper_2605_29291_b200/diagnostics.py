@@ -88,6 +88,15 @@ def infeasibility(inst: ProblemInstance, x) -> float:
     return kkt_residual(inst, Iterate(x, np.zeros(inst.p), np.zeros(inst.m))).infeas
 
 
+def mean_positive_violation(inst: ProblemInstance, x) -> float:
+    """diagnostics.py:57-66 for the orthant cone: (1/m) sum_i max(g_i(x), 0),
+    with g evaluated by a device sweep."""
+    if inst.m == 0:
+        return 0.0
+    g = np.asarray(inst.g_value(x), dtype=float)
+    return float(np.mean(np.maximum(g, 0.0)))
+
+
 def check_termination(metrics: Metrics, criteria: TerminationCriteria) -> bool:
     """diagnostics.py:252-263 (the same predicate the kernel evaluates)."""
     if criteria.criterion == "paper51":

@@ -285,6 +285,33 @@ def _upload_packed(src, n, device, pinned):
     return Qp
 
 
+@dataclass
+class LipschitzConstants:
+    """Same fields as the reference's (problem.py:93-106).  The constants are
+    only used for the reference's analysis and stepsize heuristics outside the
+    hot path (out of scope); compute_constants raises."""
+
+    L_f: float
+    L_g: float
+    B_g: float
+    C_g: float
+    L_xx: float
+    L_xy: float
+    Lhat_xx: float
+    Lhat_yx: float
+    dual_bound_used: float
+    psi1: float
+    psi2: float
+    B_g_is_estimate: bool = False
+
+
+def compute_constants(*args, **kwargs):
+    """problem.py:226-317 of the reference (Lipschitz constants and dual
+    bounds for the analysis): not part of the device hot path."""
+    raise ConfigurationError("compute_constants (problem.py:226-317) is outside the B200 hot path; "
+                             "use the reference package for the analysis constants")
+
+
 def _check_point(inst: ProblemInstance, z: Iterate):
     if z.x.shape != (inst.n,) or z.v.shape != (inst.p,) or z.lam.shape != (inst.m,):
         raise InputError(

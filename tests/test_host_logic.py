@@ -88,3 +88,24 @@ def test_factored_shard_ranges_cover_and_balance():
     from paper_2605_29291_b200.errors import ConfigurationError
     with pytest.raises(ConfigurationError):
         inst.shard_ranges(arr.mq + 2)
+
+
+def test_public_names_match_the_reference():
+    """Every name rapdb/__init__.py:4-21 exports is importable from the
+    drop-in (compute_constants fails loudly: it is outside the hot path)."""
+    import paper_2605_29291_b200 as R
+    ref = ["ApdbEngine", "SolverConfig", "TraceRecord", "initial_iterate", "run",
+           "ConfigurationError", "DataError", "InputError", "NonConvergence", "SlaterViolation",
+           "Iterate", "LipschitzConstants", "ProblemInstance", "compute_constants",
+           "coupling_value", "grad_x_coupling", "grad_y_coupling",
+           "AdaptiveRestart", "FixedRestart", "NoRestart", "RunResult", "run_restarted"]
+    for name in ref:
+        assert hasattr(R, name), name
+        assert name in R.__all__, name
+    import pytest
+    with pytest.raises(R.ConfigurationError):
+        R.compute_constants(None, None)
+    from paper_2605_29291_b200 import diagnostics
+    for name in ("kkt_residual", "infeasibility", "mean_positive_violation", "smoothed_gap",
+                 "check_termination", "Metrics", "TerminationCriteria"):
+        assert hasattr(diagnostics, name), name
