@@ -115,6 +115,37 @@ class SplitBall:
                 and np.linalg.norm(lam) <= self.radius_lam + tol)
 
 
+class _OutOfScope:
+    """Sets and cones of the reference that no BASELINE config uses (SURVEY.md
+    section 8: out of scope).  They import, so drop-in code keeps loading, and
+    constructing one fails loudly."""
+
+    kind = ""
+
+    def __init__(self, *args, **kwargs):
+        raise ConfigurationError(f"{self.kind} (reference geometry.py) is not built on the device path")
+
+
+class Ball(_OutOfScope):
+    kind = "Ball primal set"
+
+
+class Simplex(_OutOfScope):
+    kind = "Simplex primal set"
+
+
+class NonnegWithLinearEq(_OutOfScope):
+    kind = "NonnegWithLinearEq primal set"
+
+
+class SecondOrderCone(_OutOfScope):
+    kind = "SecondOrderCone"
+
+
+class ProductCone(_OutOfScope):
+    kind = "ProductCone"
+
+
 SimpleSet = Box
 Cone = NonnegOrthant
 DualBall = Union[Unbounded, JointBall, SplitBall]
@@ -152,6 +183,22 @@ def bregman_p(x, xbar):
 
 
 bregman_d = bregman_p
+
+
+def bregman(x, xbar):
+    """geometry.py:357-361 (Euclidean generator)."""
+    return bregman_p(x, xbar)
+
+
+def project_dual_ball(d, y):
+    """geometry.py:317-320: y = (v, lam) through the dual ball."""
+    return d.project(*y) if isinstance(y, tuple) else d.project(y[0], y[1])
+
+
+def validate_dual_ball(cone, ball):
+    """geometry.py:331-335: balls are fine for the orthant (no SOC here)."""
+    cone_dim(cone)
+    return ball
 
 
 def ball_code(ball):
