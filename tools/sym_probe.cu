@@ -12,6 +12,99 @@
 
 using namespace rapdb::sym;
 
+namespace rapdb {
+namespace sym {
+// ---- half-unit streaming: a unit's sub-rows travel as separate ring slots
+// (sub-row 0: sub-tiles (0,0),(0,1); sub-row 1: the rest), so a slot is held
+// only while one sub-row is computed.  Same arithmetic, same order, same Pt
+// slots as consume_unit.
+
+// sub-tiles and doubles offset (inside the unit) of half h
+__device__ __forceinline__ void unit_half(bool diag, int rs, int cs, int h, int& first, int& count) {
+  if (diag) {
+    if (h == 0) { first = 0; count = rs == 2 ? 2 : 1; }
+    else { first = 2; count = 1; }
+  } else {
+    first = h * cs;
+    count = cs;
+  }
+}
+
+struct HalfState {           // per-warp registers carried between the halves of a unit
+  double c0, c1, o1;
+};
+
+// half h of unit (bi, bj) held in shared memory at `tile` (its first stored
+// sub-tile); writes the row part(s) it completes and, at the last half, the
+// column part / diagonal block
+__device__ __forceinline__ void consume_half(const Geom& g, const double* __restrict__ tile,
+                                             const double* __restrict__ xs, int bi, int bj, int h,
+                                             double* __restrict__ Pa, uint64_t pol, HalfState& hs) {
+  const int lane = threadIdx.x & 31;
+  int rs, cs;
+  unit_subtiles(g, bi, bj, rs, cs);
+  const double* xr = xs + bi * kB;
+  const double* xc = xs + bj * kB;
+  const long long nbB = g.nbB;
+  if (bi == bj) {
+    double* out = Pa + ((long long)bi * nbB + bi) * kB;
+    if (h == 0) {
+      double o0 = col_dot(tile, xr);
+      hs.o1 = 0.0;
+      if (rs == 2) {
+        const double* T01 = tile + kTD;
+        const double xj = xc[kT + lane];
+        double v[32];
+        double c = 0.0;
+#pragma unroll
+        for (int r = 0; r < kT; ++r) {
+          const double q = T01[r * kT + lane];
+          v[r] = q * xj;
+          c = fma(q, xr[r], c);
+        }
+        o0 = o0 + transpose_reduce(v);
+        hs.o1 = c;
+      }
+      st_keep(out + lane, o0, pol);
+      if (rs == 1) st_keep(out + kT + lane, 0.0, pol);
+    } else {
+      st_keep(out + kT + lane, hs.o1 + col_dot(tile, xr + kT), pol);
+    }
+    return;
+  }
+  if (h == 0) { hs.c0 = 0.0; hs.c1 = 0.0; }
+  const int sr = h;
+  double v[32];
+#pragma unroll
+  for (int r = 0; r < kT; ++r) v[r] = 0.0;
+  for (int sc = 0; sc < cs; ++sc) {
+    const double* T = tile + sc * kTD;
+    const double xj = xc[sc * kT + lane];
+    const double* xi = xr + sr * kT;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < kT; r += 2) {
+      const double2 xx = *reinterpret_cast<const double2*>(xi + r);
+      const double q0 = T[r * kT + lane], q1 = T[(r + 1) * kT + lane];
+      v[r] = fma(q0, xj, v[r]);
+      v[r + 1] = fma(q1, xj, v[r + 1]);
+      c0 = fma(q0, xx.x, c0);
+      c1 = fma(q1, xx.y, c1);
+    }
+    if (sc == 0) hs.c0 = hs.c0 + (c0 + c1); else hs.c1 = hs.c1 + (c0 + c1);
+  }
+  double* outR = Pa + ((long long)bi * nbB + bj) * kB;
+  st_keep(outR + sr * kT + lane, transpose_reduce(v), pol);
+  if (h == rs - 1) {
+    double* outC = Pa + ((long long)bj * nbB + bi) * kB;
+    st_keep(outC + lane, hs.c0, pol);
+    if (cs == 2) st_keep(outC + kT + lane, hs.c1, pol);
+  }
+}
+
+}  // namespace sym
+}  // namespace rapdb
+
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
