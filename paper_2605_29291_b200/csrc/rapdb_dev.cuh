@@ -142,7 +142,7 @@ struct SweepPlan {
   int layout;            // 0 row-major stack [nloc][n][ld], 1 packed symmetric (symsweep.cuh)
   int pad4;
   sym::Geom geom;        // layout 1: unit geometry of one matrix
-  int l2pf;              // layout 1: units per CTA prefetched into L2 for the next sweep
+  int pad5;
   int xglobal;           // layout 1: x too long for shared memory -- per-warp 128-entry x blocks
   const sym::Unit* units;  // layout 1: [upm] unit table (device)
 };

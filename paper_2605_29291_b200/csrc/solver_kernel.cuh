@@ -371,25 +371,6 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     }
   }
   sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr);
-  // The next sweep streams the same units in the same order and only starts
-  // after the trial's control steps (tens of microseconds of latency-bound
-  // work during which HBM would idle): prefetch this CTA's first units of it
-  // into L2 now (fire-and-forget bulk prefetches, no shared memory involved).
-  if (warp == kConsumerWarps && lane == 0 && sp.l2pf > 0) {
-    long long a = b / upm;
-    int u = (int)(b - a * upm);
-    const long long lim = min(mine, (long long)sp.l2pf);
-    for (long long k = 0; k < lim; ++k) {
-      const sym::Unit un = units[u];
-      int rs, cs;
-      const unsigned bytes = (unsigned)sym::unit_subtiles(gg, un.bi, un.bj, rs, cs) * sym::kTD * 8u;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                   :: "l"(Qst + (long long)__ldg(act + a) * mat_doubles + (long long)un.off * sym::kTD), "r"(bytes)
-                   : "memory");
-      u += G;
-      while (u >= upm) { u -= upm; ++a; }
-    }
-  }
   __syncthreads();
   sub_time(S, 62, tsub);
 }
