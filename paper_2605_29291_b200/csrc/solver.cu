@@ -939,10 +939,6 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
     const char* env_xg = std::getenv("RAPDB_XGLOBAL");
     sp.xglobal = (env_xg && env_xg[0] == '1') || sp.xs_bytes + 2 * sp.stage_bytes + 256 > budget0;
     if (sp.xglobal) sp.xs_bytes = align_up((long long)kConsumerWarps * 128 * 8, 128);
-    const char* env_pf = std::getenv("RAPDB_L2PF");
-    // L2 prefetch of the next sweep's first units: measured neutral at 8 and
-    // harmful beyond (C1 1598 -> 1460 it/s at 64 units), so off by default
-    sp.l2pf = env_pf ? std::max(0, std::atoi(env_pf)) : 0;
   }
   const char* env_rc = std::getenv("RAPDB_RC_COLS");
   sp.rc_cols = env_rc ? std::atoi(env_rc) : (k1 - k0 >= 24 ? 1 : 0);
