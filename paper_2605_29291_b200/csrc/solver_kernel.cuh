@@ -151,18 +151,38 @@ __device__ __forceinline__ double rowdot(const double* row, const double* xs, lo
 // barrier per tile, so the ring keeps nstages*stage_bytes of HBM reads in
 // flight per SM; chunk partials of a row are summed in chunk order.
 // equality rows (A x - b) and q.x of skipped all-zero matrices: one warp each
-__device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par, const double* xg = nullptr) {
+// Items are dealt round-robin starting at it0 with stride istride (a warp id
+// in the grid); the default is every warp of every CTA.
+__device__ __forceinline__ void sweep_tail(const KArgs& K, Sm& S, int par, const double* xg = nullptr,
+                                           long long it0 = -1, long long istride = 0) {
   const DevProblem& P = K.P;
   const int n = P.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long items = (long long)P.p + P.nzero;
-  for (long long it = (long long)blockIdx.x * kWarps + warp; it < items; it += (long long)gridDim.x * kWarps) {
+  if (it0 < 0) {
+    it0 = (long long)blockIdx.x * kWarps + warp;
+    istride = (long long)gridDim.x * kWarps;
+  }
+  for (long long it = it0; it < items; it += istride) {
     const double* vec = it < P.p ? P.A + it * n : P.q + (long long)(P.k0 + __ldg(P.zero_list + (it - P.p))) * n;
     // 4 independent chains per lane (8 loads in flight), combined in fixed order
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int j = lane;
     // x from shared memory, or from global memory when it is too long (xg)
     auto xv = [&](int jj) { return xg ? ldcg(xg + jj) : S.xs[jj]; };
+    // four 128-strides' loads in flight at once, the same chains and order
+    for (; j + 480 < n; j += 512) {
+      double a[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) a[t] = __ldg(vec + j + 32 * t);
+#pragma unroll
+      for (int t = 0; t < 16; t += 4) {
+        s0 = fma(a[t], xv(j + 32 * t), s0);
+        s1 = fma(a[t + 1], xv(j + 32 * t + 32), s1);
+        s2 = fma(a[t + 2], xv(j + 32 * t + 64), s2);
+        s3 = fma(a[t + 3], xv(j + 32 * t + 96), s3);
+      }
+    }
     for (; j + 96 < n; j += 128) {
       const double a0 = __ldg(vec + j), a1 = __ldg(vec + j + 32), a2 = __ldg(vec + j + 64), a3 = __ldg(vec + j + 96);
       s0 = fma(a0, xv(j), s0);
@@ -299,6 +319,10 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       s += ncw;
       while (s >= ns) { s -= ns; ++use; }
     }
+  } else if (warp == ncw) {
+    // a consumer warp without a ring slot: the equality rows and the q.x of
+    // all-zero matrices (independent of the stream) while the stream runs
+    sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr, b, G);
   }
   S.pseq = base + (unsigned)mine;
   if (!gsync(K, S)) return;   // aborted: the caller's barrier reports it
@@ -370,7 +394,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       K.w.segqx[it] = qx;
     }
   }
-  sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr);
+  if (ncw == kConsumerWarps) sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr);
   __syncthreads();
   sub_time(S, 62, tsub);
 }
