@@ -16,7 +16,7 @@ import numpy as np
 from .errors import ConfigurationError, DeviceError, InputError, NonConvergence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_rapdb_b200.so")
+LIB_PATH = os.environ.get("RAPDB_LIB") or os.path.join(_HERE, "_rapdb_b200.so")   # RAPDB_LIB: A/B builds (tools/)
 
 TRACE_COLS = 11
 RUN_LIMIT, RUN_CONVERGED, RUN_BUDGET, RUN_CHECK_DUE, RUN_FIXED_DUE, RUN_NONCONV, RUN_ABORT = range(7)

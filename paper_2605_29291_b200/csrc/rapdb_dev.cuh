@@ -142,7 +142,7 @@ struct SweepPlan {
   int layout;            // 0 row-major stack [nloc][n][ld], 1 packed symmetric (symsweep.cuh)
   int pad4;
   sym::Geom geom;        // layout 1: unit geometry of one matrix
-  int pad5;
+  int nchunk;            // layout 1: matrix chunks reduced during the stream (0: all in phase B)
   int xglobal;           // layout 1: x too long for shared memory -- per-warp 128-entry x blocks
   const sym::Unit* units;  // layout 1: [upm] unit table (device)
 };
@@ -155,6 +155,8 @@ struct Work {
   double *pw2, *pcx;           // factored: chunk partials of |W_i|^2 and c_i . x
   double *wl;                  // factored: [nr] block-weighted W-cache of the recombination
   double *Pt;                  // layout 1: per-unit partial products [nact][nbB][nbB][64]
+  unsigned* ccnt;              // layout 1: [64] consumer warps done with each matrix chunk
+  int* idone;                  // layout 1: [nact*nbB] phase-B items already reduced during the stream
   double* trace;
   SolverState* st;
   unsigned long long* bar;

@@ -440,8 +440,13 @@ struct Layout {
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
-             B_W, B_PW2, B_PCX, B_PT, B_WL, B_COUNT };
+             B_W, B_PW2, B_PCX, B_PT, B_WL, B_EARLY, B_COUNT };
 static_assert(B_COUNT <= B_COUNT_MAX, "Layout::off too small");
+
+// chunk counters + per-item flags of the packed sweep's early reduction
+long long early_bytes(const rapdb_ctx* c) {
+  return c->sp.layout == 1 ? 256 + 4LL * std::max(1LL, (long long)c->P.nact * c->sp.geom.nbB) : 256;
+}
 
 Layout layout_of(const rapdb_ctx* c) {
   const long long n = c->P.n, m = c->P.m, p = c->P.p, np = n > 0 ? p + m : 0;
@@ -480,6 +485,7 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_PCX] = fac ? (long long)std::max(c->P.fnb, 1) * c->P.nchx * 8 : 8;
   sz[B_PT] = packed ? std::max(1LL, (long long)c->P.nact) * c->sp.geom.nbB * c->sp.geom.nbB * sym::kB * 8 : 8;
   sz[B_WL] = fac ? std::max(c->P.nr, 1LL) * 8 : 8;
+  sz[B_EARLY] = early_bytes(c);
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -504,6 +510,8 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   K.px = c->px;
   CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
   CK(cudaMemsetAsync(c->w.abort_flag, 0, 128, c->stream));
+  // an aborted launch can leave the early-reduction counters mid-sweep
+  if (c->sp.layout == 1) CK(cudaMemsetAsync(c->w.ccnt, 0, early_bytes(c), c->stream));
   void* args[] = {&K};
   CK(cudaLaunchCooperativeKernel((const void*)rapdb_solver_kernel, dim3(c->G), dim3(kThreads), args,
                                  c->dyn_smem, c->stream));
@@ -952,6 +960,21 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense path (x does not fit in shared memory)");
   sp.nstages = (int)ns;
   sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
+  // packed sweep: the consumer warp without a ring slot reduces the unit
+  // partials of finished matrix chunks while later chunks stream
+  // (RAPDB_EARLY_CHUNKS, 0 = everything after the stream)
+  if (layout == 1 && sp.ncw < kConsumerWarps) {
+    const char* env_ec = std::getenv("RAPDB_EARLY_CHUNKS");
+    // default with enough matrices to spread (C1, C2): chunks of <= ~24 MB of
+    // unit partials, so a chunk's partials are still in L2 when reduced (C2:
+    // 43 chunks, 5.80 -> 5.43 ms per sweep; C1: 8, 0.538 -> 0.509 ms); with
+    // a handful of matrices (C4: 4) the mid-stream fences cost more than phase B
+    const long long pt_bytes = (long long)act.size() * sp.geom.nbB * sp.geom.nbB * sym::kB * 8;
+    const long long by_l2 = (pt_bytes + (24LL << 20) - 1) / (24LL << 20);
+    const int want = env_ec ? std::atoi(env_ec) : (act.size() >= 16 ? (int)std::max(8LL, by_l2) : 0);
+    sp.nchunk = (int)std::max(0LL, std::min<long long>({(long long)want, 64LL, (long long)act.size()}));
+    if (sp.nchunk == 1) sp.nchunk = 0;
+  }
   c->dyn_smem = (size_t)(sp.xs_bytes + ns * sp.stage_bytes + 2 * ns * 8);
   c->stage_cap = ns * sp.stage_bytes / 8;
   // smoothed gap: five shared n-vectors + staged multipliers in xs+ring, and a
@@ -1176,6 +1199,8 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.pcx = D(B_PCX);
   w.Pt = D(B_PT);
   w.wl = D(B_WL);
+  w.ccnt = reinterpret_cast<unsigned*>(base + L.off[B_EARLY]);
+  w.idone = reinterpret_cast<int*>(base + L.off[B_EARLY] + 256);
   w.trace = nullptr;
   w.st = reinterpret_cast<SolverState*>(base + L.off[B_ST]);
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);

@@ -210,6 +210,94 @@ __device__ __forceinline__ void sub_time(Sm& S, int slot, unsigned long long& t)
   }
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef RAPDB_EARLY_POLL_NS
+#define RAPDB_EARLY_POLL_NS 1000
+#endif
+constexpr unsigned kEarlyPollNs = RAPDB_EARLY_POLL_NS;
+
+// streamed matrix a's chunk for the early reduction (monotone in a)
+__device__ __forceinline__ int chunk_of(long long a, int nch, int nact) { return (int)(a * nch / nact); }
+
+// One phase-B item (streamed matrix a, 64-row block B), by one warp:
+// u = sum_K Pt[a][B][K] in K order into the U-cache row segment, the block's
+// x.u and q.x sums, and the item's partial lines dropped from L2.  The same
+// bits whichever warp runs it (during the stream or after it).
+__device__ __forceinline__ void reduce_item(const KArgs& K, const double* xs, const double* xsrc, double* U,
+                                            long long it) {
+  const DevProblem& P = K.P;
+  const int n = P.n;
+  const int lane = threadIdx.x & 31;
+  const int nbB = K.sp.geom.nbB;
+  const bool xglobal = K.sp.xglobal;
+  const int a = (int)(it / nbB);
+  const int B = (int)(it - (long long)a * nbB);
+  const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
+  double sx = 0.0, sy = 0.0;
+  int kk = 0;
+  for (; kk + 32 <= nbB; kk += 32) {   // 32 x 512 B in flight per warp
+    double2 t[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) { sx += t[q].x; sy += t[q].y; }
+  }
+  for (; kk + 16 <= nbB; kk += 16) {
+    double2 t[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) { sx += t[q].x; sy += t[q].y; }
+  }
+  for (; kk + 4 <= nbB; kk += 4) {
+    const double2 t0 = __ldcg(pp + (kk + 0) * 32), t1 = __ldcg(pp + (kk + 1) * 32);
+    const double2 t2 = __ldcg(pp + (kk + 2) * 32), t3 = __ldcg(pp + (kk + 3) * 32);
+    sx += t0.x; sy += t0.y;
+    sx += t1.x; sy += t1.y;
+    sx += t2.x; sy += t2.y;
+    sx += t3.x; sy += t3.y;
+  }
+  for (; kk < nbB; ++kk) {
+    const double2 t = __ldcg(pp + kk * 32);
+    sx += t.x; sy += t.y;
+  }
+  // the item's partials are dead until the next sweep rewrites them: drop
+  // the L2 lines without writing them back to DRAM
+  __syncwarp();
+  {
+    const char* base = reinterpret_cast<const char*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB);
+    for (int L = lane; L < nbB * 4; L += 32)
+      asm volatile("discard.global.L2 [%0], 128;" :: "l"(base + (long long)L * 128) : "memory");
+  }
+  const int lm = __ldg(P.act + a);
+  const double* qa = P.q + (long long)(P.k0 + lm) * n;
+  const int r = B * sym::kB + 2 * lane;
+  double xu = 0.0, qx = 0.0;
+  if (r < n) {
+    const double x0 = xglobal ? ldcg(xsrc + r) : xs[r];
+    U[(long long)lm * n + r] = sx;
+    xu = x0 * sx;
+    qx = __ldg(qa + r) * x0;
+  }
+  if (r + 1 < n) {
+    const double x1 = xglobal ? ldcg(xsrc + r + 1) : xs[r + 1];
+    U[(long long)lm * n + r + 1] = sy;
+    xu = xu + x1 * sy;
+    qx = qx + __ldg(qa + r + 1) * x1;
+  }
+  xu = warp_sum(xu);
+  qx = warp_sum(qx);
+  if (lane == 0) {
+    K.w.segxu[it] = xu;
+    K.w.segqx[it] = qx;
+  }
+}
+
 // The packed-symmetric sweep (layout 1, symsweep.cuh): stream the upper block
 // triangle of every streamed matrix (round-robin units over the CTAs, TMA
 // bulk copies into the ring, one consumer warp per unit) into the unit
@@ -238,6 +326,7 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       if (j < xlen) S.xs[j] = v[t];
     }
   }
+  if (threadIdx.x == 0) S.flag[2] = 0;   // consumer warps finished with the stream
   // generic-proxy use of the ring (dual staging) before the bulk copies below
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -265,6 +354,8 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   const int* const act = P.act;
   const double* const Qst = P.Q;
   const sym::Geom gg = g;
+  const int nch = sp.nchunk;
+  double* const U = K.w.U + (long long)par * P.nloc * n;
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
@@ -292,7 +383,20 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
     unsigned s = (base + warp) % ns, use = (base + warp) / ns;
     const int adv = ncw * G;
     const uint64_t keep = sym::evict_last_policy();
+    // early reduction: tell the grid once this warp is past a matrix chunk
+    // (its partial stores made visible first)
+    int cch = 0;
+    auto pass_chunk = [&]() {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(K.w.ccnt + cch, 1u);
+      ++cch;
+    };
     for (long long k = warp; k < mine; k += ncw) {
+      if (nch) {
+        const int ch = min(chunk_of(a, nch, P.nact), nch - 1);
+        while (cch < ch) pass_chunk();
+      }
       if (!mbar_wait(&fullb[s], use & 1, abort_flag)) break;
       const sym::Unit un = units[u];
       if (sp.xglobal) {   // this unit's x blocks into the warp's 128-entry buffer
@@ -319,80 +423,50 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
       s += ncw;
       while (s >= ns) { s -= ns; ++use; }
     }
+    while (cch < nch - 1) pass_chunk();   // the last chunk is reduced in phase B: no signal
+    if (lane == 0) atomicAdd(S.flag + 2, 1);
   } else if (warp == ncw) {
     // a consumer warp without a ring slot: the equality rows and the q.x of
-    // all-zero matrices (independent of the stream) while the stream runs
+    // all-zero matrices (independent of the stream), then the phase-B items
+    // of every matrix chunk all consumer warps of the grid are past, until
+    // this CTA's own consumers finish (the last chunk is left to phase B)
     sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr, b, G);
+    if (nch) {
+      const unsigned target = (unsigned)(G * ncw);
+      const long long items = (long long)P.nact * gg.nbB;
+      for (long long it = b; it < items; it += G) {
+        const int ch = chunk_of(it / gg.nbB, nch, P.nact);
+        if (ch >= nch - 1) break;
+        int ok = 0;
+        if (lane == 0) {
+          volatile int* cdone = S.flag + 2;
+          while (true) {
+            if (*cdone >= ncw) break;
+            if (ld_acquire_gpu(K.w.ccnt + ch) >= target) { ok = 1; break; }
+            __nanosleep(kEarlyPollNs);
+          }
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) break;
+        reduce_item(K, xs, xsrc, U, it);
+        if (lane == 0) K.w.idone[it] = 1;
+      }
+    }
   }
   S.pseq = base + (unsigned)mine;
   if (!gsync(K, S)) return;   // aborted: the caller's barrier reports it
   sub_time(S, 61, tsub);
   // phase B: u = sum_K Pt[a][B][K] (K order), U-cache rows, block x.u and q.x
-  const int nbB = g.nbB;
-  const long long items = (long long)P.nact * nbB;
-  double* U = K.w.U + (long long)par * P.nloc * n;
+  // for the items not already reduced during the stream
+  const long long items = (long long)P.nact * g.nbB;
+  if (nch && b == 0 && threadIdx.x < nch) K.w.ccnt[threadIdx.x] = 0u;
   for (long long it = (long long)b * kWarps + warp; it < items; it += (long long)G * kWarps) {
-    const int a = (int)(it / nbB);
-    const int B = (int)(it - (long long)a * nbB);
-    const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
-    double sx = 0.0, sy = 0.0;
-    int kk = 0;
-    for (; kk + 32 <= nbB; kk += 32) {   // 32 x 512 B in flight per warp
-      double2 t[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
-#pragma unroll
-      for (int q = 0; q < 32; ++q) { sx += t[q].x; sy += t[q].y; }
+    if (nch && __ldcg(K.w.idone + it)) {
+      __syncwarp();
+      if (lane == 0) K.w.idone[it] = 0;
+      continue;
     }
-    for (; kk + 16 <= nbB; kk += 16) {
-      double2 t[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) { sx += t[q].x; sy += t[q].y; }
-    }
-    for (; kk + 4 <= nbB; kk += 4) {
-      const double2 t0 = __ldcg(pp + (kk + 0) * 32), t1 = __ldcg(pp + (kk + 1) * 32);
-      const double2 t2 = __ldcg(pp + (kk + 2) * 32), t3 = __ldcg(pp + (kk + 3) * 32);
-      sx += t0.x; sy += t0.y;
-      sx += t1.x; sy += t1.y;
-      sx += t2.x; sy += t2.y;
-      sx += t3.x; sy += t3.y;
-    }
-    for (; kk < nbB; ++kk) {
-      const double2 t = __ldcg(pp + kk * 32);
-      sx += t.x; sy += t.y;
-    }
-    // the item's partials are dead until the next sweep rewrites them: drop
-    // the L2 lines without writing them back to DRAM
-    __syncwarp();
-    {
-      const char* base = reinterpret_cast<const char*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB);
-      for (int L = lane; L < nbB * 4; L += 32)
-        asm volatile("discard.global.L2 [%0], 128;" :: "l"(base + (long long)L * 128) : "memory");
-    }
-    const int lm = __ldg(P.act + a);
-    const double* qa = P.q + (long long)(P.k0 + lm) * n;
-    const int r = B * sym::kB + 2 * lane;
-    double xu = 0.0, qx = 0.0;
-    if (r < n) {
-      const double x0 = sp.xglobal ? ldcg(xsrc + r) : xs[r];
-      U[(long long)lm * n + r] = sx;
-      xu = x0 * sx;
-      qx = __ldg(qa + r) * x0;
-    }
-    if (r + 1 < n) {
-      const double x1 = sp.xglobal ? ldcg(xsrc + r + 1) : xs[r + 1];
-      U[(long long)lm * n + r + 1] = sy;
-      xu = xu + x1 * sy;
-      qx = qx + __ldg(qa + r + 1) * x1;
-    }
-    xu = warp_sum(xu);
-    qx = warp_sum(qx);
-    if (lane == 0) {
-      K.w.segxu[it] = xu;
-      K.w.segqx[it] = qx;
-    }
+    reduce_item(K, xs, xsrc, U, it);
   }
   if (ncw == kConsumerWarps) sweep_tail(K, S, par, sp.xglobal ? xsrc : nullptr);
   __syncthreads();
