@@ -46,26 +46,29 @@ struct Sm {
 
 // ------------------------------------------------------------ grid barrier
 
+// Arrival is one acq_rel atomic (release: the CTA's writes, ordered before it
+// by the CTA barrier; acquire: invalidates L1), the wait an acquire-load spin
+// -- 1.14 us per barrier on 148 CTAs against 1.50 us for fence + atomic +
+// volatile spin + fence (tools/bar_probe.cu).
 __device__ __noinline__ bool gsync(const KArgs& K, Sm& S) {
   __syncthreads();
   if (threadIdx.x == 0) {
     S.gen += gridDim.x;
-    __threadfence();
-    atomicAdd(K.w.bar, 1ULL);
-    volatile unsigned long long* vb = K.w.bar;
+    unsigned long long r;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(r) : "l"(K.w.bar) : "memory");
+    r += 1;
     volatile int* va = K.w.abort_flag;
     const long long t0 = clock64();   // monotonic per SM (see mbar_wait)
     int ab = 0;
-    while (*vb < S.gen) {
+    while (r < S.gen) {
       if (*va) { ab = 1; break; }
       if (clock64() - t0 > 60000000000ll) {   // ~30 s watchdog
         atomicExch(K.w.abort_flag, 1);   // 1: grid-barrier timeout
         ab = 1;
         break;
       }
-      __nanosleep(16);
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(K.w.bar) : "memory");
     }
-    __threadfence();
     S.flag[0] = ab;
   }
   __syncthreads();
