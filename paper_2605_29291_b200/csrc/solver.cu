@@ -285,14 +285,11 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ double s_red[kWarps * 8];
   __shared__ double s_tot[NSLOT + 4];
-  __shared__ double s_part[2][kMaxTR][8];
   __shared__ SolverState s_st;
   __shared__ int s_flag[4];
   __shared__ unsigned s_prog[kConsumerWarps];
   __shared__ unsigned s_tag[32], s_rel[32];
-  __shared__ double s_rc[kWarps][32];
   Sm S;
-  S.rc = s_rc;
   S.prog = s_prog;
   S.tag = s_tag;
   S.rel = s_rel;
@@ -302,9 +299,9 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
   S.full = reinterpret_cast<uint64_t*>(S.ring + (long long)K.sp.nstages * K.sp.stage_bytes);
   S.empty = S.full + K.sp.nstages;
   S.stage = reinterpret_cast<double*>(S.ring);
+  S.rc = reinterpret_cast<double(*)[32]>(S.ring + (long long)K.sp.nstages * K.sp.stage_bytes - kWarps * 32 * 8);
   S.red = s_red;
   S.tot = s_tot;
-  S.part = s_part;
   S.st = &s_st;
   S.flag = s_flag;
   S.gen = 0;
@@ -954,8 +951,8 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   long long static_smem = 16384;
   if (cudaFuncGetAttributes(&fa, (const void*)rapdb_solver_kernel) == cudaSuccess)
     static_smem = (long long)fa.sharedSizeBytes;
-  const long long budget = (long long)c->optin - static_smem - 2048;
-  long long ns = (budget - sp.xs_bytes - 256) / sp.stage_bytes;
+  // dynamic = x staging + ring + 2 mbarriers per slot, within the per-block opt-in
+  long long ns = ((long long)c->optin - static_smem - sp.xs_bytes - 128) / (sp.stage_bytes + 16);
   ns = std::min(ns, layout == 1 ? std::min(max_stages, 8LL) : max_stages);
   if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense path (x does not fit in shared memory)");
   sp.nstages = (int)ns;
@@ -982,7 +979,8 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   c->gap_ok = (5LL * n + m + p + m + 64) * 8 <= sp.xs_bytes + ns * sp.stage_bytes && n <= 16384;
   if (layout == 1)   // per-warp 32 x 33 transpose buffers after the staged multipliers (gap.cuh)
     c->gap_ok = c->gap_ok && align_up((long long)m * 8, 256) + kWarps * 32LL * 33 * 8 <= ns * sp.stage_bytes;
-  if (2LL * (p + m) > c->stage_cap)
+  // the staged duals and the recombination scratch at the ring's end must not meet
+  if (2LL * (p + m) + kWarps * 32 > c->stage_cap)
     return fail(c, RAPDB_ECONFIG, "too many multipliers for the shared-memory dual staging area");
   cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->dyn_smem);

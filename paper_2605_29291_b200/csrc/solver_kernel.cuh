@@ -33,13 +33,13 @@ struct Sm {
   double* stage;           // the ring reused as a dual-vector staging area outside sweeps
   double* red;             // [kWarps*8] block-reduction scratch
   double* tot;             // [NSLOT] grid totals
-  double (*part)[kMaxTR][8];
   SolverState* st;
   int* flag;
   volatile unsigned* prog; // [8] units consumed per consumer warp in the current sweep
   volatile unsigned* tag;  // [32] sequence number of the tile last issued into each slot
   volatile unsigned* rel;  // [32] sequence number of the tile last released from each slot
-  double (*rc)[32];        // [kWarps][32] chunk partials of recombine_cols
+  double (*rc)[32];        // [kWarps][32] chunk partials of recombine_cols (the ring's last
+                           // 2 KB: used outside sweeps only, after the staged duals)
   unsigned long long gen;  // grid-barrier generation (thread 0)
   unsigned pseq;           // pipeline sequence (producer lane / consumers)
 };
