@@ -242,32 +242,15 @@ __device__ __forceinline__ void reduce_item(const KArgs& K, const double* xs, co
   const int B = (int)(it - (long long)a * nbB);
   const double2* pp = reinterpret_cast<const double2*>(K.w.Pt + ((long long)a * nbB + B) * nbB * sym::kB) + lane;
   double sx = 0.0, sy = 0.0;
-  int kk = 0;
-  for (; kk + 32 <= nbB; kk += 32) {   // 32 x 512 B in flight per warp
+  // up to 32 x 512 B in flight per warp: ceil(nbB / 32) dependent rounds
+  // (predicated, so a ragged nbB does not fall into short batches)
+  for (int kk = 0; kk < nbB; kk += 32) {
     double2 t[32];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
+    for (int q = 0; q < 32; ++q) t[q] = kk + q < nbB ? __ldcg(pp + (kk + q) * 32) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < 32; ++q) { sx += t[q].x; sy += t[q].y; }
-  }
-  for (; kk + 16 <= nbB; kk += 16) {
-    double2 t[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) t[q] = __ldcg(pp + (kk + q) * 32);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) { sx += t[q].x; sy += t[q].y; }
-  }
-  for (; kk + 4 <= nbB; kk += 4) {
-    const double2 t0 = __ldcg(pp + (kk + 0) * 32), t1 = __ldcg(pp + (kk + 1) * 32);
-    const double2 t2 = __ldcg(pp + (kk + 2) * 32), t3 = __ldcg(pp + (kk + 3) * 32);
-    sx += t0.x; sy += t0.y;
-    sx += t1.x; sy += t1.y;
-    sx += t2.x; sy += t2.y;
-    sx += t3.x; sy += t3.y;
-  }
-  for (; kk < nbB; ++kk) {
-    const double2 t = __ldcg(pp + kk * 32);
-    sx += t.x; sy += t.y;
+    for (int q = 0; q < 32; ++q)
+      if (kk + q < nbB) { sx += t[q].x; sy += t[q].y; }
   }
   // the item's partials are dead until the next sweep rewrites them: drop
   // the L2 lines without writing them back to DRAM

@@ -252,3 +252,32 @@ def test_long_x_instance_vs_oracle():
     np.testing.assert_array_equal(np.array([[t.tau_start, t.tau, t.evals_iter] for t in dev.trace]),
                                   np.array([[t.tau_start, t.tau, t.evals_iter] for t in eng.trace]))
     assert np.linalg.norm(dev.last.x - eng.x) <= 1e-9 * (1 + np.linalg.norm(eng.x))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m", [(97, 23), (333, 40), (1001, 17)])
+def test_early_reduction_is_bitwise_identical(n, m, monkeypatch):
+    """Unit partials reduced by the slot-less warp during the stream (matrix
+    chunks) or all after it: the same K-order sums whichever warp runs an
+    item, so the sweep outputs and whole solves are bit-identical for any
+    chunk count (ragged n; 2, 3, 7 and 64 chunks; with the long-x path)."""
+    import torch
+    arr = instances.dense_qcqp(n, m, max(1, min(9, n)), seed=21)
+    x = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, n)).cuda()
+    ref = None
+    for chunks, xg in (("0", "0"), ("2", "0"), ("3", "0"), ("7", "0"), ("64", "0"), ("5", "1")):
+        monkeypatch.setenv("RAPDB_EARLY_CHUNKS", chunks)
+        monkeypatch.setenv("RAPDB_XGLOBAL", xg)
+        inst = R.ProblemInstance.from_arrays(arr, validate=False)
+        ev = inst._evaluator()
+        u, g, _ = ev.ctx.probe_sweep(x, reps=4)
+        res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(40), budget=120)
+        got = (u.cpu().numpy(), g.cpu().numpy(), np.array([[t.tau, t.evals_iter] for t in res.trace]),
+               res.solution.x)
+        if ref is None:
+            ref = got
+            uref = np.stack([arr.Q[i] @ x.cpu().numpy() for i in range(m + 1)])
+            assert np.max(np.abs(got[0] - uref)) <= 1e-13 * (1 + np.max(np.abs(uref)))
+            continue
+        for a, b in zip(got, ref):
+            np.testing.assert_array_equal(a, b)
