@@ -527,7 +527,7 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   if (st.fq[0] == 1) {
     const int par = st.fq[1];
     const double* x = st.fq[2] ? rc.in_x : w.x + (long long)par * n;
-    fac_sweep_a_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, x, par);
+    fac_sweep_a_kernel<<<c->nsm * 4, kThreads, 0, c->stream>>>(P, w, x, par);   // 30 KB smem per CTA
     fac_sweep_b_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, par);
     g_launches += 2;
   } else if (st.fq[0] == 2) {

@@ -147,6 +147,91 @@ __global__ void __launch_bounds__(256) spmv_lanes_u(long long rows, const long l
   }
 }
 
+__device__ __forceinline__ double ld_el(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t pol_el() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// V3: the solver's thread-per-row (8-batch + 4 + 1, FMA-free), x gathers
+// either plain L2 (.cg) or with an evict_last policy
+template <bool XEL>
+__global__ void __launch_bounds__(256) spmv_solver(long long rows, const long long* ptr, const int* col,
+                                                  const double* val, const double* x, double* y) {
+  const uint64_t ef = pol_ef();
+  const uint64_t el = pol_el();
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+    long long k = ptr[r];
+    const long long k1 = ptr[r + 1];
+    double s = 0.0;
+    for (; k + 8 <= k1; k += 8) {
+      int c[8]; double v[8], xv[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { c[t] = ld_ef(col + k + t, ef); v[t] = ld_ef(val + k + t, ef); }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) xv[t] = XEL ? ld_el(x + c[t], el) : __ldcg(x + c[t]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) s = __dadd_rn(s, __dmul_rn(v[t], xv[t]));
+    }
+    for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(ld_ef(val + k, ef), XEL ? ld_el(x + ld_ef(col + k, ef), el) : __ldcg(x + ld_ef(col + k, ef))));
+    y[r] = s;
+  }
+}
+
+// V4: warp-cooperative coalesced staging: a warp takes 32 consecutive rows,
+// copies their contiguous (val, col) range into its shared buffer with
+// coalesced loads, then each lane sums its own row in stored order (FMA-free)
+// -- the same bits as thread-per-row.  CAP entries per warp per pass.
+template <int CAP, bool XEL>
+__global__ void __launch_bounds__(256) spmv_warpstage(long long rows, const long long* ptr, const int* col,
+                                                     const double* val, const double* x, double* y) {
+  __shared__ double sv[8][CAP];
+  __shared__ int sc[8][CAP];
+  const uint64_t ef = pol_ef();
+  const uint64_t el = pol_el();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long gw = blockIdx.x * 8LL + w, nw = gridDim.x * 8LL;
+  for (long long r0 = gw * 32; r0 < rows; r0 += nw * 32) {
+    const long long r = r0 + lane;
+    const long long kb = ptr[r0];
+    const long long ke = ptr[min(r0 + 32, rows)];
+    long long k = r < rows ? ptr[r] : ke;
+    const long long k1 = r < rows ? ptr[r + 1] : ke;
+    double s = 0.0;
+    for (long long base = kb; base < ke; base += CAP) {
+      const long long lim = min(base + CAP, ke);
+      for (long long e = base + lane; e < lim; e += 32) {
+        sv[w][e - base] = ld_ef(val + e, ef);
+        sc[w][e - base] = ld_ef(col + e, ef);
+      }
+      __syncwarp();
+      const long long kend = min(k1, lim);
+      for (; k + 4 <= kend; k += 4) {
+        double xv[4], vv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = sc[w][k + t - base];
+          vv[t] = sv[w][k + t - base];
+          xv[t] = XEL ? ld_el(x + c, el) : __ldcg(x + c);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) s = __dadd_rn(s, __dmul_rn(vv[t], xv[t]));
+      }
+      for (; k < kend; ++k) {
+        const int c = sc[w][k - base];
+        s = __dadd_rn(s, __dmul_rn(sv[w][k - base], XEL ? ld_el(x + c, el) : __ldcg(x + c)));
+      }
+      __syncwarp();
+    }
+    if (r < rows) y[r] = s;
+  }
+}
+
 int main(int argc, char** argv) {
   int nsm;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
@@ -196,6 +281,19 @@ int main(int argc, char** argv) {
     timeit("1cta: 8 lanes x4", [&] { spmv_lanes_u<8, 4><<<nsm, 256>>>(sh.rows, ptr, col, val, x, y); });
     timeit("1cta: 8 lanes x8", [&] { spmv_lanes_u<8, 8><<<nsm, 256>>>(sh.rows, ptr, col, val, x, y); });
     timeit("1cta: 16 lanes x4", [&] { spmv_lanes_u<16, 4><<<nsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+    for (int bpsm : {4, 8}) {
+      char lab[64];
+      snprintf(lab, sizeof lab, "solver x.cg b/sm=%d", bpsm);
+      timeit(lab, [&] { spmv_solver<false><<<nsm * bpsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+      snprintf(lab, sizeof lab, "solver x.el b/sm=%d", bpsm);
+      timeit(lab, [&] { spmv_solver<true><<<nsm * bpsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+      snprintf(lab, sizeof lab, "warpstage320 b/sm=%d", bpsm);
+      timeit(lab, [&] { spmv_warpstage<320, false><<<nsm * bpsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+      snprintf(lab, sizeof lab, "warpstage320 x.el b/sm=%d", bpsm);
+      timeit(lab, [&] { spmv_warpstage<320, true><<<nsm * bpsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+      snprintf(lab, sizeof lab, "warpstage128 b/sm=%d", bpsm);
+      timeit(lab, [&] { spmv_warpstage<128, false><<<nsm * bpsm, 256>>>(sh.rows, ptr, col, val, x, y); });
+    }
     CK(cudaGetLastError());
     cudaFree(ptr); cudaFree(col); cudaFree(val); cudaFree(x); cudaFree(y);
   }
