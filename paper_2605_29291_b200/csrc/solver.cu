@@ -519,6 +519,11 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
 
 // A factored stop: run the requested sweep / gradient(s) as standalone
 // kernels (8 CTAs per SM) on the context's stream, then the op resumes.
+static int gxb_per_sm() {
+  static const int v = [] { const char* e = std::getenv("RAPDB_GXB_CTAS"); return e ? std::max(1, std::atoi(e)) : 16; }();   // C3f: 8 -> 16 per SM, 1.64 -> 1.59 s
+  return v;
+}
+
 int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   const DevProblem& P = c->P;
   const Work& w = c->w;
@@ -537,7 +542,7 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
       double* out = oid == 0 ? w.gxs : w.gxb + (long long)st.ig_new * n;
       const double* Wpar = w.W + (long long)par * P.nr;
       fac_gx_a_kernel<<<grid, kThreads, (size_t)std::max(P.fnb, 1) * 8, c->stream>>>(P, w, Wpar, lam, out);
-      fac_gx_b_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, lam, out);
+      fac_gx_b_kernel<<<c->nsm * gxb_per_sm(), kThreads, 0, c->stream>>>(P, w, lam, out);
       g_launches += 2;
     }
   } else {
