@@ -177,9 +177,181 @@ __device__ __forceinline__ double dual_at(const KArgs& K, const double* v_s, con
   return j < K.P.p ? v_s[j] : lam_s[j - K.P.p];
 }
 
+// ----------------------------------- long-vector variants (factored path)
+// C3's vectors are 10^6 (x) and 5 * 10^5 (multipliers) long, and the
+// persistent kernel runs 8 warps per SM: the plain grid-stride loops are
+// latency bound.  These variants issue four strides' loads before using them
+// -- the same per-thread element order, so the same partial sums -- and live
+// out of line so the dense path's inlined steps keep their registers.  The
+// factored path has p = 0, no dual ball, multipliers read from global memory.
+constexpr int kLV = 4;
+
+__device__ __noinline__ int ty_dual_fac(const KArgs& K, Sm& S) {
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  if (threadIdx.x == 0) {
+    st.sigma = st.gamma * st.tau;
+    st.alpha_n = K.prm.c_alpha / st.sigma;
+    st.beta_n = 0.0;
+    st.theta = st.sigma_prev / st.sigma;
+  }
+  __syncthreads();
+  const long long np = K.P.m;
+  const double sigma = st.sigma, theta = st.theta;
+  const double* yc = w.y + (long long)st.cur * np;
+  const double* gc = w.gy + (long long)st.ig_cur * np;
+  const double* gp = w.gy + (long long)st.ig_prev * np;
+  const long long G = gstride();
+  for (long long j0 = gtid(); j0 < np; j0 += kLV * G) {
+    double a[kLV], b[kLV], c[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < np) { a[t] = ldcg(gc + j); b[t] = ldcg(gp + j); c[t] = ldcg(yc + j); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < np) {
+        const double t1 = (1.0 + theta) * a[t];
+        const double t2 = theta * b[t];
+        w.ytr[j] = fmax(c[t] + sigma * (t1 - t2), 0.0);
+      }
+    }
+  }
+  return gsync(K, S) ? TY_GXPART : kAbort;
+}
+
+__device__ __noinline__ int ty_primal_fac(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const long long n = P.n, m = P.m;
+  const int cur = st.cur, nxt = cur ^ 1;
+  const double tau = st.tau;
+  const double* xc = w.x + (long long)cur * n;
+  double* xn = w.x + (long long)nxt * n;
+  const long long G = gstride();
+  double s_dp = 0.0, s_gd = 0.0;
+  for (long long j0 = gtid(); j0 < n; j0 += kLV * G) {
+    double gx[kLV], xj[kLV], lo[kLV], hi[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < n) { gx[t] = ldcg(w.gxs + j); xj[t] = ldcg(xc + j); lo[t] = __ldg(P.lo + j); hi[t] = __ldg(P.hi + j); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < n) {
+        const double xnj = clipd(xj[t] - tau * gx[t], lo[t], hi[t]);
+        xn[j] = xnj;
+        const double d = xnj - xj[t];
+        s_dp += d * d;
+        s_gd += gx[t] * d;
+      }
+    }
+  }
+  double s_dd = 0.0, s_ml = 0.0;
+  const double* yc = w.y + (long long)cur * m;
+  double* yn = w.y + (long long)nxt * m;
+  const double* gvc = w.gval + (long long)cur * (m + 1);
+  for (long long j0 = gtid(); j0 < m; j0 += kLV * G) {
+    double yv[kLV], yo[kLV], gv[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) { yv[t] = ldcg(w.ytr + j); yo[t] = ldcg(yc + j); gv[t] = ldcg(gvc + (j + 1)); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) {
+        yn[j] = yv[t];
+        const double d = yv[t] - yo[t];
+        s_dd += d * d;
+        s_ml += yv[t] * gv[t];
+      }
+    }
+  }
+  const double v5[5] = {s_dp, s_gd, s_dd, 0.0, s_ml};
+  const int sl[5] = {S_DP, S_GXDX, S_DD, S_MIXV, S_MIXL};
+  put_partials(K, S, v5, sl);
+  return gsync(K, S) ? TY_SWEEP : kAbort;
+}
+
+__device__ __noinline__ int ty_gy_fac(const KArgs& K, Sm& S) {
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const long long m = K.P.m;
+  const int nxt = st.cur ^ 1;
+  const double* gvn = w.gval + (long long)nxt * (m + 1);
+  const double* gc = w.gy + (long long)st.ig_cur * m;
+  double* gnew = w.gy + (long long)st.ig_new * m;
+  const double* yn = w.y + (long long)nxt * m;
+  const long long G = gstride();
+  double s_dg = 0.0, s_nl = 0.0;
+  for (long long j0 = gtid(); j0 < m; j0 += kLV * G) {
+    double a[kLV], b[kLV], c[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) { a[t] = ldcg(gvn + (j + 1)); b[t] = ldcg(gc + j); c[t] = ldcg(yn + j); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) {
+        gnew[j] = a[t];
+        const double d = a[t] - b[t];
+        s_dg += d * d;
+        s_nl += c[t] * a[t];
+      }
+    }
+  }
+  const double v3[3] = {s_dg, 0.0, s_nl};
+  const int sl[3] = {S_DGY, S_NEWV, S_NEWL};
+  put_partials(K, S, v3, sl);
+  return gsync(K, S) ? TY_DECIDE : kAbort;
+}
+
+// the ergodic sums of roll() for long vectors
+__device__ __noinline__ void roll_sums_long(const KArgs& K, double t_k, const double* xk, const double* yk) {
+  const Work& w = K.w;
+  const long long n = K.P.n, np = K.P.p + K.P.m;
+  const long long G = gstride();
+  for (long long j0 = gtid(); j0 < n; j0 += kLV * G) {
+    double a[kLV], c[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < n) { a[t] = ldcg(xk + j); c[t] = ldcg(w.xcum + j); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < n) w.xcum[j] = c[t] + t_k * a[t];
+    }
+  }
+  for (long long j0 = gtid(); j0 < np; j0 += kLV * G) {
+    double a[kLV], c[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < np) { a[t] = ldcg(yk + j); c[t] = ldcg(w.ycum + j); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < np) w.ycum[j] = c[t] + t_k * a[t];
+    }
+  }
+}
+
 // =========================================================== APDB-yx trial
 
 __device__ int ty_dual(const KArgs& K, Sm& S) {
+  if (K.P.kind == 1) return ty_dual_fac(K, S);
   const DevProblem& P = K.P;
   const DevParams& prm = K.prm;
   const Work& w = K.w;
@@ -227,6 +399,7 @@ __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
 }
 
 __device__ int ty_primal(const KArgs& K, Sm& S) {
+  if (K.P.kind == 1) return ty_primal_fac(K, S);
   const DevProblem& P = K.P;
   const Work& w = K.w;
   SolverState& st = *S.st;
@@ -270,6 +443,7 @@ __device__ int ty_primal(const KArgs& K, Sm& S) {
 }
 
 __device__ int ty_gy(const KArgs& K, Sm& S) {
+  if (K.P.kind == 1) return ty_gy_fac(K, S);
   const DevProblem& P = K.P;
   const Work& w = K.w;
   SolverState& st = *S.st;
@@ -333,6 +507,10 @@ __device__ void roll(const KArgs& K, Sm& S) {
   const double t_k = S.tot[NSLOT + 1];
   const double* xk = w.x + (long long)st.cur * n;
   const double* yk = w.y + (long long)st.cur * np;
+  if (K.P.kind == 1) {
+    roll_sums_long(K, t_k, xk, yk);
+    return;
+  }
   for (long long j = gtid(); j < n; j += gstride()) w.xcum[j] += t_k * ldcg(xk + j);
   for (long long j = gtid(); j < np; j += gstride()) w.ycum[j] += t_k * ldcg(yk + j);
 }
