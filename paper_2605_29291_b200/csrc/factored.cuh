@@ -280,7 +280,7 @@ __device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const dou
 
 // ---- standalone kernels the host launches at a factored stop (fq requests):
 // same device code, any grid (blockDim = kThreads), many CTAs per SM
-__global__ void __launch_bounds__(kThreads) fac_sweep_a_kernel(DevProblem P, Work w, const double* x, int par) {
+__device__ __forceinline__ void fac_sweep_a_staged(const DevProblem& P, const Work& w, const double* x, int par) {
   __shared__ double sv[kWarps][kStageCap];
   __shared__ int sc[kWarps][kStageCap];
   const uint64_t ef = evict_first_policy();
@@ -303,6 +303,9 @@ __global__ void __launch_bounds__(kThreads) fac_sweep_a_kernel(DevProblem P, Wor
     s = warp_sum(s);
     if (lane == 0) w.pcx[it] = s;
   }
+}
+__global__ void __launch_bounds__(kThreads) fac_sweep_a_kernel(DevProblem P, Work w, const double* x, int par) {
+  fac_sweep_a_staged(P, w, x, par);
 }
 __global__ void __launch_bounds__(kThreads) fac_sweep_b_kernel(DevProblem P, Work w, int par) {
   fac_sweep_b(P, w, par);
