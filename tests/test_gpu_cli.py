@@ -173,3 +173,44 @@ def test_module_entry_point_exit_code():
                         os.path.join(GOLDEN, "problem_rq.json"), "--solver", "newton"],
                        cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 1 and "unknown solver" in r.stderr
+
+
+@pytest.mark.gpu
+def test_solve_binary_stack_matches_json(tmp_path):
+    """--problem as the binary stack (problem.save_stack, .npz): the same run
+    as from the reference's problem JSON."""
+    from paper_2605_29291_b200 import problem
+    src = os.path.join(GOLDEN, "problem_rq.json")
+    npz = str(tmp_path / "rq.npz")
+    problem.save_stack(problem.load(src), npz)
+    outs = {}
+    for name, path in (("json", src), ("npz", npz)):
+        s = str(tmp_path / (name + ".json"))
+        c = str(tmp_path / (name + ".csv"))
+        assert cli.main(["solve", "--problem", path, "--solver", "rapdb-yx", "--summary", s, "--out", c]) == 0
+        outs[name] = (json.load(open(s)), open(c).read())
+    a, b = outs["json"], outs["npz"]
+    assert a[1] == b[1]
+    for k in ("iterations", "evals", "converged", "kkt", "infeas", "f"):
+        assert a[0][k] == b[0][k]
+
+
+@pytest.mark.gpu
+def test_gap_at_a_given_point(tmp_path, capsys):
+    """gap --point {x, v, lam}: the device smoothed gap at that point agrees
+    with the oracle's restatement of diagnostics.smoothed_gap."""
+    from oracle import rapdb_oracle as O
+    from paper_2605_29291_b200 import problem
+    src = os.path.join(GOLDEN, "problem_rq.json")
+    inst = problem.load(src)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-0.5, 0.5, inst.n)
+    lam = rng.uniform(0.0, 1.0, inst.m)
+    pt = tmp_path / "pt.json"
+    pt.write_text(json.dumps({"x": x.tolist(), "lam": lam.tolist()}))
+    assert cli.main(["gap", "--problem", src, "--point", str(pt), "--xi", "0.1"]) == 0
+    got = json.loads(capsys.readouterr().out)
+    P = O.Problem(list(np.asarray(inst.Q)), list(np.asarray(inst.q)), inst.r, inst.A, inst.b,
+                  inst.primal_set.lower, inst.primal_set.upper, inst.mu)
+    ref_gap = O.smoothed_gap(P, x, np.zeros(inst.p), lam, 0.1)[0]
+    assert np.isclose(got["gap"], ref_gap, rtol=1e-8, atol=1e-12)
