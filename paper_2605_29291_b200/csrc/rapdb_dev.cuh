@@ -70,6 +70,7 @@ struct SolverState {
   // fq[2] = x source: 0 w.x[par], 1 rc.in_x), 2 gradient(s) (fq[1] = count,
   // then per request: parity, multiplier id, output id; factored.cuh)
   int fq[8];
+  double ball_nv, ball_nl; // CTA-local yx dual step: |v~|^2, |lam~|^2 of the trial (re-staging after a relaunch)
   double step_ns[64];      // device time per state-machine step (CTA 0, globaltimer); 60..62: sweep sub-phases
   long long step_cnt[64];
 };

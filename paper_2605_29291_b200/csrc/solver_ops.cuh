@@ -348,10 +348,81 @@ __device__ __noinline__ void roll_sums_long(const KArgs& K, double t_k, const do
   }
 }
 
+// ------------------------------------------- CTA-local yx dual step (dense)
+// With few multipliers every CTA forms the whole trial y~ itself straight into
+// its shared staging area (the same bits in every CTA: same inputs, same
+// order, the ball sums in a fixed block-level order), so the dual step needs
+// no grid barrier and the gradient and primal steps no re-staging.  CTA 0
+// also writes y~ (before the ball) to global memory; a sharded run that left
+// the kernel at the gradient exchange re-stages from it with the saved sums.
+constexpr int kLocalNp = 2048;
+__device__ __forceinline__ bool dual_cta_local(const KArgs& K) {
+  return K.P.kind == 0 && K.P.p + K.P.m <= kLocalNp;
+}
+__device__ __forceinline__ bool dual_restage(const KArgs& K) { return K.rc.split && !K.rc.p2p; }
+
+__device__ int ty_dual_local(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const DevParams& prm = K.prm;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  if (threadIdx.x == 0) {
+    st.sigma = st.gamma * st.tau;
+    st.alpha_n = prm.c_alpha / st.sigma;
+    st.beta_n = 0.0;
+    st.theta = st.sigma_prev / st.sigma;
+  }
+  __syncthreads();
+  const int p = P.p, np = P.p + P.m;
+  const double sigma = st.sigma, theta = st.theta;
+  const double* yc = w.y + (long long)st.cur * np;
+  const double* gc = w.gy + (long long)st.ig_cur * np;
+  const double* gp = w.gy + (long long)st.ig_prev * np;
+  double* stg = S.stage;   // [v_s | lam_s]
+  double nv = 0.0, nl = 0.0;
+  for (int j = threadIdx.x; j < np; j += kThreads) {
+    const double t1 = (1.0 + theta) * ldcg(gc + j);
+    const double t2 = theta * ldcg(gp + j);
+    double yt = ldcg(yc + j) + sigma * (t1 - t2);
+    if (j >= p) yt = fmax(yt, 0.0);
+    stg[j] = yt;
+    if (blockIdx.x == 0) w.ytr[j] = yt;
+    if (j < p) nv += yt * yt; else nl += yt * yt;
+  }
+  if (prm.ball) {
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const double a = warp_sum(nv), b = warp_sum(nl);
+    if (lane == 0) { S.red[wp * 8] = a; S.red[wp * 8 + 1] = b; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      double t = S.red[threadIdx.x];
+      for (int i = 1; i < kWarps; ++i) t += S.red[i * 8 + threadIdx.x];
+      S.tot[threadIdx.x == 0 ? S_BALL_V : S_BALL_L] = t;
+    }
+    __syncthreads();
+    const BallScale bs = ball_scale(prm, S.tot[S_BALL_V], S.tot[S_BALL_L]);
+    if (threadIdx.x == 0) { st.ball_nv = S.tot[S_BALL_V]; st.ball_nl = S.tot[S_BALL_L]; }
+    for (int j = threadIdx.x; j < np; j += kThreads) {
+      if (j < p) { if (bs.av) stg[j] = bs.sv * stg[j]; }
+      else if (bs.al) stg[j] = bs.sl * stg[j];
+    }
+  }
+  __syncthreads();
+  return TY_GXPART;
+}
+
+// the staged trial duals for the gradient / primal steps of a CTA-local trial
+__device__ __forceinline__ void dual_local_stage(const KArgs& K, Sm& S, bool after_relaunch) {
+  if (!after_relaunch) return;   // still in shared memory from ty_dual_local
+  const BallScale bs = K.prm.ball ? ball_scale(K.prm, S.st->ball_nv, S.st->ball_nl) : BallScale{1.0, 1.0, 0, 0};
+  stage_dual(K, K.w.ytr, bs, S.stage, S.stage + K.P.p);
+}
+
 // =========================================================== APDB-yx trial
 
 __device__ int ty_dual(const KArgs& K, Sm& S) {
   if (K.P.kind == 1) return ty_dual_fac(K, S);
+  if (dual_cta_local(K)) return ty_dual_local(K, S);
   const DevProblem& P = K.P;
   const DevParams& prm = K.prm;
   const Work& w = K.w;
@@ -389,10 +460,14 @@ __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
   const DevProblem& P = K.P;
   const Work& w = K.w;
   SolverState& st = *S.st;
-  const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
   double* v_s = S.stage;
   double* lam_s = S.stage + P.p;
-  stage_dual(K, w.ytr, bs, v_s, lam_s);
+  if (dual_cta_local(K)) {
+    dual_local_stage(K, S, false);
+  } else {
+    const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
+    stage_dual(K, w.ytr, bs, v_s, lam_s);
+  }
   if (!gx_part(K, S, st.cur, w.ytr + P.p, lam_s, w.gxs)) return kAbort;
   xk = X_GX;
   return TY_PRIMAL;
@@ -405,10 +480,14 @@ __device__ int ty_primal(const KArgs& K, Sm& S) {
   SolverState& st = *S.st;
   const int n = P.n, p = P.p, m = P.m, np = p + m;
   const int cur = st.cur, nxt = cur ^ 1;
-  const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
   double* v_s = S.stage;
   double* lam_s = S.stage + p;
-  stage_dual(K, w.ytr, bs, v_s, lam_s);
+  if (dual_cta_local(K)) {
+    dual_local_stage(K, S, dual_restage(K));
+  } else {
+    const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
+    stage_dual(K, w.ytr, bs, v_s, lam_s);
+  }
   const double tau = st.tau;
   const double* xc = w.x + (long long)cur * n;
   double* xn = w.x + (long long)nxt * n;
