@@ -446,7 +446,8 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
   // for the items not already reduced during the stream
   const long long items = (long long)P.nact * g.nbB;
   if (nch && b == 0 && threadIdx.x < nch) K.w.ccnt[threadIdx.x] = 0u;
-  for (long long it = (long long)b * kWarps + warp; it < items; it += (long long)G * kWarps) {
+  // warp-major item order: a handful of items still spreads over all SMs
+  for (long long it = (long long)warp * G + b; it < items; it += (long long)G * kWarps) {
     if (nch && __ldcg(K.w.idone + it)) {
       __syncwarp();
       if (lane == 0) K.w.idone[it] = 0;
