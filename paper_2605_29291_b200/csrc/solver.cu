@@ -558,8 +558,6 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
 // (NCCL over NVLink in the Python binding) and the op resumes in a new launch.
 int launch(rapdb_ctx* c, RunCfg rc) {
   if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
-  if (c->P.kind == 1 && c->prm.ball != 0)
-    return fail(c, RAPDB_ECONFIG, "factored instances support the unbounded dual set only");
   rc.split = c->split;
   rc.fac_host = c->fac_host;
   rc.p2p = c->p2p;

@@ -170,7 +170,7 @@ __device__ __forceinline__ bool gx_part(const KArgs& K, Sm& S, int par, const do
 }
 
 // multiplier j of a dual vector: staged copy (dense) or global y (factored;
-// balls are rejected there, so the global vector is already final)
+// a dual ball has already scaled it there: ball_in_place_fac)
 __device__ __forceinline__ double dual_at(const KArgs& K, const double* v_s, const double* lam_s, const double* yg,
                                           long long j) {
   if (K.P.kind == 1) return ldcg(yg + j);
@@ -183,8 +183,22 @@ __device__ __forceinline__ double dual_at(const KArgs& K, const double* v_s, con
 // latency bound.  These variants issue four strides' loads before using them
 // -- the same per-thread element order, so the same partial sums -- and live
 // out of line so the dense path's inlined steps keep their registers.  The
-// factored path has p = 0, no dual ball, multipliers read from global memory.
+// factored path has p = 0 and reads its multipliers from global memory (a
+// dual ball scales them there: ball_in_place_fac).
 constexpr int kLV = 4;
+
+// Factored dual ball (geometry.py:263-311; p = 0, so only the multiplier
+// block): once the trial multipliers' squared-norm partials are published
+// (and a grid barrier passed), every thread scales the entries it wrote
+// itself -- the same grid-stride elements -- so the global y~ that the
+// gradient gather, the primal step and the test read is already final.
+__device__ __noinline__ bool ball_in_place_fac(const KArgs& K, Sm& S) {
+  if (!K.prm.ball) return true;
+  const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
+  if (!bs.al) return true;
+  for (long long j = gtid(); j < K.P.m; j += gstride()) K.w.ytr[j] = bs.sl * K.w.ytr[j];
+  return gsync(K, S);
+}
 
 __device__ __noinline__ int ty_dual_fac(const KArgs& K, Sm& S) {
   const Work& w = K.w;
@@ -202,6 +216,7 @@ __device__ __noinline__ int ty_dual_fac(const KArgs& K, Sm& S) {
   const double* gc = w.gy + (long long)st.ig_cur * np;
   const double* gp = w.gy + (long long)st.ig_prev * np;
   const long long G = gstride();
+  double nl = 0.0;
   for (long long j0 = gtid(); j0 < np; j0 += kLV * G) {
     double a[kLV], b[kLV], c[kLV];
 #pragma unroll
@@ -215,11 +230,19 @@ __device__ __noinline__ int ty_dual_fac(const KArgs& K, Sm& S) {
       if (j < np) {
         const double t1 = (1.0 + theta) * a[t];
         const double t2 = theta * b[t];
-        w.ytr[j] = fmax(c[t] + sigma * (t1 - t2), 0.0);
+        const double yt = fmax(c[t] + sigma * (t1 - t2), 0.0);
+        w.ytr[j] = yt;
+        nl += yt * yt;
       }
     }
   }
-  return gsync(K, S) ? TY_GXPART : kAbort;
+  if (K.prm.ball) {
+    const double v2[2] = {0.0, nl};
+    const int sl[2] = {S_BALL_V, S_BALL_L};
+    put_partials(K, S, v2, sl);
+  }
+  if (!gsync(K, S)) return kAbort;
+  return ball_in_place_fac(K, S) ? TY_GXPART : kAbort;
 }
 
 __device__ __noinline__ int ty_primal_fac(const KArgs& K, Sm& S) {
@@ -712,6 +735,7 @@ __device__ int tx_gxpart(const KArgs& K, Sm& S, int& xk) {
   const Work& w = K.w;
   SolverState& st = *S.st;
   const int n = P.n, p = P.p, np = p + P.m;
+  if (P.kind == 1 && !ball_in_place_fac(K, S)) return kAbort;   // factored: y~ scaled in global memory
   const BallScale bs = ball_from_slots(K, S, S_BALL_V, S_BALL_L);
   double* v_n = S.stage;
   double* lam_n = S.stage + p;

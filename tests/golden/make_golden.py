@@ -214,13 +214,21 @@ def small_fixtures():
         print(key, "iterations", out["iterations"], "wall", round(wall, 2))
     save("c0", arrays, meta)
 
-    # 4. C4-shaped small KML epigraph (N=120): p = 1, free t, zero Q0
+    kml_fixtures()
+
+
+def kml_fixtures():
+    # 4. C4-shaped small KML epigraph (N=120): p = 1, free t, zero Q0.  Both
+    # step searches under FixedRestart(500): nm stops at the 3000 budget, mono
+    # converges after ~12k iterations (the full-size C4 mono run is far slower)
     arr = instances.kml_epigraph(N=120, d=10)
     inst = ref_instance(arr)
     arrays, meta = {}, {"instance": "instances.kml_epigraph(N=120, d=10)", "cases": {}}
     arrays["Q_checksum"] = np.array([float(np.sum(arr.Q[i])) for i in range(arr.m + 1)])
     for key, case in {"nm_fixed500": dict(nm=True, policy={"kind": "fixed", "period": 500},
-                                          budget=3000, eps=1e-6)}.items():
+                                          budget=3000, eps=1e-6),
+                      "mono_fixed500": dict(nm=False, policy={"kind": "fixed", "period": 500},
+                                            budget=20000, eps=1e-6)}.items():
         out, wall = run_case(inst, case, set(range(1, 201)))
         for k, v in out.items():
             arrays[f"{key}/{k}"] = v
@@ -309,9 +317,12 @@ if __name__ == "__main__":
     ap.add_argument("--factored", action="store_true")
     ap.add_argument("--c4", action="store_true")
     ap.add_argument("--c2s", action="store_true")
+    ap.add_argument("--kml", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
         small_fixtures()
+    if a.kml:
+        kml_fixtures()
     if a.factored:
         factored_fixtures()
     if a.c1:

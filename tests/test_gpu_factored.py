@@ -139,11 +139,42 @@ def test_factored_shapes_vs_oracle(shape, nm):
     np.testing.assert_allclose(inst.g_value(z.x), O.FactoredProblem(arr).g(z.x), rtol=1e-10, atol=1e-10)
 
 
+@pytest.mark.parametrize("kind", ["joint", "split"])
+@pytest.mark.parametrize("mode,nm", [("yx", False), ("yx", True), ("xy", True)])
+def test_factored_dual_ball_vs_oracle(small, kind, mode, nm):
+    """JointBall / SplitBall on the factored path (geometry.py:263-311): the
+    radius is half the unbounded run's multiplier norm after 200 iterations,
+    so the ball binds.  The device scales y~ from a fixed-order norm, numpy
+    from np.linalg.norm: rounding-level differences, same tolerances as the
+    unbounded traces."""
+    from paper_2605_29291_b200.geometry import JointBall, SplitBall
+    arr, inst, g = small
+    r = 0.5 * float(np.linalg.norm(g["mono/snap_lam"][-1]))
+    assert r > 0
+    ball = JointBall(r) if kind == "joint" else SplitBall(1.0, r)
+    oball = O.Ball(1, r) if kind == "joint" else O.Ball(2, 1.0, r)
+    iters = 120
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=4):
+        res = O.run_restarted(O.factored_problem(arr), O.Options(mode=mode, nonmonotone=nm, ball=oball),
+                              O.Policy(kind="none"), budget=iters)
+    tr_o = np.array([[t.iter, t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total]
+                     for t in res.trace])
+    cfg = R.SolverConfig(mode=mode, nonmonotone=nm, dual_ball=ball)
+    eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst, ball))
+    eng.run_block(iters)
+    tr = trace_arr(eng.trace)
+    np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
+    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    z = eng.last
+    assert rel(z.x, res.x) <= 1e-8
+    assert rel(z.lam, res.lam) <= 1e-8
+    assert np.linalg.norm(z.lam) <= r * (1 + 1e-12)
+    assert np.linalg.norm(res.lam) >= 0.999 * r   # the ball is active at the end
+
+
 def test_factored_rejects_unsupported(small):
     arr, inst, _ = small
-    from paper_2605_29291_b200.geometry import JointBall
-    with pytest.raises(R.ConfigurationError):
-        R.ApdbEngine(inst, R.SolverConfig(dual_ball=JointBall(5.0)), R.initial_iterate(inst))
     with pytest.raises(R.ConfigurationError):
         R.run_restarted(inst, R.SolverConfig(), R.AdaptiveRestart(warmup=5, check_period=5), budget=30)
 
@@ -198,6 +229,33 @@ def test_factored_emulated_shards(small, nranks, nm):
         assert rel(z.lam, ref.last.lam) <= 1e-11
         np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
         np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+
+
+def test_factored_emulated_shards_with_ball(small):
+    """Two constraint shards with a binding JointBall: the multipliers are
+    replicated, so each rank's norm is complete and the scaled y~ agrees with
+    the unsharded run (same steps, iterates to 1e-11)."""
+    from paper_2605_29291_b200.geometry import JointBall
+    from paper_2605_29291_b200.sharding import EmulatedCluster
+    arr, inst, g = small
+    ball = JointBall(0.5 * float(np.linalg.norm(g["mono/snap_lam"][-1])))
+    cfg = R.SolverConfig(mode="yx", nonmonotone=True, dual_ball=ball)
+    iters = 80
+    ref = R.ApdbEngine(inst, cfg, R.initial_iterate(inst, ball))
+    ref.run_block(iters)
+    tr_ref = trace_arr(ref.trace)
+    cluster = EmulatedCluster(2)
+
+    def body(shard):
+        eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst, ball), shard=shard)
+        eng.run_block(iters)
+        return trace_arr(eng.trace), eng.last
+
+    for tr, z in cluster.run(inst, body):
+        np.testing.assert_array_equal(tr[:, 5], tr_ref[:, 5])
+        np.testing.assert_allclose(tr[:, 1:5], tr_ref[:, 1:5], rtol=1e-12)
+        assert rel(z.x, ref.last.x) <= 1e-12
+        assert rel(z.lam, ref.last.lam) <= 1e-11
 
 
 @pytest.mark.slow

@@ -241,6 +241,26 @@ def test_kml_small_epigraph():
     assert res.iterations == int(g["nm_fixed500/iterations"])
 
 
+def test_kml_small_epigraph_monotone_to_convergence():
+    """Monotone step search on the C4-shaped KML epigraph: the reference
+    needs ~12k iterations (5 restarts of 500 do not shorten it); the device
+    run must stop within 2% of that count (north_star) with the first 200
+    accepted step sizes bit-identical and the final point at 1e-6."""
+    g = load_golden("kml_small")
+    arr = instances.kml_epigraph(N=120, d=10)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    res = R.run_restarted(inst, R.SolverConfig(mode="yx", nonmonotone=False), R.FixedRestart(500),
+                          budget=20000, criteria=crit(1e-6))
+    tr = trace_arr(res.trace)
+    np.testing.assert_array_equal(tr[:200, TAU], g["mono_fixed500/trace"][:200, TAU])
+    n_ref = int(g["mono_fixed500/iterations"])
+    assert bool(res.converged) and bool(g["mono_fixed500/converged"])
+    assert abs(res.iterations - n_ref) <= 0.02 * n_ref, (res.iterations, n_ref)
+    k_ref, f_ref = float(g["mono_fixed500/metrics"][0]), float(g["mono_fixed500/metrics"][5])
+    assert res.metrics.kkt_residual <= 1e-6
+    assert abs(res.metrics.f_value - f_ref) <= 1e-6 * (1 + abs(f_ref)), (res.metrics.f_value, f_ref, k_ref)
+
+
 def test_nonconvergence_state(small):
     _, inst = small
     eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", tau_bar=1e6, max_backtracks=0), R.initial_iterate(inst))
