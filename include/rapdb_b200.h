@@ -181,9 +181,10 @@ int rapdb_pack_symmetric(int n, long long count, const double* src, long long ld
  *   rblk  HOST [mq+2] row offsets of the blocks (rblk[0] = 0, rblk[mq+1] = nr)
  *   C     [(mq+1) x n] linear terms, d [mq+1] constants
  *   A     CSR [L x n] (a_ptr[L+1], a_col, a_val), A^T CSR [n x L], b [L]
- * All other pointers are device pointers.  No equality block (p = 0), the
- * dual set must be Unbounded, and the smoothed gap is not available (its
- * n x n H does not fit at this n): adaptive restarts need a dense instance.
+ * All other pointers are device pointers.  No equality block (p = 0), and
+ * the smoothed gap is not available (its n x n H does not fit at this n):
+ * adaptive restarts need a dense instance.  Dual balls are supported (the
+ * trial multipliers are scaled in place after one norm reduction).
  * Equivalent to rapdb_bind_factored_range over the whole instance.          */
 int rapdb_bind_factored(rapdb_ctx* ctx, int n, int mq, int L, long long nr,
                         const long long* r_ptr, const int* r_col, const double* r_val,
