@@ -394,16 +394,12 @@ __device__ __noinline__ void sweep_sym(const KArgs& K, Sm& S, const double* xsrc
         xw[96 + lane] = c0 + 32 + lane < n ? ldcg(xsrc + c0 + 32 + lane) : 0.0;
         __syncwarp();
         sym::consume_unit_x(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xw, xw + 64,
-                            un.bi, un.bj, Pt + a * pstride, keep);
+                            un.bi, un.bj, Pt + a * pstride, keep, &emptyb[s]);
         __syncwarp();
-      } else {
+      } else {   // the slot is handed back inside, right after the last tile read
         sym::consume_unit(gg, reinterpret_cast<const double*>(ring + (long long)s * stage_bytes), xs,
-                          un.bi, un.bj, Pt + a * pstride, keep);
+                          un.bi, un.bj, Pt + a * pstride, keep, &emptyb[s]);
       }
-      // generic-proxy reads of the slot before the producer's next bulk write
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyb[s]);
       u += adv;
       while (u >= upm) { u -= upm; ++a; }
       s += ncw;

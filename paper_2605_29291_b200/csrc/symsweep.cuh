@@ -158,9 +158,25 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ T, const do
 // One unit held in shared memory (tile) -> its slots of Pt.  xs: staged x,
 // zero padded to nbB * 64.  Pa: Pt + a * nbB * nbB * 64 (this matrix).
 // xr / xc: the 64 entries of x at block rows Bi / Bj (shared memory)
+// Hand the ring slot back as soon as the warp's last read of the tile is
+// done (before the final butterfly and the partial stores): generic-proxy
+// reads ordered before the producer's next bulk write, then one arrival.  The
+// asm memory clobbers keep the tile loads on this side; the arithmetic is
+// unchanged (same bits), only the slot is held for less time.
+__device__ __forceinline__ void release_slot(uint64_t* bar) {
+  if (!bar) return;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(a) : "memory");
+  }
+}
+
 __device__ __forceinline__ void consume_unit_x(const Geom& g, const double* __restrict__ tile,
                                                const double* __restrict__ xr, const double* __restrict__ xc,
-                                               int bi, int bj, double* __restrict__ Pa, uint64_t pol) {
+                                               int bi, int bj, double* __restrict__ Pa, uint64_t pol,
+                                               uint64_t* rel = nullptr) {
   const int lane = threadIdx.x & 31;
   int rs, cs;
   unit_subtiles(g, bi, bj, rs, cs);
@@ -181,8 +197,11 @@ __device__ __forceinline__ void consume_unit_x(const Geom& g, const double* __re
         v[r] = q * xj;
         c = fma(q, xr[r], c);
       }
-      o0 = o0 + transpose_reduce(v);
       o1 = c + col_dot(tile + 2 * kTD, xr + kT);
+      release_slot(rel);
+      o0 = o0 + transpose_reduce(v);
+    } else {
+      release_slot(rel);
     }
     double* out = Pa + ((long long)bi * nbB + bi) * kB;
     st_keep(out + lane, o0, pol);
@@ -211,6 +230,7 @@ __device__ __forceinline__ void consume_unit_x(const Geom& g, const double* __re
       }
       c[sc] = c[sc] + (c0 + c1);
     }
+    if (sr == rs - 1) release_slot(rel);
     st_keep(outR + sr * kT + lane, transpose_reduce(v), pol);
   }
   double* outC = Pa + ((long long)bj * nbB + bi) * kB;
@@ -219,8 +239,8 @@ __device__ __forceinline__ void consume_unit_x(const Geom& g, const double* __re
 
 __device__ __forceinline__ void consume_unit(const Geom& g, const double* __restrict__ tile,
                                              const double* __restrict__ xs, int bi, int bj,
-                                             double* __restrict__ Pa, uint64_t pol) {
-  consume_unit_x(g, tile, xs + bi * kB, xs + bj * kB, bi, bj, Pa, pol);
+                                             double* __restrict__ Pa, uint64_t pol, uint64_t* rel = nullptr) {
+  consume_unit_x(g, tile, xs + bi * kB, xs + bj * kB, bi, bj, Pa, pol, rel);
 }
 
 }  // namespace sym
