@@ -79,8 +79,13 @@ def run_case(inst, case, snap_iters):
                              dual_ball=ball_of(case.get("ball")))
     crit = None
     if case.get("eps") is not None:
-        crit = diagnostics.TerminationCriteria(criterion="conic", eps_kkt=case["eps"],
-                                               eps_feas=case["eps"])
+        if case.get("criterion", "conic") == "conic":
+            crit = diagnostics.TerminationCriteria(criterion="conic", eps_kkt=case["eps"],
+                                                   eps_feas=case["eps"],
+                                                   f_star=case.get("f_star"))
+        else:   # "paper51" (diagnostics.py:254-258): relative f-gap + mean violation
+            crit = diagnostics.TerminationCriteria(criterion="paper51", eps=case["eps"],
+                                                   f_star=case.get("f_star"))
     snaps_x, snaps_lam, snaps_v = {}, {}, {}
     orig_step = rapdb.engine.ApdbEngine.step
 
@@ -105,6 +110,7 @@ def run_case(inst, case, snap_iters):
     met = res.metrics
     out = {
         "trace": trace_array(res.trace),
+        "subopt": np.array([np.nan if r.subopt is None else r.subopt for r in res.trace]),
         "snap_iters": np.array(keys, dtype=np.int64),
         "snap_x": np.array([snaps_x[k] for k in keys]).reshape(len(keys), -1),
         "snap_lam": np.array([snaps_lam[k] for k in keys]).reshape(len(keys), -1),
@@ -120,6 +126,7 @@ def run_case(inst, case, snap_iters):
                              met.mean_pos_violation]),
         "iterations": np.int64(res.iterations), "evals": np.int64(res.evals),
         "converged": np.int64(res.converged),
+        "subopt_final": np.float64(np.nan if met.subopt_abs is None else met.subopt_abs),
     }
     return out, wall
 
@@ -310,6 +317,107 @@ def scaled_fixtures(name, cfg_name, scale, cases, snaps=(1, 2, 5, 10, 20, 50, 10
     save(name, arrays, meta)
 
 
+def restart_option_fixtures():
+    """Round 2: goldens for rows a6 (``warm_tau=True``, engine.py:111-113 via
+    restarts.py:129/:153; mirrors pkg/tests/test_restarts.py:57-65) and a13
+    (``criterion="paper51"`` with ``f_star``, diagnostics.py:254-258, and the
+    ``subopt`` trace column, restarts.py:120).  Instances: the reference's own
+    ``random_qcqp(20, 3, seed=3)`` (arrays in small_qcqp.npz), the analytic
+    suite (arrays in analytic.npz) and C0 (regenerated from the seed)."""
+    arrays, meta = {}, {"cases": {}}
+    small = generate.random_qcqp(20, 3, seed=3)
+    suite = {a.name: a for a in generate.analytic_suite()}
+    c0 = ref_instance(instances.config_instance("C0"))
+
+    # f* for small_qcqp / C0 from tight reference solves (recorded, not assumed)
+    fstars = {}
+    for key, inst in (("small", small), ("c0", c0)):
+        out, wall = run_case(inst, dict(nm=False, policy={"kind": "none"}, budget=50000,
+                                        eps=1e-10), {1})
+        fstars[key] = float(out["metrics"][5])
+        arrays[f"fstar/{key}"] = np.float64(fstars[key])
+        meta["cases"][f"fstar/{key}"] = {"iterations": int(out["iterations"]),
+                                         "converged": int(out["converged"]), "wall_s": wall}
+        print("f*", key, fstars[key], out["iterations"], round(wall, 2), flush=True)
+
+    cases = {
+        # --- warm_tau (a6) ---
+        "ball/warm_fixed30": ("ball", dict(nm=False, policy={"kind": "fixed", "period": 30},
+                                           budget=61, warm_tau=True)),
+        "ball/cold_fixed30": ("ball", dict(nm=False, policy={"kind": "fixed", "period": 30},
+                                           budget=61, warm_tau=False)),
+        "small/warm_nm_fixed40": ("small", dict(nm=True, policy={"kind": "fixed", "period": 40},
+                                                budget=200, warm_tau=True)),
+        "small/warm_mono_fixed40avg": ("small", dict(nm=False, policy={"kind": "fixed", "period": 40,
+                                                                       "point": "average"},
+                                                     budget=200, warm_tau=True)),
+        "small/warm_xy_nm_fixed40": ("small", dict(mode="xy", nm=True,
+                                                   policy={"kind": "fixed", "period": 40},
+                                                   budget=200, warm_tau=True)),
+        "small/warm_nm_ada": ("small", dict(nm=True, policy={"kind": "adaptive", "warmup": 50,
+                                                             "check_period": 100},
+                                            budget=1500, eps=1e-8, warm_tau=True)),
+        "c0/warm_mono_fixed500": ("c0", dict(nm=False, policy={"kind": "fixed", "period": 500},
+                                             budget=50000, eps=1e-6, warm_tau=True)),
+        "c0/warm_mono_ada": ("c0", dict(nm=False, policy={"kind": "adaptive", "xi": 0.04, "q": 0.5,
+                                                          "warmup": 50, "check_period": 200},
+                                        budget=50000, eps=1e-6, warm_tau=True)),
+        # --- paper51 + f_star, and the subopt column under "conic" (a13) ---
+        "small/p51_nm_fixed100": ("small", dict(nm=True, policy={"kind": "fixed", "period": 100},
+                                                budget=20000, eps=1e-6, criterion="paper51",
+                                                f_star="small")),
+        "small/conic_fstar_mono": ("small", dict(nm=False, policy={"kind": "none"},
+                                                 budget=20000, eps=1e-7, f_star="small")),
+        "small/p51_nofstar_mono": ("small", dict(nm=False, policy={"kind": "none"},
+                                                 budget=20000, eps=1e-7, criterion="paper51")),
+        "c0/p51_mono_fixed500": ("c0", dict(nm=False, policy={"kind": "fixed", "period": 500},
+                                            budget=50000, eps=1e-6, criterion="paper51",
+                                            f_star="c0")),
+    }
+    for name in ("ball", "box-lp", "eq-qp", "strongly-convex"):
+        cases[f"{name}/p51_nm_fixed500"] = (name, dict(nm=True, policy={"kind": "fixed", "period": 500},
+                                                       budget=5000, eps=1e-7, criterion="paper51",
+                                                       f_star="analytic"))
+    for key, (which, case) in cases.items():
+        inst = small if which == "small" else c0 if which == "c0" else suite[which].instance
+        run = dict(case)
+        if run.get("f_star") == "analytic":
+            run["f_star"] = float(suite[which].f_star)
+        elif isinstance(run.get("f_star"), str):
+            run["f_star"] = fstars[run["f_star"]]
+        out, wall = run_case(inst, run, set(range(1, 201)))
+        for k, v in out.items():
+            arrays[f"{key}/{k}"] = v
+        meta["cases"][key] = dict(run, instance=which, wall_s=wall)
+        print(key, "iterations", int(out["iterations"]), "conv", int(out["converged"]),
+              round(wall, 2), flush=True)
+    save("restart_opts", arrays, meta)
+
+
+def c1_kkt_fixtures():
+    """Round 2: the bench configuration end to end -- C1 yx monotone +
+    FixedRestart(500) to conic KKT 1e-6 (restarts.py:111-170), plus mono +
+    adaptive, by the real reference on the same seeded arrays."""
+    arr = instances.config_instance("C1")
+    t0 = time.time()
+    inst = ref_instance(arr)
+    print("C1 instance", time.time() - t0, flush=True)
+    arrays = {"Q_checksum": np.array([float(np.sum(arr.Q[i])) for i in range(arr.m + 1)])}
+    meta = {"instance": "instances.config_instance('C1')", "cases": {}}
+    snaps = {1, 2, 5, 10, 50, 100, 200, 300, 400, 499, 500, 501, 502, 510, 550, 560, 570}
+    for key, case in {"mono_fixed500": dict(nm=False, policy={"kind": "fixed", "period": 500},
+                                            budget=3000, eps=1e-6),
+                      "mono_ada": dict(nm=False, policy={"kind": "adaptive", "xi": 0.04, "q": 0.5,
+                                                         "warmup": 50, "check_period": 200},
+                                       budget=3000, eps=1e-6)}.items():
+        out, wall = run_case(inst, case, snaps)
+        for k, v in out.items():
+            arrays[f"{key}/{k}"] = v
+        meta["cases"][key] = dict(case, wall_s=wall)
+        print("C1", key, int(out["iterations"]), int(out["converged"]), wall, flush=True)
+        save("c1_kkt", arrays, meta)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
@@ -318,6 +426,8 @@ if __name__ == "__main__":
     ap.add_argument("--c4", action="store_true")
     ap.add_argument("--c2s", action="store_true")
     ap.add_argument("--kml", action="store_true")
+    ap.add_argument("--restart-opts", action="store_true")
+    ap.add_argument("--c1-kkt", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
         small_fixtures()
@@ -327,6 +437,10 @@ if __name__ == "__main__":
         factored_fixtures()
     if a.c1:
         c1_fixtures()
+    if a.restart_opts:
+        restart_option_fixtures()
+    if a.c1_kkt:
+        c1_kkt_fixtures()
     if a.c4:   # BASELINE C4 at full size (N = 4000, n = 4001): nm and mono, no restart in 200
         scaled_fixtures("c4_200", "C4", None,
                         {"nm": dict(nm=True, policy={"kind": "fixed", "period": 500}, budget=200),
