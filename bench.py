@@ -7,10 +7,16 @@ backtracking (the variant that converges on C1; the non-monotone variant is
 timed on a fixed 1000-iteration budget and reported under ``nonmonotone``).
 
 * ``value``        accepted iterations / s, Q stack resident in HBM.  N ranks
-                   (torchrun): the constraints are sharded over the GPUs and each
-                   trial all-reduces one n-vector and one (m+1)-vector over NCCL
-                   (``scaling: strong``, one solve); ``--replicas`` runs
+                   (torchrun, or ``--gpus N`` which launches torchrun itself):
+                   the constraints are sharded over the GPUs and each trial
+                   sums one n-vector and one (m+1)-vector across ranks with the
+                   library's own rank-ordered NCCL exchange (csrc/comm.cuh;
+                   ``scaling: strong``, one solve); ``--replicas`` runs
                    independent replicas instead (``scaling: weak``).
+                   torch.distributed (gloo) is only the bootstrap / barrier.
+* ``c2``           BASELINE C2 (n=4096, m=512, 69 GB dense / 34.7 GB packed),
+                   generated on the device and sharded over the same N ranks:
+                   it/s, time to KKT and sweep GB/s per GPU (the 6x target's basis).
 * ``ms_per_step``  = time-to-1e-6-KKT of one solve.
 * ``e2e``          the same solve through the public API with the instance on
                    the HOST: pinned H2D of the 6.4 GB Q stack + vectors, solve,
@@ -18,10 +24,12 @@ timed on a fixed 1000-iteration budget and reported under ``nonmonotone``).
 * ``roofline``     the solver kernel: algorithmic Q bytes streamed (sweeps x
                    (m+1) n^2 8 B) / CUDA-event duration of its launches.
 * ``cpu_baseline`` the CPU oracle (numpy restatement of the reference, same
-                   arithmetic and matvec count) on a bounded sample of C1 iterations.
+                   arithmetic and matvec count) solving the same C1 arrays TO KKT
+                   with the same policy (wall-capped), on the host's cores.
 
-``--impl reference`` times that CPU restatement alone (the reference is pure
-Python: nothing is compiled into oracle/_ref).  Inputs (6.4 GB) exceed the
+``--impl reference`` times that CPU restatement alone, to KKT, the timed
+iterations split into K steps (the reference is pure Python: nothing is
+compiled into oracle/_ref).  Inputs (6.4 GB) exceed the
 126 MB L2, so no L2 flush is needed between steps.
 """
 
@@ -57,9 +65,10 @@ def parse():
                     help="force the constraint-sharded (NCCL exchange) path even with one rank")
     ap.add_argument("--p2p", action="store_true",
                     help="sharded runs exchange in-kernel over NVLink peer memory instead of NCCL")
-    ap.add_argument("--cpu-sample-iters", type=int, default=24,
-                    help="accepted C1 iterations per CPU sample (~0.25 s each on 16 cores)")
+    ap.add_argument("--cpu-cap-s", type=float, default=240.0,
+                    help="wall-clock cap of the CPU solve to KKT (reported as not converged beyond it)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--c2-steps", type=int, default=1, help="timed C2 solves (0: no c2 block)")
     return ap.parse_args()
 
 
@@ -153,19 +162,57 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def oracle_sample(arr, iters, warm_iters=1):
-    """CPU oracle: `iters` accepted mono-yx iterations after `warm_iters` (bounded sample)."""
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = os.cpu_count()
+    return {"cpu_model": model, "affinity_cores": aff, "blas_threads": blas_threads(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+class _Cap(Exception):
+    pass
+
+
+def oracle_to_kkt(arr, cap_s, marks=None):
+    """The CPU port (oracle/rapdb_oracle.py, the reference's arithmetic and
+    matvec count) solving `arr` to conic KKT 1e-6 with the bench policy
+    (yx monotone + FixedRestart(500), KKT every 10 iterations), stopped at
+    `cap_s` seconds of wall time.  marks: list receiving (iteration, t)."""
     from oracle import rapdb_oracle as O
     P = O.Problem.from_arrays(arr)
-    opt = O.Options(mode="yx", nonmonotone=False)
-    eng = O.Engine(P, opt, *O.initial_point(P))
-    for _ in range(warm_iters):
-        eng.step()
     t0 = time.perf_counter()
-    for _ in range(iters):
-        eng.step()
+    state = {"it": 0}
+
+    def hook(total, eng):
+        state["it"] = total
+        now = time.perf_counter() - t0
+        if marks is not None:
+            marks.append((total, now))
+        if now > cap_s:
+            raise _Cap()
+
+    converged = False
+    try:
+        res = O.run_restarted(P, O.Options(mode="yx", nonmonotone=False), O.Policy(kind="fixed", period=500),
+                              budget=50_000, criteria=dict(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6),
+                              metrics_every=10, on_iter=hook)
+        converged = bool(res.converged)
+        iters = res.iterations
+    except _Cap:
+        iters = state["it"]
     dt = time.perf_counter() - t0
-    return iters / dt, dt, eng
+    return iters, dt, converged
 
 
 def config_block(arr, name, policy, extra=None):
@@ -187,66 +234,193 @@ def run_reference(args):
         emit({"impl": "reference", "unavailable": "C2's 69 GB dense stack does not fit the CPU reference's host"})
         return
     arr = instances.config_instance(args.config)
-    from oracle import rapdb_oracle as O
-    P = O.Problem.from_arrays(arr)
-    eng = O.Engine(P, O.Options(mode="yx", nonmonotone=False), *O.initial_point(P))
-    eng.step()                      # the first iteration backtracks from tau_bar (excluded)
-    for _ in range(args.warmup):
-        eng.step()
-    per_step = max(1, args.cpu_sample_iters)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for _ in range(per_step):
-            eng.step()
-    dt = time.perf_counter() - t0
-    iters = args.steps * per_step
-    v = iters / dt
-    cores = blas_threads()
-    sample = (f"{args.steps} steps x {per_step} accepted mono-yx iterations of {args.config} "
-              f"(after {1 + args.warmup} warm-up iterations), numpy/OpenBLAS restatement of the reference")
-    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+    marks = []
+    iters, dt, conv = oracle_to_kkt(arr, args.cpu_cap_s, marks)
+    # warm-up = the first W accepted iterations (includes the initial
+    # backtracking from tau_bar); the rest of the solve is split into K steps
+    w = min(max(args.warmup, 0), max(iters - 1, 0))
+    t_w = marks[w - 1][1] if w > 0 else 0.0
+    timed_iters = iters - w
+    timed_s = dt - t_w
+    v = timed_iters / timed_s if timed_s > 0 else None
+    info = host_info()
+    sample = (f"port (oracle/rapdb_oracle.py) solving {args.config} to conic KKT 1e-6, yx monotone + "
+              f"FixedRestart(500): {iters} iterations in {dt:.1f} s ({'converged' if conv else 'wall cap hit'}); "
+              f"the first {w} iterations are the warm-up, the remaining {timed_iters} are timed as "
+              f"{args.steps} steps")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * timed_s / max(args.steps, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded CounterRng, BASELINE config 1 shapes)",
-           "config": config_block(arr, args.config, "yx monotone, per-step sample of accepted iterations"),
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+           "data": "synthetic (seeded CounterRng, BASELINE config shapes)",
+           "config": config_block(arr, args.config, "yx monotone + FixedRestart(500) (rapdb-yx), to KKT"),
+           "time_to_kkt_s": dt if conv else None, "converged": conv, "iterations": iters,
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": info["blas_threads"], "kind": "port",
+                            "sample": sample, **info},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: launch N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_dist(ws, local, need_group):
+    """torch.distributed (gloo) as plumbing only: the NCCL unique-id bootstrap,
+    barriers and the max-over-ranks of the timings.  The data path's
+    exchanges run in the library over its own NCCL communicator."""
+    import torch
+    torch.cuda.set_device(local)
+    if not need_group:
+        return None
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("gloo")
+    return dist
+
+
+class Ranks:
+    def __init__(self, dist, dev):
+        self.dist, self.dev = dist, dev
+
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def reduce(self, v, op):
+        if self.dist is None:
+            return v
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        self.dist.all_reduce(t, op=op(self.dist))
+        return float(t.item())
+
+    def max(self, v):
+        return self.reduce(v, lambda d: d.ReduceOp.MAX)
+
+    def min(self, v):
+        return self.reduce(v, lambda d: d.ReduceOp.MIN)
+
+    def sum(self, v):
+        return self.reduce(v, lambda d: d.ReduceOp.SUM)
+
+
+def timed_solves(R, inst, cfg, pol, crit, dev, shard, ranks, steps, warmup, budget=50_000):
+    """W untimed + K timed solves, CUDA events on the launching stream, max over ranks."""
+    import torch
+
+    def solve():
+        return R.run_restarted(inst, cfg, pol, budget=budget, criteria=crit, metrics_every=10, device=dev,
+                               shard=shard)
+    for _ in range(warmup):
+        solve()
+    ranks.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    results = [solve() for _ in range(steps)]
+    ev1.record()
+    ranks.barrier()
+    return results, ranks.max(ev0.elapsed_time(ev1))
+
+
+def sweep_stats(results):
+    kern_ms = sum(r.device_stats["kernel_ms"] for r in results)
+    sweeps = sum(r.device_stats["sweeps"] for r in results)
+    sweep_ns = sum(r.device_stats["sweep_ns"] for r in results)
+    sweep_bytes = results[-1].device_stats["sweep_bytes"]
+    return kern_ms, sweeps, sweep_ns, sweep_bytes
+
+
+def c2_block(R, args, dev, shard_fn, ranks, ws, peak):
+    """BASELINE C2 sharded over the job's ranks (device-generated stack)."""
+    import torch
+    inst = R.DeviceDenseInstance(4096, 512, 256, seed=0, name="C2 (device-generated)")
+    shard = shard_fn(inst)
+    krange = None if shard is None else (shard.k0, shard.k1)
+    t0 = time.perf_counter()
+    inst.device_data(dev, krange=krange)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    cfg = R.SolverConfig(mode="yx", nonmonotone=False)
+    crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
+    results, t_ms = timed_solves(R, inst, cfg, R.FixedRestart(500), crit, dev, shard, ranks,
+                                 args.c2_steps, 1)
+    kern_ms, sweeps, sweep_ns, sweep_bytes = sweep_stats(results)
+    local_gbs = sweeps * sweep_bytes / (kern_ms / 1e3) / 1e9
+    local_sweep_gbs = sweeps * sweep_bytes / sweep_ns
+    its = results[-1].iterations
+    out = {"workload": "C2: dense convex QCQP n=4096, m=512, B_i rank 256 (device-generated, same "
+                       "distribution as BASELINE config 2), 68.85 GB dense / 34.70 GB packed fp64",
+           "policy": "yx monotone + FixedRestart(500), conic KKT 1e-6",
+           "n_gpus": ws, "shard_range": None if shard is None else [shard.k0, shard.k1],
+           "iters_per_s": its * args.c2_steps / (t_ms / 1e3), "time_to_kkt_ms": t_ms / args.c2_steps,
+           "iterations": its, "evals": results[-1].evals, "converged": bool(results[-1].converged),
+           "final_kkt": results[-1].metrics.kkt_residual,
+           "sweep_bytes_per_gpu_max": ranks.max(sweep_bytes),
+           "kernel_gbs_per_gpu_min": ranks.min(local_gbs),
+           "sweep_phase_gbs_per_gpu_min": ranks.min(local_sweep_gbs),
+           "roofline_frac_min": ranks.min(local_gbs) / peak,
+           "sweep_phase_frac_min": ranks.min(local_sweep_gbs) / peak,
+           "generate_s": gen_s, "steps": args.c2_steps, "warmup": 1}
+    inst.drop_device_data()
+    return out
+
+
 def main():
     args = parse()
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     _claim_stdout()
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
-    ws, rank, local = dist_env()
+    if torch.cuda.device_count() < max(ws, 1) and ws > 1:
+        raise SystemExit(f"{ws} ranks need {ws} GPUs, {torch.cuda.device_count()} visible")
     sharded = (ws > 1 and not args.replicas) or args.shard
-    os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
-    if ws > 1 or args.shard:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        if not dist.is_initialized():
-            if ws == 1:
-                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                os.environ.setdefault("MASTER_PORT", "29511")
-                os.environ.setdefault("RANK", "0")
-                os.environ.setdefault("WORLD_SIZE", "1")
-            dist.init_process_group("nccl")
-    else:
-        dist = None
-        torch.cuda.set_device(0)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")        # communicator lines go to stderr (_claim_stdout)
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist = init_dist(ws, local, ws > 1 or args.shard)
     dev = torch.device("cuda", torch.cuda.current_device())
+    ranks = Ranks(dist, dev)
 
     import paper_2605_29291_b200 as R
     from paper_2605_29291_b200 import _capi, instances
     from paper_2605_29291_b200.sharding import nccl_shard
 
+    def shard_fn(inst):
+        if not sharded:
+            return None
+        sh = nccl_shard(inst, device_index=dev.index)
+        sh.force_split = True
+        sh.p2p = bool(args.p2p)
+        return sh
+
     device_generated = args.config == "C2"
     if device_generated:
-        # the C2 host instance needs ~69 GB of host RAM and minutes of BLAS:
-        # generate and pack the stack on the device (same distribution)
         inst = R.DeviceDenseInstance(4096, 512, 256, seed=0, name="C2 (device-generated)")
         arr = inst
     else:
@@ -255,69 +429,28 @@ def main():
     cfg = R.SolverConfig(mode="yx", nonmonotone=False)
     pol = R.FixedRestart(500)
     crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
-    shard = None
-    if sharded:
-        shard = nccl_shard(inst)
-        shard.force_split = True
-        shard.p2p = bool(args.p2p)
+    shard = shard_fn(inst)
     krange = None if shard is None else (shard.k0, shard.k1)
-
-    def solve(c=cfg, budget=50_000, criteria=crit):
-        return R.run_restarted(inst, c, pol, budget=budget, criteria=criteria, metrics_every=10, device=dev,
-                               shard=shard)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
     inst.device_data(dev, krange=krange)
-    for _ in range(args.warmup):
-        solve()
+    peak, peak_src = measured_peak()
 
     # ---- device-resident timed region -----------------------------------
     clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
     launches0 = _capi.launch_count()
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    results = [solve() for _ in range(args.steps)]
-    ev1.record()
-    barrier()
-    launches = _capi.launch_count() - launches0
+    clocks.start()
+    results, t_ms = timed_solves(R, inst, cfg, pol, crit, dev, shard, ranks, args.steps, args.warmup)
     clk = clocks.stop()
-    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    launches = _capi.launch_count() - launches0
     iters_local = sum(r.iterations for r in results)
     # sharded: every rank runs the same solve (strong scaling); replicas: sum
-    iters_all = iters_local if sharded else sum_over_ranks(iters_local)
+    iters_all = iters_local if sharded else ranks.sum(iters_local)
     value = iters_all / (t_ms / 1e3)
     conv = all(r.converged for r in results)
-    st = results[-1].device_stats
-    sweep_bytes = st["sweep_bytes"]
+    kern_ms, sweeps, sweep_ns, sweep_bytes = sweep_stats(results)
     layout = os.environ.get("RAPDB_LAYOUT", "packed")
     dense_bytes = (arr.m + 1 if shard is None else shard.k1 - shard.k0) * arr.n * arr.n * 8
-    kern_ms = sum(r.device_stats["kernel_ms"] for r in results)
-    sweeps = sum(r.device_stats["sweeps"] for r in results)
-    sweep_ns = sum(r.device_stats["sweep_ns"] for r in results)
     achieved = sweeps * sweep_bytes / (kern_ms / 1e3) / 1e9
     sweep_phase_gbs = sweeps * sweep_bytes / sweep_ns
-    peak, peak_src = measured_peak()
 
     # standalone sweep launch (one kernel launch = one fused sweep), CUDA events
     probe_ms = None
@@ -328,10 +461,10 @@ def main():
         _, _, probe_ms = ev.ctx.probe_sweep(xprobe, reps=10)
 
     # ---- e2e through the public API with host-resident inputs -----------
+    e2e_block = None
     if device_generated:
         e2e_block = {"unavailable": "device-generated instance: its inputs never exist on the host"}
     else:
-        e2e_block = None
         inst.pin_host()
         inst.drop_device_data()
     torch.cuda.synchronize()
@@ -347,37 +480,47 @@ def main():
     e2e_iters, e2e_s, d2h = 0, 0.0, 0
     for _ in range(0 if device_generated else args.steps):
         inst.drop_device_data()
-        barrier()
+        ranks.barrier()
         t0 = time.perf_counter()
-        r = solve()
-        sol = (r.solution.x, r.average.x)
-        barrier()
+        r = R.run_restarted(inst, cfg, pol, budget=50_000, criteria=crit, metrics_every=10, device=dev,
+                            shard=shard)
+        sol = (r.solution.x, r.average.x)     # noqa: F841 -- the D2H reads are part of the call
+        ranks.barrier()
         e2e_s += time.perf_counter() - t0
         e2e_iters += r.iterations
-        d2h = (2 * (arr.n + arr.m + arr.p) * 8 + r.device_stats["run_launches"] * 0
-               + r.iterations * 11 * 8 + 8 * 8)
-    e2e_s = max_over_ranks(e2e_s)
-    e2e_value = (e2e_iters if sharded else sum_over_ranks(e2e_iters)) / e2e_s if e2e_s > 0 else None
+        # solution + average (x, v, lam), the trace rows and the metrics
+        d2h = 2 * (arr.n + arr.m + arr.p) * 8 + r.iterations * 11 * 8 + 8 * 8
+    e2e_s = ranks.max(e2e_s)
+    e2e_value = (e2e_iters if sharded else ranks.sum(e2e_iters)) / e2e_s if e2e_s > 0 else None
 
     # non-monotone variant: fixed 1000-iteration budget (it/s only)
     inst.device_data(dev, krange=krange)
     nm_cfg = R.SolverConfig(mode="yx", nonmonotone=True)
-    torch.cuda.synchronize()
+    ranks.barrier()
     tn = time.perf_counter()
-    rnm = solve(c=nm_cfg, budget=1000)
-    torch.cuda.synchronize()
-    tn = time.perf_counter() - tn
+    rnm = R.run_restarted(inst, nm_cfg, pol, budget=1000, criteria=crit, metrics_every=10, device=dev,
+                          shard=shard)
+    ranks.barrier()
+    tn = ranks.max(time.perf_counter() - tn)
+    if not device_generated:
+        inst.drop_device_data()
 
-    out = None
+    c2 = None
+    if args.c2_steps > 0 and not device_generated:
+        c2 = c2_block(R, args, dev, shard_fn, ranks, ws, peak)
+
     if rank == 0:
         cpu = None
         if not args.skip_cpu and ws == 1 and not device_generated:
-            v_cpu, dt_cpu, _ = oracle_sample(arr, args.cpu_sample_iters)
-            cpu = {"value": v_cpu, "unit": UNIT, "cores": blas_threads(), "kind": "port",
-                   "sample": f"{args.cpu_sample_iters} accepted mono-yx iterations of C1 after the first "
-                             f"(backtracking) iteration, numpy/OpenBLAS restatement of the reference "
-                             f"(oracle/rapdb_oracle.py), {dt_cpu:.1f} s",
-                   "extrapolated_time_to_kkt_s": results[-1].iterations / v_cpu}
+            iters_c, dt_c, conv_c = oracle_to_kkt(arr, args.cpu_cap_s)
+            info = host_info()
+            cpu = {"value": iters_c / dt_c, "unit": UNIT, "cores": info["blas_threads"], "kind": "port",
+                   "sample": (f"port (oracle/rapdb_oracle.py: the reference's arithmetic and matvec count) "
+                              f"solving the same {args.config} arrays to conic KKT 1e-6 with the same policy: "
+                              f"{iters_c} iterations in {dt_c:.1f} s"
+                              + ("" if conv_c else f" (wall cap {args.cpu_cap_s:.0f} s hit, not converged)")),
+                   "time_to_kkt_s": dt_c if conv_c else None, "converged": conv_c, "iterations": iters_c,
+                   **info}
         prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
         traffic = None
         if os.path.exists(prof):
@@ -392,7 +535,8 @@ def main():
             "data": ("synthetic (device-generated, BASELINE config 2 shapes and distribution)" if device_generated
                      else f"synthetic (seeded CounterRng, BASELINE {args.config} shapes; random instance, no dataset)"),
             "config": config_block(arr, args.config, "yx monotone + FixedRestart(500) (rapdb-yx)",
-                                   {"parallelism": (f"constraint-sharded over {ws} GPU(s), NCCL all-reduce per trial"
+                                   {"parallelism": (f"constraint-sharded over {ws} GPU(s), rank-ordered NCCL "
+                                                    f"exchange per trial (library-owned communicator)"
                                                     if sharded else ("replicas only" if ws > 1 else "single GPU")),
                                     "shard_range": None if shard is None else [shard.k0, shard.k1],
                                     "iterations_per_solve": results[-1].iterations,
@@ -422,6 +566,7 @@ def main():
                                  "d2h_bytes_per_step": int(d2h), "time_to_kkt_ms": 1e3 * e2e_s / args.steps},
             "nonmonotone": {"iters_per_s": rnm.iterations / tn, "iterations": rnm.iterations,
                             "evals": rnm.evals, "budget": 1000, "final_kkt": rnm.metrics.kkt_residual},
+            "c2": c2,
             "gpu_launches": int(launches),
             "clocks": clk,
         }

@@ -100,6 +100,24 @@ int rapdb_exchange_buffers(rapdb_ctx* ctx, int kind, double** buf0, long long* c
 /* number of exchanges performed by this context so far */
 long long rapdb_exchange_count(const rapdb_ctx* ctx);
 
+/* Native exchange over NCCL (the default of the Python binding's
+ * nccl_shard): one communicator per process and GPU, bootstrapped from a
+ * 128-byte ncclUniqueId that rank 0 creates and the caller distributes.  A
+ * context given a communicator sums its exchange buffers itself, on its
+ * stream, without calling back into the host: NCCL only moves bytes
+ * (all-gather, or send/recv + all-gather for long buffers) and a kernel of
+ * this library adds the R partials in rank order, so every rank -- and the
+ * emulated / peer-memory paths -- gets the same bits whatever algorithm NCCL
+ * picks (fixed reduction order).                               */
+typedef struct rapdb_comm rapdb_comm;
+int rapdb_comm_unique_id(unsigned char* id128);
+int rapdb_comm_create(int device, const unsigned char* id128, int rank, int nranks, rapdb_comm** out);
+void rapdb_comm_destroy(rapdb_comm* comm);
+/* rank-ordered in-place all-reduce of a device buffer (synchronises stream) */
+int rapdb_comm_allreduce_ordered(rapdb_comm* comm, double* buf, long long count, void* stream);
+/* use `comm` for this context's exchanges (replaces rapdb_set_exchange)     */
+int rapdb_set_comm_exchange(rapdb_ctx* ctx, rapdb_comm* comm, int force_split);
+
 /* In-kernel exchange over NVLink peer memory (dense shards; opt-in): each
  * rank allocates a zeroed device region of rapdb_peer_region_bytes(ctx)
  * bytes (rapdb_region_alloc), shares it with the other ranks (CUDA IPC handles:

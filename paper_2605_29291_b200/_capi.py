@@ -50,7 +50,8 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_dense_packed", "rapdb_packed_doubles", "rapdb_pack_symmetric",
            "rapdb_bind_factored_range", "rapdb_egm", "rapdb_peer_region_bytes", "rapdb_ipc_handle",
            "rapdb_ipc_open", "rapdb_ipc_close", "rapdb_set_peer_exchange", "rapdb_region_alloc",
-           "rapdb_region_free"]
+           "rapdb_region_free", "rapdb_comm_unique_id", "rapdb_comm_create", "rapdb_comm_destroy",
+           "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
@@ -118,6 +119,49 @@ class PeerRegion:
             pass
 
 
+def comm_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for rapdb_comm_create."""
+    buf = C.create_string_buffer(128)
+    if load().rapdb_comm_unique_id(buf) != 0:
+        raise DeviceError("ncclGetUniqueId failed")
+    return buf.raw
+
+
+class Comm:
+    """Native NCCL communicator (rapdb_comm): the library's rank-ordered
+    exchange for sharded contexts.  Collective: every rank constructs it with
+    the same unique id."""
+
+    def __init__(self, device_index: int, unique_id: bytes, rank: int, nranks: int):
+        if len(unique_id) != 128:
+            raise InputError("an ncclUniqueId is 128 bytes")
+        self.lib = load()
+        self.rank, self.nranks, self.device_index = rank, nranks, device_index
+        h = C.c_void_p()
+        if self.lib.rapdb_comm_create(int(device_index), unique_id, int(rank), int(nranks), C.byref(h)) != 0:
+            raise DeviceError(f"ncclCommInitRank failed (rank {rank} of {nranks})")
+        self.h = h
+
+    def allreduce_ordered(self, t, stream_ptr: int = 0):
+        """In-place rank-ordered sum of a contiguous float64 CUDA tensor."""
+        if t.dtype.itemsize != 8 or not t.is_contiguous() or not t.is_cuda:
+            raise InputError("need a contiguous float64 CUDA tensor")
+        if self.lib.rapdb_comm_allreduce_ordered(self.h, C.c_void_p(t.data_ptr()), t.numel(),
+                                                 C.c_void_p(stream_ptr)) != 0:
+            raise DeviceError("rank-ordered all-reduce failed")
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.rapdb_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter shutdown
+            pass
+
+
 def load(path: str = LIB_PATH):
     """Open the native library (raises DeviceError when it is absent)."""
     global _lib
@@ -168,6 +212,12 @@ def load(path: str = LIB_PATH):
     lib.rapdb_region_free.argtypes = [P]
     lib.rapdb_set_peer_exchange.argtypes = [P, C.POINTER(P)]
     lib.rapdb_grad_x.argtypes = [P, P, P, P, P, P]
+    lib.rapdb_comm_unique_id.argtypes = [C.c_char_p]
+    lib.rapdb_comm_create.argtypes = [I, C.c_char_p, I, I, C.POINTER(P)]
+    lib.rapdb_comm_destroy.argtypes = [P]
+    lib.rapdb_comm_destroy.restype = None
+    lib.rapdb_comm_allreduce_ordered.argtypes = [P, P, LL, P]
+    lib.rapdb_set_comm_exchange.argtypes = [P, P, I]
     _lib = lib
     return lib
 
@@ -238,6 +288,11 @@ class Context:
                 return 1
         self._cb = EXCHANGE_FN(_cb)      # keep the thunk alive
         self._check(self.lib.rapdb_set_exchange(self.h, self._cb, None, 1 if force_split else 0))
+
+    def set_comm_exchange(self, comm: "Comm", force_split=False):
+        """Exchanges summed by the library itself over `comm` (no host callback)."""
+        self._comm = comm      # keep the communicator alive with the context
+        self._check(self.lib.rapdb_set_comm_exchange(self.h, comm.h, 1 if force_split else 0))
 
     def exchange_views(self, kind):
         """float64 views into the workspace of the buffer(s) to all-reduce."""

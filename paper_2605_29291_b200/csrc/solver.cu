@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "egm.cuh"
 #include "gap.cuh"
 #include "rapdb_b200.h"
@@ -374,8 +375,17 @@ struct rapdb_ctx {
   void* d_px = nullptr;     // device tables of the peer region pointers
   rapdb_exchange_fn xcb = nullptr;
   void* xuser = nullptr;
+  rapdb_comm* comm = nullptr;        // native rank-ordered NCCL exchange (instead of xcb)
+  rcomm::Scratch xscratch;      // its gather / reduce-scatter scratch
   long long exchanges = 0;
   SolverState last_st{};
+};
+
+// One NCCL communicator per process and device, shared by every context of
+// a sharded run (comm.cuh: rank-ordered sums, NCCL moves bytes only).
+struct rapdb_comm {
+  ncclComm_t nccl = nullptr;
+  int device = 0, rank = 0, nranks = 1;
 };
 
 namespace {
@@ -552,6 +562,26 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   return RAPDB_OK;
 }
 
+// The buffers of exchange `kind` summed across ranks in rank order on the
+// context's stream (no host synchronisation: the relaunch queues behind it).
+int comm_exchange(rapdb_ctx* c, int kind) {
+  double *b0 = nullptr, *b1 = nullptr;
+  long long n0 = 0, n1 = 0;
+  int r = rapdb_exchange_buffers(c, kind, &b0, &n0, &b1, &n1);
+  if (r) return r;
+  const rapdb_comm* m = c->comm;
+  const char* what = "";
+  for (int v = 0; v < 2; ++v) {
+    double* b = v ? b1 : b0;
+    const long long n = v ? n1 : n0;
+    if (!b || n <= 0) continue;
+    const int e = rcomm::ordered_allreduce(m->nccl, m->rank, m->nranks, b, n, c->xscratch, c->stream,
+                                                c->nsm, &what);
+    if (e) return fail(c, RAPDB_EDEVICE, std::string("rank-ordered exchange: ") + what);
+  }
+  return RAPDB_OK;
+}
+
 // Launch an op.  Single-rank contexts run it to completion in one launch
 // (asynchronous).  Sharded contexts ("split") stop at every exchange point:
 // the registered callback all-reduces the buffer rapdb_exchange_buffers names
@@ -573,8 +603,13 @@ int launch(rapdb_ctx* c, RunCfg rc) {
       if (r) return r;
     }
     if (c->split && c->last_st.xkind != X_NONE) {
-      if (!c->xcb) return fail(c, RAPDB_ECONFIG, "sharded context has no exchange callback");
-      if (c->xcb(c->xuser, c->last_st.xkind) != 0) return fail(c, RAPDB_EDEVICE, "exchange callback failed");
+      if (c->comm) {
+        r = comm_exchange(c, c->last_st.xkind);
+        if (r) return r;
+      } else {
+        if (!c->xcb) return fail(c, RAPDB_ECONFIG, "sharded context has no exchange callback");
+        if (c->xcb(c->xuser, c->last_st.xkind) != 0) return fail(c, RAPDB_EDEVICE, "exchange callback failed");
+      }
       ++c->exchanges;
     }
     rc.resume = 1;
@@ -694,6 +729,62 @@ int rapdb_exchange_buffers(rapdb_ctx* c, int kind, double** b0, long long* n0, d
 }
 
 long long rapdb_exchange_count(const rapdb_ctx* c) { return c ? c->exchanges : -1; }
+
+int rapdb_comm_unique_id(unsigned char* id128) {
+  if (!id128) return RAPDB_EINPUT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RAPDB_EDEVICE;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, &id, sizeof(id));
+  return RAPDB_OK;
+}
+
+int rapdb_comm_create(int device, const unsigned char* id128, int rank, int nranks, rapdb_comm** out) {
+  if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) return RAPDB_EINPUT;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return RAPDB_EDEVICE;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  rapdb_comm* m = new rapdb_comm();
+  m->device = device;
+  m->rank = rank;
+  m->nranks = nranks;
+  if (ncclCommInitRank(&m->nccl, nranks, id, rank) != ncclSuccess) {
+    delete m;
+    return RAPDB_EDEVICE;
+  }
+  *out = m;
+  return RAPDB_OK;
+}
+
+void rapdb_comm_destroy(rapdb_comm* m) {
+  if (!m) return;
+  if (m->nccl) ncclCommDestroy(m->nccl);
+  delete m;
+}
+
+int rapdb_comm_allreduce_ordered(rapdb_comm* m, double* buf, long long count, void* stream) {
+  if (!m || (!buf && count > 0) || count < 0) return RAPDB_EINPUT;
+  rcomm::Scratch sc;
+  const char* what = "";
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rcomm::ordered_allreduce(m->nccl, m->rank, m->nranks, buf, count, sc, s, nsm, &what)) return RAPDB_EDEVICE;
+  // the scratch is freed on return: finish the queued work first
+  return cudaStreamSynchronize(s) == cudaSuccess ? RAPDB_OK : RAPDB_EDEVICE;
+}
+
+int rapdb_set_comm_exchange(rapdb_ctx* c, rapdb_comm* m, int force_split) {
+  if (!c || !m) return RAPDB_EINPUT;
+  if (m->nranks != c->nranks || m->rank != c->rank)
+    return fail(c, RAPDB_ECONFIG, "communicator rank/size differ from the context's");
+  if (m->device != c->device) return fail(c, RAPDB_ECONFIG, "communicator is on another device");
+  c->comm = m;
+  c->xcb = nullptr;
+  c->split = (c->nranks > 1 || force_split) ? 1 : 0;
+  return RAPDB_OK;
+}
 
 // ---- in-kernel peer exchange (sharded dense contexts) ---------------------
 namespace {

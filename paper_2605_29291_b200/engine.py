@@ -120,7 +120,10 @@ class ApdbEngine:
         else:
             self._ctx = _capi.Context(idx, shard.rank, shard.nranks)
             ctx = self._ctx
-            ctx.set_exchange(lambda kind: shard.exchange(ctx.exchange_views(kind)), force_split=shard.split)
+            if getattr(shard, "comm", None) is not None:     # native rank-ordered NCCL exchange
+                ctx.set_comm_exchange(shard.comm, force_split=shard.split)
+            else:
+                ctx.set_exchange(lambda kind: shard.exchange(ctx.exchange_views(kind)), force_split=shard.split)
             if getattr(shard, "l0", None) is not None:
                 self._data = inst.device_data(ctx.device, krange=(shard.k0, shard.k1), lrange=(shard.l0, shard.l1))
             else:

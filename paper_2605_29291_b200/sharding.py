@@ -9,8 +9,17 @@ identically on every rank, so the host control flow stays in lockstep without
 further communication.  The smoothed gap adds one exchange of H (n x n) per
 adaptive check.
 
-* ``nccl_shard(inst)``: the production path -- one process per GPU,
-  ``torch.distributed`` with the NCCL backend, all-reduces over NVLink/NVSwitch.
+* ``nccl_shard(inst)``: the production path -- one process per GPU; the
+  library owns an NCCL communicator (``_capi.Comm``, bootstrapped once per
+  process from a unique id that rank 0 broadcasts over ``torch.distributed``)
+  and sums every exchange itself, rank-ordered (csrc/comm.cuh), without a
+  host callback: NCCL moves the bytes over NVLink/NVSwitch, the sum order is
+  fixed, so every rank and every algorithm NCCL picks give the
+  same bits.
+* ``group_shard(inst, group)``: the same rank-ordered exchange through a
+  ``torch.distributed`` group at the host (any backend, e.g. gloo): used to
+  run real multi-process shards where NCCL cannot (several ranks on one GPU:
+  the kernels stop at every exchange point, so they never wait on each other).
 * ``EmulatedCluster``: R shards of one instance on ONE GPU, driven by R host
   threads that meet at each exchange (the kernels never wait on each other:
   each launch ends at the exchange point).  Used by the tests.
@@ -38,6 +47,7 @@ class Shard:
     l1: Optional[int] = None
     p2p: bool = False             # dense: exchange in-kernel over NVLink peer memory (opt-in)
     group: object = None          # torch.distributed group for the peer-region handshake
+    comm: object = None           # _capi.Comm: native rank-ordered NCCL exchange (no host callback)
     _peer: object = None          # [(region, opened peer pointers)] kept alive by the shard
 
     def attach_peer_exchange(self, ctx):
@@ -101,19 +111,72 @@ def shard_ranges(inst, nranks: int):
     return [(k0, k1, None, None) for k0, k1 in plan(inst.m, nranks, inst.zero_flags().astype(bool))]
 
 
-def nccl_shard(inst, group=None) -> Shard:
-    """This process's shard for the current torch.distributed (NCCL) group."""
+_COMMS = {}
+
+
+def native_comm(group=None, device_index: Optional[int] = None):
+    """The process's native NCCL communicator for a torch.distributed group
+    (created once, collectively: rank 0 makes the unique id and broadcasts it
+    over the group -- bootstrap only, no solver data goes through torch)."""
+    import torch
+    import torch.distributed as dist
+    from . import _capi
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = torch.cuda.current_device() if device_index is None else int(device_index)
+    key = (id(group), world, rank, dev)
+    if key not in _COMMS:
+        box = [_capi.comm_unique_id() if rank == 0 else None]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(box, src=src, group=group)
+        _COMMS[key] = _capi.Comm(dev, box[0], rank, world)
+    return _COMMS[key]
+
+
+def nccl_shard(inst, group=None, device_index: Optional[int] = None) -> Shard:
+    """This process's shard for the current torch.distributed group, with the
+    library's own rank-ordered NCCL exchange."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     k0, k1, l0, l1 = shard_ranges(inst, world)[rank]
+    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, name="nccl", l0=l0, l1=l1, group=group,
+                 comm=native_comm(group, device_index))
 
-    def allreduce(views):
-        for v in views:
-            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
 
-    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, exchange=allreduce, name="nccl", l0=l0, l1=l1,
-                 group=group)
+def ordered_allreduce_host(views, group=None):
+    """Rank-ordered in-place sum of tensors across a torch.distributed group
+    (any backend): all-gather the R contributions, then add them as
+    ((p_0 + p_1) + p_2) + ... -- the association csrc/comm.cuh, the emulated
+    cluster and the in-kernel peer exchange use.  CUDA tensors are staged
+    through the host when the backend is gloo."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world == 1:
+        return
+    host = dist.get_backend(group) == "gloo"
+    for v in views:
+        src = v.detach().to("cpu") if host and v.is_cuda else v.detach()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src.contiguous(), group=group)
+        tot = parts[0].clone()
+        for r in range(1, world):
+            tot += parts[r]
+        v.copy_(tot)
+    if any(v.is_cuda for v in views):
+        torch.cuda.synchronize()
+
+
+def group_shard(inst, group=None) -> Shard:
+    """This process's shard, exchanging through ``ordered_allreduce_host``
+    over a torch.distributed group (multi-process runs on one GPU, gloo)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    k0, k1, l0, l1 = shard_ranges(inst, world)[rank]
+    return Shard(rank=rank, nranks=world, k0=k0, k1=k1, name="group", l0=l0, l1=l1, group=group,
+                 exchange=lambda views: ordered_allreduce_host(views, group), force_split=True)
 
 
 class EmulatedCluster:

@@ -5,8 +5,10 @@
 * R emulated shards (one context per shard, host threads meeting at each
   exchange, rank-ordered sums) must reproduce the reference's accepted step
   sizes and iterates like the unsharded path.
-The multi-process NCCL transport itself is exercised by tests/test_sharding_gloo.py
-(the same exchange protocol over torch.distributed, gloo on CPU).
+The library's own NCCL communicator runs at world size 1 (one GPU per box),
+and two real processes share the GPU with a gloo rank-ordered exchange
+(bottom of this file); tests/test_sharding_gloo.py runs the exchange
+(sharding.ordered_allreduce_host) over gloo on CPU at world size 2-3.
 """
 
 import numpy as np
@@ -160,3 +162,123 @@ def test_peer_exchange_single_rank_is_bitwise_identical(mode, policy):
     np.testing.assert_array_equal(trace_arr(peer.trace)[:, :7], trace_arr(fused.trace)[:, :7])
     np.testing.assert_array_equal(peer.solution.x, fused.solution.x)
     np.testing.assert_array_equal(peer.solution.lam, fused.solution.lam)
+
+
+# --------------------------------------------------------------------------
+# The library's own NCCL communicator (csrc/comm.cuh) and real multi-process
+# shards.  Only one GPU is available per test box: NCCL refuses two ranks on
+# one device, so the native communicator runs at world size 1 here (split
+# mode, every exchange through rapdb_comm: bitwise identity with the fused
+# run), and the multi-process path runs its exchanges through a gloo group
+# (sharding.group_shard) -- the kernels stop at each exchange point, so the
+# processes never spin on each other on the shared GPU.
+
+
+def _native_comm():
+    from paper_2605_29291_b200 import _capi
+    return _capi.Comm(0, _capi.comm_unique_id(), 0, 1)
+
+
+@pytest.mark.parametrize("mode,policy", [("yx", "fixed"), ("xy", "fixed"), ("yx", "adaptive")])
+def test_native_comm_single_rank_is_bitwise_identical(mode, policy):
+    arr = instances.dense_qcqp(150, 9, 12, seed=4)
+    inst = R.ProblemInstance.from_arrays(arr, validate=False)
+    pol = R.FixedRestart(40) if policy == "fixed" else R.AdaptiveRestart(warmup=30, check_period=60)
+    fused = _solve(inst, None, mode, True, pol, 300, 1e-9)
+    shard = Shard(rank=0, nranks=1, k0=0, k1=arr.m + 1, force_split=True, comm=_native_comm(), name="nccl")
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode=mode, nonmonotone=True), R.initial_iterate(inst), shard=shard)
+    eng.run_block(5)
+    assert eng._ctx.exchange_count() > 0, "split mode never reached the native exchange"
+    split = _solve(inst, shard, mode, True, pol, 300, 1e-9)
+    np.testing.assert_array_equal(trace_arr(split.trace)[:, :7], trace_arr(fused.trace)[:, :7])
+    np.testing.assert_array_equal(split.solution.x, fused.solution.x)
+    np.testing.assert_array_equal(split.solution.lam, fused.solution.lam)
+
+
+def test_native_comm_factored_single_rank():
+    from conftest import FACTORED_SMALL
+    from paper_2605_29291_b200.factored import FactoredInstance
+    arr = instances.factored_qcqp(**FACTORED_SMALL)
+    inst = FactoredInstance.from_arrays(arr)
+    cfg = R.SolverConfig(mode="yx", nonmonotone=True)
+    ref = R.ApdbEngine(inst, cfg, R.initial_iterate(inst))
+    ref.run_block(60)
+    k0, k1, l0, l1 = inst.shard_ranges(1)[0]
+    shard = Shard(rank=0, nranks=1, k0=k0, k1=k1, l0=l0, l1=l1, force_split=True, comm=_native_comm())
+    eng = R.ApdbEngine(inst, cfg, R.initial_iterate(inst), shard=shard)
+    eng.run_block(60)
+    np.testing.assert_array_equal(trace_arr(eng.trace)[:, :7], trace_arr(ref.trace)[:, :7])
+    np.testing.assert_array_equal(eng.last.x, ref.last.x)
+
+
+def test_native_comm_allreduce_world_one_is_identity():
+    import torch
+    comm = _native_comm()
+    for n in (7, 3 << 20):        # the all-gather and the send/recv + all-gather paths
+        t = torch.randn(n, dtype=torch.float64, device="cuda")
+        before = t.clone()
+        comm.allreduce_ordered(t, torch.cuda.current_stream().cuda_stream)
+        assert torch.equal(t, before)
+
+
+def _group_worker(rank, world, port, out, kind):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2605_29291_b200.sharding import group_shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        if kind == "dense":
+            arr = instances.dense_qcqp(150, 9, 12, seed=4)
+            inst = R.ProblemInstance.from_arrays(arr, validate=False)
+            cfg = R.SolverConfig(mode="yx", nonmonotone=True)
+            pol = R.FixedRestart(40)
+        else:
+            from conftest import FACTORED_SMALL
+            from paper_2605_29291_b200.factored import FactoredInstance
+            inst = FactoredInstance.from_arrays(instances.factored_qcqp(**FACTORED_SMALL))
+            cfg = R.SolverConfig(mode="yx", nonmonotone=False)
+            pol = R.FixedRestart(50)
+        res = R.run_restarted(inst, cfg, pol, budget=150, criteria=crit(1e-9), shard=group_shard(inst))
+        np.save(os.path.join(out, f"{kind}{rank}_trace.npy"), trace_arr(res.trace)[:, :7])
+        np.save(os.path.join(out, f"{kind}{rank}_x.npy"), res.solution.x)
+        np.save(os.path.join(out, f"{kind}{rank}_lam.npy"), res.solution.lam)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["dense", "factored"])
+def test_two_processes_one_gpu_group_exchange(tmp_path, kind):
+    """Two real processes, each binding its own constraint shard on the GPU and
+    running run_restarted(shard=group_shard(...)) with a rank-ordered gloo
+    exchange: both ranks agree bit for bit with each other and with the
+    emulated 2-rank cluster (the same rank-ordered sums), and the accepted
+    step sizes equal the unsharded run's."""
+    import torch.multiprocessing as mp
+    from test_sharding_gloo import _free_port
+    world = 2
+    mp.spawn(_group_worker, args=(world, _free_port(), str(tmp_path), kind), nprocs=world, join=True)
+    if kind == "dense":
+        arr = instances.dense_qcqp(150, 9, 12, seed=4)
+        inst = R.ProblemInstance.from_arrays(arr, validate=False)
+        cfg, pol = R.SolverConfig(mode="yx", nonmonotone=True), R.FixedRestart(40)
+    else:
+        from conftest import FACTORED_SMALL
+        from paper_2605_29291_b200.factored import FactoredInstance
+        inst = FactoredInstance.from_arrays(instances.factored_qcqp(**FACTORED_SMALL))
+        cfg, pol = R.SolverConfig(mode="yx", nonmonotone=False), R.FixedRestart(50)
+    fused = R.run_restarted(inst, cfg, pol, budget=150, criteria=crit(1e-9))
+    emu = EmulatedCluster(world).run(
+        inst, lambda sh: R.run_restarted(inst, cfg, pol, budget=150, criteria=crit(1e-9), shard=sh))
+    for r in range(world):
+        tr = np.load(tmp_path / f"{kind}{r}_trace.npy")
+        x = np.load(tmp_path / f"{kind}{r}_x.npy")
+        lam = np.load(tmp_path / f"{kind}{r}_lam.npy")
+        np.testing.assert_array_equal(tr[:, TAU], trace_arr(fused.trace)[:, TAU])
+        np.testing.assert_array_equal(tr, trace_arr(emu[r].trace)[:, :7])
+        np.testing.assert_array_equal(x, emu[r].solution.x)
+        np.testing.assert_array_equal(lam, emu[r].solution.lam)
+        assert rel(x, fused.solution.x) <= 1e-12

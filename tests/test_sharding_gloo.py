@@ -19,7 +19,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2605_29291_b200 import instances
-from paper_2605_29291_b200.sharding import plan
+from paper_2605_29291_b200.sharding import ordered_allreduce_host, plan
 
 
 def test_plan_balanced_and_contiguous():
@@ -123,9 +123,9 @@ def _worker(rank, world, port, iters, nm, out):
         arr = instances.dense_qcqp(40, 6, 5, seed=9)
         k0, k1 = plan(arr.m, world)[rank]
 
-        def allreduce(v):
-            t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        def allreduce(v):     # the product's rank-ordered exchange (sharding.py)
+            t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64).copy())
+            ordered_allreduce_host([t])
             return t.numpy().copy()
 
         taus, x = _sharded_run(arr, k0, k1, allreduce, iters, nm)
@@ -151,3 +151,36 @@ def test_sharded_decomposition_gloo(tmp_path, world, nm):
         np.testing.assert_array_equal(np.load(tmp_path / f"rank{r}_taus.npy"), ref_taus)
         np.testing.assert_array_equal(xs[r], xs[0])            # replicas agree bit for bit
     assert np.linalg.norm(xs[0] - eng.x) <= 1e-12 * np.linalg.norm(eng.x)
+
+
+def _ordered_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # contributions whose sum depends on the association: rank-ordered
+        # ((p0 + p1) + p2) gives 1e16 in slot 0 (1e16 + 1 rounds back to
+        # 1e16 twice), p0 + (p1 + p2) gives 1e16 + 2
+        vals = {0: [1e16, 0.1, 3.0], 1: [1.0, 0.2, -1.0], 2: [1.0, 0.3, 2.0 ** -60]}[rank]
+        t = torch.tensor(vals, dtype=torch.float64)
+        t2 = torch.full((5,), float(rank + 1), dtype=torch.float64)
+        ordered_allreduce_host([t, t2])
+        np.save(os.path.join(out, f"ord{rank}.npy"), np.concatenate([t.numpy(), t2.numpy()]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ordered_allreduce_host_is_rank_ordered(tmp_path):
+    """sharding.ordered_allreduce_host (the exchange of group_shard, and the
+    association csrc/comm.cuh's NCCL exchange uses): every rank gets the same
+    bits, equal to the left-to-right sum in rank order."""
+    world = 3
+    mp.spawn(_ordered_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    got = [np.load(tmp_path / f"ord{r}.npy") for r in range(world)]
+    p = [np.array(v) for v in ([1e16, 0.1, 3.0], [1.0, 0.2, -1.0], [1.0, 0.3, 2.0 ** -60])]
+    want = (p[0] + p[1]) + p[2]
+    assert want[0] == 1e16 and (p[0] + (p[1] + p[2]))[0] == 1e16 + 2
+    for g in got:
+        np.testing.assert_array_equal(g[:3], want)
+        np.testing.assert_array_equal(g[3:], np.full(5, 6.0))
+        np.testing.assert_array_equal(g, got[0])
