@@ -141,6 +141,13 @@ int rapdb_set_peer_exchange(rapdb_ctx* ctx, void* const* regions);
  * the op state machine (step ids: rapdb_dev.cuh enum Step), for profiling */
 int rapdb_step_profile(rapdb_ctx* ctx, double* ns, long long* counts, int nsteps);
 
+/* problem.spectral_norm (problem.py:47-68) of a dense device matrix M
+ * [rows][ld] (ld >= cols): power iteration on M'M from cos(k + 1/2), at most
+ * iters steps, stop when |est - prev| <= tol max(est, 1); *out = 1.01 est.
+ * Runs on `stream` and synchronises it.                                     */
+int rapdb_spectral_norm(const double* M, long long rows, long long cols, long long ld, int iters, double tol,
+                        void* stream, double* out);
+
 /* version of the ABI (bumped on incompatible change) */
 int rapdb_abi_version(void);
 
@@ -228,6 +235,20 @@ int rapdb_bind_factored_range(rapdb_ctx* ctx, int n, int mq, int L, int fb0, int
                               const long long* a_ptr, const int* a_col, const double* a_val,
                               const long long* at_ptr, const int* at_row, const double* at_val,
                               const double* b, const double* lower, const double* upper, double mu);
+
+/* Row-phased layout of R^T for the gradient gather (after a factored bind;
+ * optional -- the plain CSR passed to the bind is one untagged phase).  The
+ * stacked rows are split into nph ranges ph_bounds[0..nph] (HOST, 0 .. nr);
+ * pptr (device, [nph][n+1] int64) holds one CSR of R^T per phase over ONE
+ * pair of entry arrays prow / pval (phase-major), so column j's phase-p
+ * entries are [pptr[p (n+1) + j], pptr[p (n+1) + j + 1]) and walking the
+ * phases in order walks the column in sorted row order.  Each phase's
+ * gathers touch only its slice of the W-cache, which then stays in L2.
+ * tagged: prow holds r | (local block of r) << 23 (needs nr <= 2^23, at most
+ * 256 local blocks) and the gather weights W by the block's multiplier on the
+ * fly instead of reading a separately weighted copy.                        */
+int rapdb_set_factored_transpose(rapdb_ctx* ctx, int nph, const long long* ph_bounds, const long long* pptr,
+                                 const int* prow, const double* pval, int tagged);
 
 /* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
  * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */

@@ -51,7 +51,8 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_factored_range", "rapdb_egm", "rapdb_peer_region_bytes", "rapdb_ipc_handle",
            "rapdb_ipc_open", "rapdb_ipc_close", "rapdb_set_peer_exchange", "rapdb_region_alloc",
            "rapdb_region_free", "rapdb_comm_unique_id", "rapdb_comm_create", "rapdb_comm_destroy",
-           "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange"]
+           "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange", "rapdb_set_factored_transpose",
+           "rapdb_spectral_norm"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
@@ -117,6 +118,20 @@ class PeerRegion:
                 load().rapdb_region_free(C.c_void_p(self.ptr))
         except Exception:   # interpreter shutdown
             pass
+
+
+def spectral_norm(M, iters: int, tol: float) -> float:
+    """rapdb_spectral_norm of a float64 CUDA tensor [rows][cols] (row stride = stride(0))."""
+    import torch
+    if M.dtype != torch.float64 or not M.is_cuda or M.dim() != 2 or M.stride(1) != 1:
+        raise InputError("need a row-major float64 CUDA matrix")
+    out = C.c_double()
+    code = load().rapdb_spectral_norm(C.c_void_p(M.data_ptr()), M.shape[0], M.shape[1], M.stride(0), int(iters),
+                                      float(tol), C.c_void_p(torch.cuda.current_stream(M.device).cuda_stream),
+                                      C.byref(out))
+    if code != 0:
+        raise DeviceError(f"rapdb_spectral_norm failed (code {code})")
+    return float(out.value)
 
 
 def comm_unique_id() -> bytes:
@@ -218,6 +233,8 @@ def load(path: str = LIB_PATH):
     lib.rapdb_comm_destroy.restype = None
     lib.rapdb_comm_allreduce_ordered.argtypes = [P, P, LL, P]
     lib.rapdb_set_comm_exchange.argtypes = [P, P, I]
+    lib.rapdb_set_factored_transpose.argtypes = [P, I, P, P, P, P, I]
+    lib.rapdb_spectral_norm.argtypes = [P, LL, LL, LL, I, D, P, C.POINTER(D)]
     _lib = lib
     return lib
 
@@ -341,6 +358,11 @@ class Context:
                 _ptr(data.a_ptr), _ptr(data.a_col), _ptr(data.a_val),
                 _ptr(data.at_ptr), _ptr(data.at_row), _ptr(data.at_val),
                 _ptr(data.b), _ptr(data.lower), _ptr(data.upper), float(data.mu)))
+            if getattr(data, "rt_nph", None):
+                bounds = np.ascontiguousarray(data.rt_bounds, dtype=np.int64)
+                self._check(self.lib.rapdb_set_factored_transpose(
+                    self.h, int(data.rt_nph), bounds.ctypes.data_as(C.c_void_p), _ptr(data.rt_ptr),
+                    _ptr(data.rt_row), _ptr(data.rt_val), int(data.rt_tag)))
         else:
             k1 = data.m + 1 if k1 is None else k1
             zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)

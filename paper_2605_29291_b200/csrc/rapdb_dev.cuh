@@ -107,9 +107,15 @@ struct DevProblem {
   int mq;                // quadratic constraints (factored matrices 0..mq)
   long long nr;          // rows of the stacked R
   int L;                 // linear rows A x <= b (orthant constraints with Q = 0)
-  int nchx;              // chunks of 1024 columns for c_i . x
+  int nchx;              // chunks of kCxCols columns for c_i . x (factored.cuh)
+  int nfpart;            // warps of a fused-trial gradient launch (its D_p / <gx, dx> partials)
   const long long* r_ptr; const int* r_col; const double* r_val;    // CSR R   [nr x n]
-  const long long* rt_ptr; const int* rt_row; const double* rt_val; // CSR R^T [n x nr]
+  const long long* rt_ptr; const int* rt_row; const double* rt_val; // CSR R^T [n x nr], rt_nph row phases:
+  // rt_ptr [rt_nph][n+1] -- column j's entries with rows in phase p are
+  // [rt_ptr[p (n+1) + j], rt_ptr[p (n+1) + j + 1]), phases in row order, so
+  // walking the phases walks each column in sorted row order; rt_tag: rt_row
+  // holds r | (local block of r) << 23 (the gather weights W on the fly)
+  int rt_nph, rt_tag;
   const int* rmat;                                                  // [nr] block of each R row
   const long long* rblk;                                            // [mq+2] first row of block i
   const long long* a_ptr; const int* a_col; const double* a_val;    // CSR A   [L x n]
@@ -155,6 +161,8 @@ struct Work {
   double *W;                   // factored: [2][nr] W = R x at both parities
   double *pw2, *pcx;           // factored: chunk partials of |W_i|^2 and c_i . x
   double *wl;                  // factored: [nr] block-weighted W-cache of the recombination
+  double *fpart;               // factored fused trial: [2][nfpart] per-warp partials of D_p, <gx, dx>
+  unsigned *fctr;              // factored row kernel: [2] work-item / finished-CTA counters
   double *Pt;                  // layout 1: per-unit partial products [nact][nbB][nbB][64]
   unsigned* ccnt;              // layout 1: [64] consumer warps done with each matrix chunk
   int* idone;                  // layout 1: [nact*nbB] phase-B items already reduced during the stream

@@ -16,6 +16,7 @@
 #include "comm.cuh"
 #include "egm.cuh"
 #include "gap.cuh"
+#include "spectral.cuh"
 #include "rapdb_b200.h"
 #include "solver_ops.cuh"
 
@@ -367,7 +368,7 @@ struct rapdb_ctx {
   long long stage_cap = 0;  // doubles available in the staging area
   bool gap_ok = false;      // dense H + shared n-vectors fit (smoothed gap available)
   long long sweep_bytes = 0;  // algorithmic bytes of one sweep (the roofline numerator)
-  long long nchw = 0;       // factored: 1024-row chunks of W over all blocks
+  long long nchw = 0;       // factored: kWChunk-row chunks of W over all blocks
   int split = 0;            // sharded: stop at exchange points
   int fac_host = 0;         // factored: sweeps / gradients as host-launched high-occupancy kernels
   int p2p = 0;              // sharded dense: in-kernel exchanges over peer memory
@@ -447,7 +448,7 @@ struct Layout {
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
-             B_W, B_PW2, B_PCX, B_PT, B_WL, B_EARLY, B_COUNT };
+             B_W, B_PW2, B_PCX, B_PT, B_WL, B_EARLY, B_FPART, B_FCTR, B_COUNT };
 static_assert(B_COUNT <= B_COUNT_MAX, "Layout::off too small");
 
 // chunk counters + per-item flags of the packed sweep's early reduction
@@ -493,6 +494,8 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_PT] = packed ? std::max(1LL, (long long)c->P.nact) * c->sp.geom.nbB * c->sp.geom.nbB * sym::kB * 8 : 8;
   sz[B_WL] = fac ? std::max(c->P.nr, 1LL) * 8 : 8;
   sz[B_EARLY] = early_bytes(c);
+  sz[B_FPART] = fac ? 2LL * std::max(c->P.nfpart, 1) * 8 : 8;
+  sz[B_FCTR] = 64;
   Layout L;
   long long o = 0;
   for (int i = 0; i < B_COUNT; ++i) {
@@ -527,34 +530,90 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   return RAPDB_OK;
 }
 
-// A factored stop: run the requested sweep / gradient(s) as standalone
-// kernels (8 CTAs per SM) on the context's stream, then the op resumes.
-static int gxb_per_sm() {
-  static const int v = [] { const char* e = std::getenv("RAPDB_GXB_CTAS"); return e ? std::max(1, std::atoi(e)) : 16; }();   // C3f: 8 -> 16 per SM, 1.64 -> 1.59 s
-  return v;
+// The max-dynamic-shared-memory attribute is per function and process-wide:
+// only ever raise it, so a context bound later with a smaller need cannot
+// invalidate the launches of an earlier one.
+std::mutex g_attr_mu;
+cudaError_t raise_smem_attr(const void* f, int bytes) {
+  static std::vector<std::pair<const void*, int>> seen;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto& e : seen)
+    if (e.first == f) {
+      if (bytes <= e.second) return cudaSuccess;
+      const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (r == cudaSuccess) e.second = bytes;
+      return r;
+    }
+  const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (r == cudaSuccess) seen.emplace_back(f, bytes);
+  return r;
+}
+
+// A factored stop: run the requested sweep / gradient(s) / fused trial as
+// standalone kernels (several CTAs per SM) on the context's stream, then the
+// op resumes.  Dynamic shared memory of the factored kernels:
+// opt the factored kernels into their shared memory (the per-block weight
+// table rides in dynamic shared memory)
+int fac_kernel_attrs(rapdb_ctx* c) {
+  const DevProblem& P = c->P;
+  const int wq = std::max(P.fnb, 1) * 8;
+  const void* ks[] = {(const void*)fac_grad_kernel<true>, (const void*)fac_grad_kernel<false>,
+                      (const void*)fac_wl_kernel};
+  for (const void* f : ks) {
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, f));
+    if ((long long)fa.sharedSizeBytes + wq > (long long)c->optin)
+      return fail(c, RAPDB_ECONFIG, "too many quadratic blocks for the factored kernels' shared memory");
+    CK(raise_smem_attr(f, wq));
+  }
+  return RAPDB_OK;
+}
+
+// the gradient at W-cache Wpar with multipliers lam into out; TRIAL also
+// takes the fused yx trial's primal step (exactly P.nfpart warps)
+int fac_gradient(rapdb_ctx* c, const Work& w, const double* Wpar, const double* lam, double* out, bool trial,
+                 double tau, int cur) {
+  const DevProblem& P = c->P;
+  const size_t wq = (size_t)std::max(P.fnb, 1) * 8;
+  const double* Wsrc = Wpar;
+  if (!P.rt_tag) {   // block-weighted W-cache first
+    fac_wl_kernel<<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wpar, lam);
+    Wsrc = w.wl;
+    ++g_launches;
+  }
+  if (P.rt_tag) fac_grad_kernel<true><<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out);
+  else fac_grad_kernel<false><<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out);
+  const int fgrid = P.nfpart / kWarps;
+  if (trial) fac_grad_fin_kernel<true><<<fgrid, kThreads, 0, c->stream>>>(P, w, out, tau, cur);
+  else fac_grad_fin_kernel<false><<<fgrid, kThreads, 0, c->stream>>>(P, w, out, tau, cur);
+  g_launches += 2;
+  return RAPDB_OK;
 }
 
 int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   const DevProblem& P = c->P;
   const Work& w = c->w;
-  const int grid = c->nsm * 8;
   const long long n = P.n, np = (long long)P.p + P.m;
+  const int rgrid = c->nsm * 4;   // row pass: 4 CTAs per SM (a multiple of 4 warps)
   if (st.fq[0] == 1) {
     const int par = st.fq[1];
     const double* x = st.fq[2] ? rc.in_x : w.x + (long long)par * n;
-    fac_sweep_a_kernel<<<c->nsm * 4, kThreads, 0, c->stream>>>(P, w, x, par);   // 30 KB smem per CTA
-    fac_sweep_b_kernel<<<grid, kThreads, 0, c->stream>>>(P, w, par);
-    g_launches += 2;
+    fac_row_kernel<<<rgrid, kThreads, 0, c->stream>>>(P, w, x, par);
+    ++g_launches;
   } else if (st.fq[0] == 2) {
     for (int k = 0; k < st.fq[1] && k < 2; ++k) {
       const int par = st.fq[2 + 3 * k], lid = st.fq[3 + 3 * k], oid = st.fq[4 + 3 * k];
       const double* lam = lid == 0 ? w.ytr + P.p : lid == 1 ? w.y + P.p : lid == 2 ? w.y + np + P.p : rc.in_lam;
       double* out = oid == 0 ? w.gxs : w.gxb + (long long)st.ig_new * n;
-      const double* Wpar = w.W + (long long)par * P.nr;
-      fac_gx_a_kernel<<<grid, kThreads, (size_t)std::max(P.fnb, 1) * 8, c->stream>>>(P, w, Wpar, lam, out);
-      fac_gx_b_kernel<<<c->nsm * gxb_per_sm(), kThreads, 0, c->stream>>>(P, w, lam, out);
-      g_launches += 2;
+      fac_gradient(c, w, w.W + (long long)par * P.nr, lam, out, false, 0.0, 0);
     }
+  } else if (st.fq[0] == 3) {
+    // the fused yx trial (unsharded): gradient + primal step, then the row
+    // pass (W, |W|^2, A x - b, c_i . x) at x_new
+    const int cur = st.fq[1];
+    fac_gradient(c, w, w.W + (long long)cur * P.nr, w.ytr + P.p, w.gxs, true, st.tau, cur);
+    fac_row_kernel<<<rgrid, kThreads, 0, c->stream>>>(P, w, w.x + (long long)(cur ^ 1) * n, cur ^ 1);
+    ++g_launches;
   } else {
     return fail(c, RAPDB_EDEVICE, "unknown factored request");
   }
@@ -1076,8 +1135,7 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   // the staged duals and the recombination scratch at the ring's end must not meet
   if (2LL * (p + m) + kWarps * 32 > c->stage_cap)
     return fail(c, RAPDB_ECONFIG, "too many multipliers for the shared-memory dual staging area");
-  cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->dyn_smem);
+  cudaError_t e = raise_smem_attr((const void*)rapdb_solver_kernel, (int)c->dyn_smem);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaFuncSetAttribute");
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)rapdb_solver_kernel, kThreads, c->dyn_smem);
@@ -1085,6 +1143,10 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   if (occ < 1) return fail(c, RAPDB_EDEVICE, "solver kernel cannot be resident");
   c->G = c->nsm * occ;
   if (c->G > 256) c->G = 256;   // get_totals keeps <= 8 partials per lane
+  if (const char* eg = std::getenv("RAPDB_GRID")) {   // experiment knob: fewer CTAs
+    const int g = std::atoi(eg);
+    if (g >= 1 && g < c->G) c->G = g;
+  }
   const int G = c->G;
   // row partition of the streamed rows over CTAs and the segment tables
   const long long R = (long long)act.size() * n;
@@ -1186,7 +1248,7 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   for (int i = 0; i < fnb; ++i) {
     if (rblk[i + 1] < rblk[i]) return fail(c, RAPDB_EINPUT, "rblk must be nondecreasing");
     ll[i] = rblk[i];
-    ll[fnb + 1 + i + 1] = ll[fnb + 1 + i] + (rblk[i + 1] - rblk[i] + 1023) / 1024;
+    ll[fnb + 1 + i + 1] = ll[fnb + 1 + i] + (rblk[i + 1] - rblk[i] + kWChunk - 1) / kWChunk;   // W chunks
   }
   ll[fnb] = nr;
   const long long nchw = ll[2 * (fnb + 1) - 1];
@@ -1206,7 +1268,7 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   SweepPlan sp{};
   sp.TR = 1; sp.cpr = 1; sp.chunk = 2; sp.nstages = 1; sp.ncw = 1; sp.segmax = 1;
   sp.rc_cols = 1;   // the recombination ends warp-per-column: barrier before the primal step
-  sp.stage_bytes = align_up((long long)std::max(fnb, 1) * 8, 128);
+  sp.stage_bytes = align_up((long long)(kWarps + 1) * std::max(fnb, 1) * 8, 128);   // wq / c_i . x sums
   sp.xs_bytes = 0;
   sp.rows_total = 0;
   c->dyn_smem = (size_t)(sp.stage_bytes + 16);
@@ -1214,8 +1276,7 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   c->gap_ok = false;
   if ((long long)c->dyn_smem + 4096 > (long long)c->optin)
     return fail(c, RAPDB_ECONFIG, "too many quadratic constraints for the staging area");
-  cudaError_t e = cudaFuncSetAttribute((const void*)rapdb_solver_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->dyn_smem);
+  cudaError_t e = raise_smem_attr((const void*)rapdb_solver_kernel, (int)c->dyn_smem);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaFuncSetAttribute");
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)rapdb_solver_kernel, kThreads, c->dyn_smem);
@@ -1227,10 +1288,12 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   P.n = n; P.m = m; P.p = 0; P.k0 = 0; P.k1 = m + 1; P.nloc = 0; P.nact = 0; P.nzero = 0; P.ld = n;
   P.Q = nullptr; P.q = C; P.r = d; P.A = nullptr; P.b = b; P.lo = lower; P.hi = upper; P.mu = mu;
   P.act = P.zero_list = P.seg_lo = P.seg_hi = P.cta_a0 = P.mat_slot = c->d_ints;
-  P.kind = 1; P.mq = mq; P.nr = nr; P.L = L; P.nchx = (n + 1023) / 1024;
+  P.kind = 1; P.mq = mq; P.nr = nr; P.L = L; P.nchx = (n + kCxCols - 1) / kCxCols;
+  P.nfpart = c->nsm * 4 * kWarps;   // fused-trial gradient grid: 4 CTAs per SM
   P.fb0 = fb0; P.fnb = fnb; P.l0 = l0; P.Lloc = Lloc;
   P.r_ptr = r_ptr; P.r_col = r_col; P.r_val = r_val;
   P.rt_ptr = rt_ptr; P.rt_row = rt_row; P.rt_val = rt_val;
+  P.rt_nph = 1; P.rt_tag = 0;   // plain CSR of R^T until rapdb_set_factored_transpose
   P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (fnb + 1);
   P.a_ptr = a_ptr; P.a_col = a_col; P.a_val = a_val;
   P.at_ptr = at_ptr; P.at_row = at_row; P.at_val = at_val;
@@ -1242,8 +1305,72 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   // one factored sweep: R (12 B/nnz + row pointers) streamed, W written and
   // re-read, C and A (+ b) read, x gathered once
   c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * fnb * n + 12 * nnz_a + 16LL * Lloc + 8 + 8LL * n;
+  {
+    const int ra = fac_kernel_attrs(c);
+    if (ra) return ra;
+  }
   c->bound = true;
   c->have_ws = false;
+  return RAPDB_OK;
+}
+
+int rapdb_spectral_norm(const double* M, long long rows, long long cols, long long ld, int iters, double tol,
+                        void* stream, double* out) {
+  if (!M || !out || rows < 0 || cols < 0 || ld < cols || iters < 0) return RAPDB_EINPUT;
+  *out = 0.0;
+  if (rows == 0 || cols == 0) return RAPDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double *v = nullptr, *w1 = nullptr, *w = nullptr, *nr = nullptr, *h = nullptr;
+  const size_t bytes = (size_t)(2 * cols + rows + 2) * sizeof(double);
+  if (cudaMallocAsync(reinterpret_cast<void**>(&v), bytes, s) != cudaSuccess) return RAPDB_EDEVICE;
+  w = v + cols;
+  w1 = w + cols;
+  nr = w1 + rows;
+  int rc = RAPDB_OK;
+  if (cudaMallocHost(reinterpret_cast<void**>(&h), sizeof(double)) != cudaSuccess) rc = RAPDB_EDEVICE;
+  const int blocks = (int)std::min<long long>(1184, (cols + 255) / 256);
+  const int rblocks = (int)std::min<long long>(1184, (rows * 32 + 255) / 256);
+  if (!rc) {
+    rapdb_spec::init_v<<<blocks, 256, 0, s>>>(v, cols);
+    rapdb_spec::norm_normalize<<<1, 1024, 0, s>>>(v, v, cols, nr, 1);    // v /= |v|
+    g_launches += 2;
+    double prev = 0.0;
+    for (int it = 0; it < iters; ++it) {
+      rapdb_spec::mv_rows<<<rblocks, 256, 0, s>>>(M, rows, cols, ld, v, w1);
+      rapdb_spec::mv_cols<<<blocks, 256, 0, s>>>(M, rows, cols, ld, w1, w);
+      rapdb_spec::norm_normalize<<<1, 1024, 0, s>>>(w, v, cols, nr, 1);
+      g_launches += 3;
+      if (cudaMemcpyAsync(h, nr, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess) { rc = RAPDB_EDEVICE; break; }
+      const double nrm = *h;
+      if (nrm == 0.0) { prev = 0.0; break; }
+      const double est = std::sqrt(nrm);
+      const bool done = std::fabs(est - prev) <= tol * std::max(est, 1.0);
+      prev = est;
+      if (done) break;
+    }
+    *out = 1.01 * prev;
+  }
+  if (h) cudaFreeHost(h);
+  cudaFreeAsync(v, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) rc = RAPDB_EDEVICE;
+  return rc;
+}
+
+int rapdb_set_factored_transpose(rapdb_ctx* c, int nph, const long long* ph_bounds, const long long* pptr,
+                                 const int* prow, const double* pval, int tagged) {
+  if (!c) return RAPDB_EINPUT;
+  if (!c->bound || c->P.kind != 1) return fail(c, RAPDB_ECONFIG, "bind a factored instance first");
+  DevProblem& P = c->P;
+  if (nph < 1 || !ph_bounds || !pptr || (P.nr > 0 && (!prow || !pval)))
+    return fail(c, RAPDB_EINPUT, "need nph >= 1 phases and their arrays");
+  if (ph_bounds[0] != 0 || ph_bounds[nph] != P.nr) return fail(c, RAPDB_EINPUT, "phase bounds must run from 0 to nr");
+  for (int i = 0; i < nph; ++i)
+    if (ph_bounds[i + 1] < ph_bounds[i]) return fail(c, RAPDB_EINPUT, "phase bounds must be nondecreasing");
+  if (tagged && (P.nr > kRtRowMask + 1LL || P.fnb > (1 << (31 - kRtTagShift))))
+    return fail(c, RAPDB_EINPUT, "tagged R^T rows need nr <= 2^23 and at most 256 local blocks");
+  P.rt_ptr = pptr; P.rt_row = prow; P.rt_val = pval;
+  P.rt_nph = nph; P.rt_tag = tagged ? 1 : 0;
   return RAPDB_OK;
 }
 
@@ -1291,6 +1418,8 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.pcx = D(B_PCX);
   w.Pt = D(B_PT);
   w.wl = D(B_WL);
+  w.fpart = D(B_FPART);
+  w.fctr = reinterpret_cast<unsigned*>(base + L.off[B_FCTR]);
   w.ccnt = reinterpret_cast<unsigned*>(base + L.off[B_EARLY]);
   w.idone = reinterpret_cast<int*>(base + L.off[B_EARLY] + 256);
   w.trace = nullptr;

@@ -303,6 +303,53 @@ __device__ __noinline__ int ty_primal_fac(const KArgs& K, Sm& S) {
   return gsync(K, S) ? TY_SWEEP : kAbort;
 }
 
+// after the fused trial's kernels (x_new, gx, W / g parts at x_new are in
+// place): the dual side of ty_primal_fac plus the gradient kernel's per-warp
+// partials of D_p and <gx, dx>, dealt to the persistent grid's threads in a
+// fixed pattern and reduced with the other partials (fixed order); the
+// sweep already ran, so the trial continues at TY_GLOCAL.
+__device__ __noinline__ int ty_primal_fac_fused(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const Work& w = K.w;
+  SolverState& st = *S.st;
+  const long long m = P.m;
+  const int cur = st.cur, nxt = cur ^ 1;
+  // thread t of CTA b takes the gradient kernel's warps b + G t, b + G (t + 256), ...
+  double s_dp = 0.0, s_gd = 0.0;
+  for (long long c = blockIdx.x + (long long)gridDim.x * threadIdx.x; c < P.nfpart; c += gstride()) {
+    s_dp += ldcg(w.fpart + c);
+    s_gd += ldcg(w.fpart + P.nfpart + c);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st.sweeps += 1;
+  const long long G = gstride();
+  double s_dd = 0.0, s_ml = 0.0;
+  const double* yc = w.y + (long long)cur * m;
+  double* yn = w.y + (long long)nxt * m;
+  const double* gvc = w.gval + (long long)cur * (m + 1);
+  for (long long j0 = gtid(); j0 < m; j0 += kLV * G) {
+    double yv[kLV], yo[kLV], gv[kLV];
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) { yv[t] = ldcg(w.ytr + j); yo[t] = ldcg(yc + j); gv[t] = ldcg(gvc + (j + 1)); }
+    }
+#pragma unroll
+    for (int t = 0; t < kLV; ++t) {
+      const long long j = j0 + t * G;
+      if (j < m) {
+        yn[j] = yv[t];
+        const double d = yv[t] - yo[t];
+        s_dd += d * d;
+        s_ml += yv[t] * gv[t];
+      }
+    }
+  }
+  const double v5[5] = {s_dp, s_gd, s_dd, 0.0, s_ml};
+  const int sl[5] = {S_DP, S_GXDX, S_DD, S_MIXV, S_MIXL};
+  put_partials(K, S, v5, sl);
+  return gsync(K, S) ? TY_GLOCAL : kAbort;
+}
+
 __device__ __noinline__ int ty_gy_fac(const KArgs& K, Sm& S) {
   const Work& w = K.w;
   SolverState& st = *S.st;
@@ -479,10 +526,26 @@ __device__ int ty_dual(const KArgs& K, Sm& S) {
   return gsync(K, S) ? TY_GXPART : kAbort;
 }
 
+// The fused factored yx trial (unsharded, host-launched kernels): one stop
+// per trial runs the gradient, the primal step, c_i . x_new (one pass over
+// C) and the row pass at x_new (factored.cuh fac_trial_kernel /
+// fac_row_kernel); ty_primal_fac_fused then adds the dual-side partials.
+__device__ __forceinline__ bool fac_fused_trial(const KArgs& K) {
+  return K.P.kind == 1 && K.rc.fac_host && !K.rc.split && K.prm.mode == 0;
+}
+
 __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
   const DevProblem& P = K.P;
   const Work& w = K.w;
   SolverState& st = *S.st;
+  if (fac_fused_trial(K)) {
+    if (threadIdx.x == 0) {
+      st.fq[0] = 3;
+      st.fq[1] = st.cur;
+    }
+    __syncthreads();
+    return TY_PRIMAL;
+  }
   double* v_s = S.stage;
   double* lam_s = S.stage + P.p;
   if (dual_cta_local(K)) {
@@ -497,6 +560,7 @@ __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {
 }
 
 __device__ int ty_primal(const KArgs& K, Sm& S) {
+  if (fac_fused_trial(K)) return ty_primal_fac_fused(K, S);
   if (K.P.kind == 1) return ty_primal_fac(K, S);
   const DevProblem& P = K.P;
   const Work& w = K.w;

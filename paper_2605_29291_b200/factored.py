@@ -13,9 +13,14 @@ config 3 is new capability built on the same operator contract
 ``problem.ProblemInstance`` (n, m, p, primal_set, cone, mu, f/g evaluation,
 device upload), so ``ApdbEngine`` / ``run_restarted`` / ``kkt_residual`` take
 either.  HBM layout (``FactoredDeviceData``): the stacked R as CSR (int64 row
-pointers, int32 columns, fp64 values) plus a second CSR of R^T so the
-transposed product is a gather (no atomics, fixed summation order), the
-block id of every stacked row, C [(mq+1) x n], and A / A^T as CSR.
+pointers, int32 columns, fp64 values) plus R^T as a gather (no atomics, fixed
+summation order) in ROW PHASES: the stacked rows are cut into ranges of at
+most ``RT_PHASE_ROWS`` (12 MB of the W-cache), with one CSR of R^T per phase
+over phase-major entry arrays, each entry's row tagged with its block id
+(``rapdb_set_factored_transpose``) -- so each gather phase touches an
+L2-sized slice of W, and walking the phases walks every column in sorted row
+order; plus the block id of every stacked row, C [(mq+1) x n], and A / A^T
+as CSR.
 """
 
 from __future__ import annotations
@@ -26,6 +31,32 @@ import numpy as np
 
 from .errors import ConfigurationError, InputError
 from .geometry import Box, NonnegOrthant
+
+import os as _os
+
+# W-cache rows gathered per R^T phase (RAPDB_RT_PHASE_ROWS overrides; A/B runs)
+RT_PHASE_ROWS = int(_os.environ.get("RAPDB_RT_PHASE_ROWS", str(1 << 23)))
+RT_TAG_SHIFT = 23              # tagged R^T rows: r | block << 23
+
+
+def phased_transpose(R, rmat, nph: int, tag: bool):
+    """(bounds, ptr [nph][n+1], rows, vals) of R^T split into nph row phases,
+    entries phase-major; rows tagged with their block id when ``tag``."""
+    nr, n = R.shape
+    bounds = np.array([nr * p // nph for p in range(nph + 1)], dtype=np.int64)
+    ptrs, rows, vals = [], [], []
+    off = 0
+    for p in range(nph):
+        Rt = R[bounds[p]:bounds[p + 1]].T.tocsr()      # sorted rows per column
+        Rt.sort_indices()
+        idx = Rt.indices.astype(np.int64) + bounds[p]
+        if tag:
+            idx = idx | (rmat[idx].astype(np.int64) << RT_TAG_SHIFT)
+        ptrs.append(Rt.indptr.astype(np.int64) + off)
+        rows.append(idx.astype(np.int32))
+        vals.append(Rt.data)
+        off += Rt.nnz
+    return bounds, np.concatenate(ptrs), np.concatenate(rows), np.concatenate(vals)
 
 
 class FactoredInstance:
@@ -169,13 +200,15 @@ class FactoredDeviceData:
         r0, r1 = int(inst.rblk[k0]), int(inst.rblk[k1])
         R = inst.R[r0:r1]
         rblk = inst.rblk[k0:k1 + 1] - r0
-        Rt = R.T.tocsr()
         A = inst.A[l0:l1]
         At = A.T.tocsr()
         nr = R.shape[0]
         rmat = np.repeat(np.arange(k1 - k0, dtype=np.int32), np.diff(rblk))
         r_ptr, r_col, r_val = csr(R)
-        rt_ptr, rt_row, rt_val = csr(Rt)
+        nph = max(1, -(-nr // RT_PHASE_ROWS))
+        tag = nr <= (1 << RT_TAG_SHIFT) and (k1 - k0) <= 256
+        rt_bounds, pp, pr, pv = phased_transpose(R, rmat, nph, tag)
+        rt_ptr, rt_row, rt_val = i64(pp), i32(pr), f64(pv)
         a_ptr, a_col, a_val = csr(A)
         at_ptr, at_row, at_val = csr(At)
         one = lambda t: t if t.numel() else torch.zeros(1, dtype=t.dtype, device=device)
@@ -186,4 +219,4 @@ class FactoredDeviceData:
                    a_ptr=a_ptr, a_col=one(a_col), a_val=one(a_val), at_ptr=at_ptr, at_row=one(at_row),
                    at_val=one(at_val), b=one(f64(inst.b[l0:l1])), lower=f64(inst.primal_set.lower),
                    upper=f64(inst.primal_set.upper), mu=inst.mu, device=device,
-                   nnz_r=int(R.nnz), nnz_a=int(A.nnz))
+                   nnz_r=int(R.nnz), nnz_a=int(A.nnz), rt_nph=nph, rt_bounds=rt_bounds, rt_tag=int(tag))

@@ -23,7 +23,7 @@ from typing import Optional
 
 import numpy as np
 
-from .errors import ConfigurationError, InputError
+from .errors import ConfigurationError, DeviceError, InputError
 from .geometry import Box, NonnegOrthant, cone_dim, set_dim
 
 
@@ -303,6 +303,25 @@ class LipschitzConstants:
     psi1: float
     psi2: float
     B_g_is_estimate: bool = False
+    bar_B_used: float = np.inf
+
+
+def spectral_norm(M, iters: int = 200, tol: float = 1e-10, device=None) -> float:
+    """problem.py:47-68 on the device (rapdb_spectral_norm): power iteration on
+    M'M from cos(k + 1/2), stop when |est - prev| <= tol max(est, 1), 1.01
+    inflation.  Sparse M is densified for the device product."""
+    import torch
+    from . import _capi
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: spectral_norm runs on the GPU (no CPU fallback)")
+    Md = M.toarray() if hasattr(M, "toarray") else np.asarray(M, dtype=np.float64)
+    Md = np.ascontiguousarray(Md, dtype=np.float64)
+    if Md.ndim != 2:
+        raise InputError("spectral_norm needs a matrix")
+    if Md.shape[0] == 0 or Md.shape[1] == 0:
+        return 0.0
+    dev = torch.device("cuda", 0) if device is None else torch.device(device)
+    return _capi.spectral_norm(torch.from_numpy(Md).to(dev), iters, tol)
 
 
 def compute_constants(*args, **kwargs):

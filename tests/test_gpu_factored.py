@@ -2,10 +2,11 @@
 through the C ABI, against the reference's golden run of the densified
 instance and the oracle's factored restatement.
 
-Tolerances: the device sums CSR products in a different order than scipy
-(gathers over R and R^T, fixed warp/chunk trees), so traces agree to
-rounding, not bitwise: backtrack counts identical, step sizes to 1e-9
-relative, iterates to 1e-8 relative over 200 iterations.
+Tolerances: the device sums some CSR products in a different order than
+scipy (the R^T gather per column, fixed chunk trees for the dot products),
+so iterates agree to rounding (1e-8 relative over 200 iterations); the
+accepted step sizes depend on the data only through the accept decisions,
+so they -- and the backtrack counts -- must be identical.
 """
 
 import numpy as np
@@ -77,7 +78,7 @@ def test_factored_200_vs_reference(small, key, nm):
     tr = trace_arr(eng.trace)
     tg = g[f"{key}/trace"]
     np.testing.assert_array_equal(tr[:, 5], tg[:, 5])
-    np.testing.assert_allclose(tr[:, 1:5], tg[:, 1:5], rtol=1e-9)
+    np.testing.assert_array_equal(tr[:, 1:5], tg[:, 1:5])
     assert rel(eng.average().x, g[f"{key}/avg_x"]) <= 1e-8
 
 
@@ -88,7 +89,7 @@ def test_factored_xy_vs_oracle(small):
     eng.run_block(150)
     tr = trace_arr(eng.trace)
     np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
-    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
     assert rel(eng.last.x, res.x) <= 1e-8
 
 
@@ -131,7 +132,7 @@ def test_factored_shapes_vs_oracle(shape, nm):
     eng.run_block(iters)
     tr = trace_arr(eng.trace)
     np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
-    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
     z = eng.last
     assert rel(z.x, res.x) <= 1e-8
     if arr.m:
@@ -165,7 +166,7 @@ def test_factored_dual_ball_vs_oracle(small, kind, mode, nm):
     eng.run_block(iters)
     tr = trace_arr(eng.trace)
     np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
-    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+    np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
     z = eng.last
     assert rel(z.x, res.x) <= 1e-8
     assert rel(z.lam, res.lam) <= 1e-8
@@ -224,11 +225,11 @@ def test_factored_emulated_shards(small, nranks, nm):
 
     for tr, z in cluster.run(inst, body):
         np.testing.assert_array_equal(tr[:, 5], tr_ref[:, 5])
-        np.testing.assert_allclose(tr[:, 1:5], tr_ref[:, 1:5], rtol=1e-12)
+        np.testing.assert_array_equal(tr[:, 1:5], tr_ref[:, 1:5])
         assert rel(z.x, ref.last.x) <= 1e-12
         assert rel(z.lam, ref.last.lam) <= 1e-11
         np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
-        np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-9)
+        np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
 
 
 def test_factored_emulated_shards_with_ball(small):
@@ -253,7 +254,7 @@ def test_factored_emulated_shards_with_ball(small):
 
     for tr, z in cluster.run(inst, body):
         np.testing.assert_array_equal(tr[:, 5], tr_ref[:, 5])
-        np.testing.assert_allclose(tr[:, 1:5], tr_ref[:, 1:5], rtol=1e-12)
+        np.testing.assert_array_equal(tr[:, 1:5], tr_ref[:, 1:5])
         assert rel(z.x, ref.last.x) <= 1e-12
         assert rel(z.lam, ref.last.lam) <= 1e-11
 
@@ -272,6 +273,6 @@ def test_c3_full_size_first_iterations():
     eng.run_block(3)
     tr = trace_arr(eng.trace)
     np.testing.assert_array_equal(tr[:, 5], tr_o[:, 5])
-    np.testing.assert_allclose(tr[:, 1:5], tr_o[:, 1:5], rtol=1e-12)
+    np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
     assert rel(eng.last.x, res_o.x) <= 1e-9
     assert rel(eng.last.lam, res_o.lam) <= 1e-9

@@ -83,3 +83,19 @@ def test_grad_x_finite_differences(layout):
 def test_dimension_mismatch():
     with pytest.raises(R.InputError):
         R.coupling_value(ball(), R.Iterate(np.zeros(3), np.zeros(0), np.zeros(1)))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 3), (40, 40), (300, 123), (123, 300)])
+def test_spectral_norm_vs_oracle(shape):
+    """problem.spectral_norm (problem.py:47-68) on the device vs the oracle's
+    restatement: same start vector, stop rule and 1.01 inflation."""
+    from oracle import rapdb_oracle as O
+    from paper_2605_29291_b200.problem import spectral_norm
+    rng = np.random.default_rng(sum(shape))
+    M = rng.standard_normal(shape)
+    M[rng.random(shape) < 0.3] = 0.0
+    got = spectral_norm(M)
+    want = O.spectral_norm(M)
+    assert abs(got - want) <= 1e-9 * want, (got, want)
+    assert abs(got - 1.01 * np.linalg.norm(M, 2)) <= 1e-3 * got   # converged to ||M||_2
+    assert spectral_norm(np.zeros((3, 4))) == 0.0

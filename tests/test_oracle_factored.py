@@ -62,3 +62,32 @@ def test_oracle_factored_restatement(arr, golden_factored, key):
     np.testing.assert_allclose(tr[:, 1:5], tg[:, 1:5], rtol=1e-9)
     np.testing.assert_allclose(res.x, golden_factored[f"{key}/final_x"], rtol=1e-8, atol=1e-9)
     np.testing.assert_allclose(res.lam, golden_factored[f"{key}/final_lam"], rtol=1e-8, atol=1e-9)
+
+
+def test_phased_transpose_walks_columns_in_row_order():
+    """factored.phased_transpose (the R^T gather layout): concatenating a
+    column's entries over the phases gives that column of R^T.tocsr() in
+    sorted row order, and the tags decode to (row, block)."""
+    from paper_2605_29291_b200.factored import RT_TAG_SHIFT, phased_transpose
+    arr = instances.factored_qcqp(n=300, mq=4, rows=30, nnz_row=10, lin_rows=20, lin_nnz=5, seed=5)
+    R = arr.R
+    nr, n = R.shape
+    rmat = np.repeat(np.arange(arr.mq + 1, dtype=np.int32), arr.rows)
+    full = R.T.tocsr()
+    full.sort_indices()
+    for nph, tag in ((1, False), (3, True), (7, True)):
+        bounds, ptr, rows, vals = phased_transpose(R, rmat, nph, tag)
+        assert bounds[0] == 0 and bounds[-1] == nr and ptr.shape == (nph * (n + 1),)
+        for j in range(n):
+            seg_r, seg_v = [], []
+            for p in range(nph):
+                a, b = ptr[p * (n + 1) + j], ptr[p * (n + 1) + j + 1]
+                seg_r.append(rows[a:b])
+                seg_v.append(vals[a:b])
+            r = np.concatenate(seg_r).astype(np.int64)
+            v = np.concatenate(seg_v)
+            if tag:
+                np.testing.assert_array_equal(r >> RT_TAG_SHIFT, rmat[r & ((1 << RT_TAG_SHIFT) - 1)])
+                r = r & ((1 << RT_TAG_SHIFT) - 1)
+            np.testing.assert_array_equal(r, full.indices[full.indptr[j]:full.indptr[j + 1]])
+            np.testing.assert_array_equal(v, full.data[full.indptr[j]:full.indptr[j + 1]])
