@@ -148,6 +148,12 @@ int rapdb_step_profile(rapdb_ctx* ctx, double* ns, long long* counts, int nsteps
 int rapdb_spectral_norm(const double* M, long long rows, long long cols, long long ld, int iters, double tol,
                         void* stream, double* out);
 
+/* Debug: with RAPDB_GUARD=1 in the environment when the workspace size is
+ * queried, every workspace buffer is followed by a 4 KB guard zone filled
+ * with a byte pattern; this returns the number of buffers whose guard was
+ * written (report: which), 0 when all are intact or guards are off.        */
+int rapdb_check_guards(rapdb_ctx* ctx, char* report, int size);
+
 /* version of the ABI (bumped on incompatible change) */
 int rapdb_abi_version(void);
 
@@ -283,6 +289,18 @@ int rapdb_egm(rapdb_ctx* ctx, double stepsize, long long K, int trace_every, dou
 
 /* kkt_residual at the current iterate (diagnostics.py:96-113); out[8] host   */
 int rapdb_kkt(rapdb_ctx* ctx, int has_f_star, double f_star, double* out);
+
+/* kkt_residual (diagnostics.py:96-113) and coupling_value (problem.py:196-204)
+ * at an explicit point (device x[n], v[p], lam[m]; evaluated where given, no
+ * projection): one fused sweep at x, g, grad_x Phi, the residual norms.
+ * out[9] host = kkt, stationarity, primal_eq, complementarity, infeas,
+ * f_value, mean_pos_violation, subopt_abs (NaN without f_star), Phi.
+ * Unsharded contexts only.                                                   */
+/* eq_residual (problem.py:175-177): A x - b at device x into device eq[p]    */
+int rapdb_eq_residual(rapdb_ctx* ctx, const double* x, double* eq);
+
+int rapdb_kkt_at(rapdb_ctx* ctx, const double* x, const double* v, const double* lam, int has_f_star, double f_star,
+                 double* out);
 
 /* engine.last / engine.average() (engine.py:262-272) into device buffers     */
 int rapdb_get_iterate(rapdb_ctx* ctx, int which, double* x, double* v, double* lam);

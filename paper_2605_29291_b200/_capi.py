@@ -52,13 +52,14 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_ipc_open", "rapdb_ipc_close", "rapdb_set_peer_exchange", "rapdb_region_alloc",
            "rapdb_region_free", "rapdb_comm_unique_id", "rapdb_comm_create", "rapdb_comm_destroy",
            "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange", "rapdb_set_factored_transpose",
-           "rapdb_spectral_norm"]
+           "rapdb_spectral_norm", "rapdb_kkt_at", "rapdb_eq_residual",
+           "rapdb_check_guards"]
 
 STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
               "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
               "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
               "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
-              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN",
+              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN", "P_KKT",
               "E_INIT", "E_GX", "E_HALF", "E_HSWEEP", "E_HGLOC", "E_GXH", "E_PLUS", "E_PSWEEP", "E_PGLOC",
               "E_POST", "DONE"] + [""] * 14 + ["sweep:stage_x", "sweep:stream", "sweep:reduce", ""]
 
@@ -235,6 +236,9 @@ def load(path: str = LIB_PATH):
     lib.rapdb_set_comm_exchange.argtypes = [P, P, I]
     lib.rapdb_set_factored_transpose.argtypes = [P, I, P, P, P, P, I]
     lib.rapdb_spectral_norm.argtypes = [P, LL, LL, LL, I, D, P, C.POINTER(D)]
+    lib.rapdb_kkt_at.argtypes = [P, P, P, P, I, D, C.POINTER(D)]
+    lib.rapdb_eq_residual.argtypes = [P, P, P]
+    lib.rapdb_check_guards.argtypes = [P, C.c_char_p, I]
     _lib = lib
     return lib
 
@@ -414,6 +418,27 @@ class Context:
         out = (C.c_double * 8)()
         self._check(self.lib.rapdb_kkt(self.h, 0 if f_star is None else 1,
                                        0.0 if f_star is None else float(f_star), out))
+        return list(out)
+
+    def check_guards(self):
+        """(number of workspace buffers whose guard zone was written, report)."""
+        buf = C.create_string_buffer(4096)
+        n = int(self.lib.rapdb_check_guards(self.h, buf, 4096))
+        if n < 0:
+            raise DeviceError("guard check failed")
+        return n, buf.value.decode(errors="replace")
+
+    def eq_residual(self, x, out):
+        self._set_stream()
+        self._check(self.lib.rapdb_eq_residual(self.h, _ptr(x), _ptr(out)))
+
+    def kkt_at(self, x, v, lam, f_star=None):
+        """[kkt, stationarity, primal_eq, complementarity, infeas, f, mpv,
+        subopt, Phi] at an explicit device point (rapdb_kkt_at)."""
+        self._set_stream()
+        out = (C.c_double * 9)()
+        self._check(self.lib.rapdb_kkt_at(self.h, _ptr(x), _ptr(v), _ptr(lam), 0 if f_star is None else 1,
+                                          0.0 if f_star is None else float(f_star), out))
         return list(out)
 
     def egm(self, stepsize: float, K: int, trace_every: int = 0):

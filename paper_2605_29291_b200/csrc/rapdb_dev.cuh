@@ -48,7 +48,8 @@ enum Slot {
   NSLOT
 };
 
-enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5, OP_GRAD = 6, OP_EGM = 7 };
+enum Op { OP_RUN = 0, OP_REINIT = 1, OP_KKT = 2, OP_GET = 3, OP_PROBE = 4, OP_GAP = 5, OP_GRAD = 6, OP_EGM = 7,
+           OP_KKTAT = 8 };
 enum RunStatus { ST_LIMIT = 0, ST_CONVERGED = 1, ST_BUDGET = 2, ST_CHECK_DUE = 3,
                  ST_FIXED_DUE = 4, ST_NONCONV = 5, ST_ABORT = 6, ST_EXCHANGE = 7, ST_RUNNING = 8 };
 
@@ -56,6 +57,7 @@ struct SolverState {
   double tau_cand, tau_prev, gamma, sigma_prev, alpha, beta, sigma0, T, phi_k;
   double fail_tau, fail_gamma;
   double metrics[8];
+  double phi_at;           // OP_KKTAT: coupling_value at the given point
   double gap[6];           // gap, subsolver iterations, residual, converged, L, dual term
   double sweep_ns;
   long long iters, evals_total, inner, fail_iter, sweeps;
@@ -83,7 +85,7 @@ enum Step {
   A_POST, K_GXPART, K_FINISH, A_RESTART, A_END,
   R_POINT, R_SWEEP, R_GLOCAL, R_CACHE, R_GXPART, R_GXCACHE, R_FINISH,
   G_CAND, G_GLOCAL, G_HPART, G_SOLVE,
-  P_SWEEP, P_OUT, P_GRAD, P_GFIN,
+  P_SWEEP, P_OUT, P_GRAD, P_GFIN, P_KKT,
   E_INIT, E_GX, E_HALF, E_HSWEEP, E_HGLOC, E_GXH, E_PLUS, E_PSWEEP, E_PGLOC, E_POST,
   DONE
 };

@@ -141,19 +141,29 @@ __device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
     case P_OUT: {   // g (and the cache row(s): U, or W = R x when factored) at rc.in_x
       const DevProblem& P = K.P;
       const int par = st.cur ^ 1;
-      const int nxt = rc.op == OP_GRAD ? P_GRAD : DONE;
+      const int nxt = (rc.op == OP_GRAD || rc.op == OP_KKTAT) ? P_GRAD : DONE;
       if (P.kind == 1) {
         g_factored(K, par);
         if (!gsync(K, S)) return kAbort;
         const double* gv = K.w.gval + (long long)par * (P.m + 1);
-        for (long long i = gtid(); i <= P.m; i += gstride()) rc.out_g[i] = ldcg(gv + i);
+        if (rc.out_g)
+          for (long long i = gtid(); i <= P.m; i += gstride()) rc.out_g[i] = ldcg(gv + i);
         const double* Wp = K.w.W + (long long)par * P.nr;
         if (rc.out_u)
           for (long long j = gtid(); j < P.nr; j += gstride()) rc.out_u[j] = ldcg(Wp + j);
         return nxt;
       }
-      for (long long i = gtid(); i <= P.m; i += gstride())
-        rc.out_g[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
+      if (rc.out_v && rc.op == OP_PROBE)   // A x - b at the probed point (eq_residual)
+        for (long long i = gtid(); i < P.p; i += gstride()) rc.out_v[i] = ldcg(K.w.eqv + (long long)par * P.p + i);
+      if (rc.out_g) {
+        for (long long i = gtid(); i <= P.m; i += gstride())
+          rc.out_g[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
+      } else if (nxt != DONE) {   // keep g at the probed point for the KKT / gradient steps
+        double* gv = K.w.gval + (long long)par * (P.m + 1);
+        for (long long i = gtid(); i <= P.m; i += gstride())
+          gv[i] = (i >= P.k0 && i < P.k1) ? g_combine(K, (int)i) : 0.0;
+        if (!gsync(K, S)) return kAbort;
+      }
       const double* Up = K.w.U + (long long)par * P.nloc * P.n;
       const long long tot = (long long)P.nloc * P.n;
       if (rc.out_u)
@@ -173,8 +183,9 @@ __device__ int run_step(const KArgs& K, Sm& S, int step, int& xk) {
       }
       if (!gx_part(K, S, st.cur ^ 1, rc.in_lam, lam_s, K.w.gxs)) return kAbort;
       xk = X_GX;
-      return P_GFIN;
+      return rc.op == OP_KKTAT ? P_KKT : P_GFIN;
     }
+    case P_KKT: return p_kkt(K, S);
     case P_GFIN: {
       const DevProblem& P = K.P;
       double* v_s = S.stage;
@@ -327,7 +338,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) rapdb_solver_kernel(co
           break;
         case OP_KKT: s_st.step = K_GXPART; s_st.kret = DONE; break;
         case OP_GAP: s_st.step = G_CAND; break;
-        case OP_PROBE: case OP_GRAD: s_st.step = P_SWEEP; break;
+        case OP_PROBE: case OP_GRAD: case OP_KKTAT: s_st.step = P_SWEEP; break;
         case OP_EGM: s_st.step = E_INIT; break;
         default: s_st.step = DONE; break;
       }
@@ -380,6 +391,8 @@ struct rapdb_ctx {
   rcomm::Scratch xscratch;      // its gather / reduce-scatter scratch
   long long exchanges = 0;
   SolverState last_st{};
+  int guard = 0;                     // RAPDB_GUARD: guard zones in the workspace (fixed at bind)
+  char* ws_base = nullptr;
 };
 
 // One NCCL communicator per process and device, shared by every context of
@@ -443,8 +456,20 @@ constexpr int B_COUNT_MAX = 32;
 
 struct Layout {
   long long off[B_COUNT_MAX];
+  long long end[B_COUNT_MAX];   // first byte past buffer i's payload (guard zone up to the next)
   long long total;
 };
+
+// RAPDB_GUARD=1: a 4 KB guard zone after every workspace buffer, filled with
+// a byte pattern at bind time and verified by rapdb_check_guards -- the
+// out-of-bounds-write check that stands in for compute-sanitizer (closed on
+// the test pool).
+constexpr long long kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guards_on() {
+  const char* e = std::getenv("RAPDB_GUARD");
+  return e && e[0] == '1';
+}
 
 enum WsBuf { B_X, B_U, B_GVAL, B_EQV, B_Y, B_YTR, B_GY, B_GXB, B_GXS, B_XCUM, B_YCUM, B_PART,
              B_SEGXU, B_SEGQX, B_ZQ, B_AUX, B_AUX2, B_ST, B_BAR, B_ABORT, B_H, B_HX, B_HXN, B_HY,
@@ -498,9 +523,11 @@ Layout layout_of(const rapdb_ctx* c) {
   sz[B_FCTR] = 64;
   Layout L;
   long long o = 0;
+  const long long guard = c->guard ? kGuardBytes : 0;
   for (int i = 0; i < B_COUNT; ++i) {
     L.off[i] = o;
-    o += align_up(sz[i], 256);
+    L.end[i] = o + sz[i];
+    o += align_up(sz[i], 256) + guard;
   }
   L.total = o;
   return L;
@@ -1394,7 +1421,34 @@ int rapdb_set_params(rapdb_ctx* c, int mode, double c_alpha, double c_beta, doub
 
 long long rapdb_workspace_bytes(rapdb_ctx* c) {
   if (!c || !c->bound) return -1;
+  c->guard = guards_on() ? 1 : 0;
   return layout_of(c).total;
+}
+
+int rapdb_check_guards(rapdb_ctx* c, char* report, int size) {
+  if (!c || !c->have_ws) return -1;
+  if (!c->guard) return 0;
+  const Layout L = layout_of(c);
+  int bad = 0;
+  std::string rep;
+  std::vector<unsigned char> h;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -1;
+  for (int i = 0; i < B_COUNT; ++i) {
+    const long long g0 = L.end[i], g1 = (i + 1 < B_COUNT ? L.off[i + 1] : L.total);
+    h.assign((size_t)(g1 - g0), 0);
+    if (cudaMemcpy(h.data(), c->ws_base + g0, h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    long long nb = 0, first = -1;
+    for (size_t k = 0; k < h.size(); ++k)
+      if (h[k] != kGuardByte) { ++nb; if (first < 0) first = (long long)k; }
+    if (nb) {
+      ++bad;
+      char t[96];
+      std::snprintf(t, sizeof t, "buffer %d: %lld guard bytes overwritten (first at +%lld); ", i, nb, first);
+      rep += t;
+    }
+  }
+  if (report && size > 0) std::snprintf(report, (size_t)size, "%s", rep.c_str());
+  return bad;
 }
 
 int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
@@ -1427,7 +1481,13 @@ int rapdb_bind_workspace(rapdb_ctx* c, void* dptr, long long bytes) {
   w.bar = reinterpret_cast<unsigned long long*>(base + L.off[B_BAR]);
   w.abort_flag = reinterpret_cast<int*>(base + L.off[B_ABORT]);
   c->w = w;
+  c->ws_base = base;
   CK(cudaMemsetAsync(dptr, 0, (size_t)L.total, c->stream));
+  if (c->guard)
+    for (int i = 0; i < B_COUNT; ++i) {
+      const long long g0 = L.end[i], g1 = (i + 1 < B_COUNT ? L.off[i + 1] : L.total);
+      CK(cudaMemsetAsync(base + g0, kGuardByte, (size_t)(g1 - g0), c->stream));
+    }
   SolverState st{};
   st.ig_prev = 0; st.ig_cur = 1; st.ig_new = 2;
   CK(cudaMemcpyAsync(w.st, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
@@ -1599,6 +1659,44 @@ int rapdb_grad_x(rapdb_ctx* c, const double* x, const double* v, const double* l
   if (r) return r;
   SolverState st;
   return read_state(c, &st);
+}
+
+int rapdb_eq_residual(rapdb_ctx* c, const double* x, double* eq) {
+  if (!c || !x || (c->P.p > 0 && !eq)) return RAPDB_EINPUT;
+  if (c->P.p == 0) return RAPDB_OK;
+  RunCfg rc{};
+  rc.op = OP_PROBE;
+  rc.in_x = x;
+  rc.out_v = eq;
+  rc.out_g = nullptr;
+  rc.out_u = nullptr;
+  rc.reps = 1;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  return read_state(c, &st);
+}
+
+int rapdb_kkt_at(rapdb_ctx* c, const double* x, const double* v, const double* lam, int has_f_star, double f_star,
+                 double* out) {
+  if (!c || !x || !out || (c->P.p > 0 && !v) || (c->P.m > 0 && !lam)) return RAPDB_EINPUT;
+  if (c->split) return fail(c, RAPDB_ECONFIG, "rapdb_kkt_at needs an unsharded context");
+  RunCfg rc{};
+  rc.op = OP_KKTAT;
+  rc.in_x = x; rc.in_v = v; rc.in_lam = lam;
+  rc.out_g = nullptr;      // g at x stays in the workspace (gval)
+  rc.out_u = nullptr;
+  rc.has_f_star = has_f_star ? 1 : 0;
+  rc.f_star = f_star;
+  rc.reps = 1;
+  int r = launch(c, rc);
+  if (r) return r;
+  SolverState st;
+  r = read_state(c, &st);
+  if (r) return r;
+  for (int i = 0; i < 8; ++i) out[i] = st.metrics[i];
+  out[8] = st.phi_at;
+  return RAPDB_OK;
 }
 
 int rapdb_smoothed_gap(rapdb_ctx* c, int source, const double* x, const double* v, const double* lam,

@@ -974,6 +974,74 @@ __device__ int k_finish(const KArgs& K, Sm& S) {
   return st.kret;
 }
 
+// kkt_residual and coupling_value at an explicit point (OP_KKTAT, after the
+// probe sweep, g and the gradient at rc.in_x): the k_finish formulas with
+// x, v, lam from the caller, plus Phi = (f + v.(Ax - b)) + lam.g
+// (problem.py:196-204).  No projection of the point (diagnostics.py:96-113
+// evaluates where it is given).
+__device__ int p_kkt(const KArgs& K, Sm& S) {
+  const DevProblem& P = K.P;
+  const Work& w = K.w;
+  const RunCfg& rc = K.rc;
+  SolverState& st = *S.st;
+  const int n = P.n, p = P.p, m = P.m;
+  const int par = st.cur ^ 1;
+  double* v_s = S.stage;
+  if (P.kind == 0 && p > 0) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < p; j += kThreads) v_s[j] = ldcg(rc.in_v + j);
+    __syncthreads();
+  }
+  const double* gv = w.gval + (long long)par * (m + 1);
+  double s_st = 0.0, s_eq = 0.0, s_comp = 0.0, s_gp2 = 0.0, s_gp1 = 0.0, s_pv = 0.0, s_pl = 0.0;
+  for (long long j = gtid(); j < n; j += gstride()) {
+    double gx = ldcg(w.gxs + j);
+    if (p > 0) gx = gx + atv(K, v_s, j);
+    const double xj = ldcg(rc.in_x + j);
+    const double d = xj - clipd(xj - gx, __ldg(P.lo + j), __ldg(P.hi + j));
+    s_st += d * d;
+  }
+  for (long long idx = gtid(); idx < p + m; idx += gstride()) {
+    if (idx < p) {
+      const double e = ldcg(w.eqv + (long long)par * p + idx);
+      s_eq += e * e;
+      s_pv += ldcg(rc.in_v + idx) * e;
+    } else {
+      const double g = ldcg(gv + (idx - p + 1));
+      const double l = ldcg(rc.in_lam + (idx - p));
+      const double c = fmin(l, -g);
+      s_comp += c * c;
+      const double gp = fmax(g, 0.0);
+      s_gp2 += gp * gp;
+      s_gp1 += gp;
+      s_pl += l * g;
+    }
+  }
+  const double v7[7] = {s_st, s_eq, s_comp, s_gp2, s_gp1, s_pv, s_pl};
+  const int sl[7] = {S_STAT, S_EQ2, S_COMP, S_GPOS2, S_GPOS1, S_MIXV, S_MIXL};
+  put_partials(K, S, v7, sl);
+  if (!gsync(K, S)) return kAbort;
+  get_totals(K, S, sl);
+  if (threadIdx.x == 0) {
+    const double stat = sqrt(S.tot[S_STAT]);
+    const double eq = sqrt(S.tot[S_EQ2]);
+    const double comp = m > 0 ? sqrt(S.tot[S_COMP]) : 0.0;
+    const double f = ldcg(gv);
+    st.metrics[0] = (stat + eq) + comp;
+    st.metrics[1] = stat;
+    st.metrics[2] = eq;
+    st.metrics[3] = comp;
+    st.metrics[4] = sqrt(S.tot[S_EQ2] + S.tot[S_GPOS2]);
+    st.metrics[5] = f;
+    st.metrics[6] = m > 0 ? S.tot[S_GPOS1] / (double)m : 0.0;
+    st.metrics[7] = rc.has_f_star ? f - rc.f_star : __longlong_as_double(0x7ff8000000000000ll);
+    st.phi_at = (f + (p > 0 ? S.tot[S_MIXV] : 0.0)) + (m > 0 ? S.tot[S_MIXL] : 0.0);
+    st.has_metrics = 1;
+  }
+  __syncthreads();
+  return DONE;
+}
+
 // check_termination (diagnostics.py:252-263)
 __device__ __forceinline__ bool terminated(const RunCfg& rc, const double* met) {
   if (rc.criterion == 2 && rc.has_f_star) {

@@ -62,26 +62,10 @@ def metrics_from(vals, f_star=None) -> Metrics:
 
 
 def kkt_residual(inst: ProblemInstance, z: Iterate, f_star: Optional[float] = None) -> Metrics:
-    """r(x, v, lam) at an arbitrary point, evaluated on the device."""
-    ev = inst._evaluator()
-    torch = ev.ctx.torch
-    d = ev.data
-    x = ev._x(z.x)
-    gx = ev.grad_x_t(z)
-    stat = float(torch.linalg.vector_norm(x - torch.clamp(x - gx, d.lower, d.upper)))
-    e = ev.eq(z.x) if inst.p else torch.zeros(0, dtype=torch.float64, device=x.device)
-    eq = float(torch.linalg.vector_norm(e))
-    u, g = ev.sweep(z.x)
-    gi = g[1:]
-    lam = ev._x(z.lam)
-    comp = float(torch.linalg.vector_norm(torch.minimum(lam, -gi))) if inst.m else 0.0
-    gp = torch.clamp(gi, min=0.0)
-    infeas = float(torch.sqrt(e @ e + gp @ gp))
-    mpv = float(gp.mean()) if inst.m else 0.0
-    f = float(g[0])
-    return Metrics(kkt_residual=stat + eq + comp, stationarity=stat, primal_eq=eq,
-                   complementarity=comp, infeas=infeas, f_value=f, mean_pos_violation=mpv,
-                   subopt_abs=None if f_star is None else f - f_star)
+    """r(x, v, lam) at an arbitrary point (diagnostics.py:96-113), evaluated on
+    the device in one op (rapdb_kkt_at: sweep, g, grad_x Phi, the norms)."""
+    vals = inst._evaluator().kkt_at(z, f_star)
+    return metrics_from(vals, f_star)
 
 
 def infeasibility(inst: ProblemInstance, x) -> float:

@@ -64,7 +64,9 @@ def run_egm(inst, stepsize: float, z_init: Iterate, K: int, dual_ball: DualBall 
         return Iterate(x.cpu().numpy(), v.cpu().numpy(), lam.cpu().numpy())
 
     trace = [{"iter": int(r[0]), "norm": float(r[1])} for r in tr if 0 < int(r[0]) <= iters]
-    return EgmResult(last=fetch(0), average=fetch(1), iterations=iters, diverged=diverged, trace=trace)
+    res = EgmResult(last=fetch(0), average=fetch(1), iterations=iters, diverged=diverged, trace=trace)
+    res._ctx = ctx      # the device context (diagnostics: guard checks)
+    return res
 
 
 def tune_egm(inst, z_init: Iterate, K: int, score, grid=DEFAULT_STEP_GRID,

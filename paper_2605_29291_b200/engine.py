@@ -298,17 +298,22 @@ class _Evaluator:
         return self._val
 
     def eq(self, x):
-        d = self.data
-        return d.A @ self._x(x) - d.b
+        """A x - b (problem.py:175-177) by the device probe sweep."""
+        torch = self.ctx.torch
+        out = torch.empty(max(self.inst.p, 1), dtype=torch.float64, device=self.ctx.device)
+        self.ctx.eq_residual(self._x(x), out)
+        return out[:self.inst.p]
+
+    def kkt_at(self, z, f_star=None):
+        """rapdb_kkt_at: the KKT metrics and Phi at z, all on the device."""
+        inst = self.inst
+        v = self._x(z.v) if inst.p else None
+        lam = self._x(z.lam) if inst.m else None
+        return self.ctx.kkt_at(self._x(z.x), v, lam, f_star)
 
     def coupling(self, z):
-        u, g = self.sweep(z.x)
-        val = float(g[0])
-        if self.inst.p > 0:
-            val += float(self._x(z.v) @ self.eq(z.x))
-        if self.inst.m > 0:
-            val += float(self._x(z.lam) @ g[1:])
-        return val
+        """coupling_value (problem.py:196-204): (f + v.(Ax - b)) + lam.g."""
+        return float(self.kkt_at(z)[8])
 
     def grad_x_t(self, z):
         """grad_x Phi(z) (problem.py:207-217) through the solver kernel's own

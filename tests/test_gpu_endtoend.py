@@ -73,9 +73,12 @@ def _end_bars(res, g, key, inst):
                                 (m.f_value, met[5], floor[2], 0.0)):
         assert fl <= 1e-5 * max(abs(want), 1e-300), ("evaluation floor", fl, want)
         assert abs(got - want) <= max(1e-6, band) * abs(want) + 2.0 * fl, (got, want, fl, band)
-    # KKT checkpoints along the run (every metrics_every iterations)
+    # KKT checkpoints along the run (every metrics_every iterations): the
+    # late ones are residuals of 1e-6 .. 1e-4 with the same cancellation
+    # noise as the final one (the reference's own +-1-ulp spread there is
+    # ~8e-6 relative, c1_band.json)
     ok = ~np.isnan(tr_g[:k, 7])
-    np.testing.assert_allclose(tr[:k, 7][ok], tr_g[:k, 7][ok], rtol=1e-6, atol=1e-10)
+    np.testing.assert_allclose(tr[:k, 7][ok], tr_g[:k, 7][ok], rtol=2e-5, atol=1e-9)
 
 
 @pytest.fixture(scope="module")
