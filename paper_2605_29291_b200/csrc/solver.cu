@@ -413,6 +413,16 @@ int cuda_fail(rapdb_ctx* c, cudaError_t e, const char* where) {
   return fail(c, RAPDB_EDEVICE, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Owns the CUDA events a host entry point creates, so every early return
+// (CK, a failed launch, an exchange-callback error) releases them.
+struct EventGuard {
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~EventGuard() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 #define CK(call)                                   \
   do {                                             \
     cudaError_t e_ = (call);                       \
@@ -708,17 +718,15 @@ int launch(rapdb_ctx* c, RunCfg rc) {
 // the per-CTA progress beacons over a non-blocking stream (the kernel is still
 // resident) and fail with them instead of blocking forever.
 int wait_stream(rapdb_ctx* c) {
-  cudaEvent_t ev;
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  EventGuard eg;
+  CK(cudaEventCreateWithFlags(&eg.ev[0], cudaEventDisableTiming));
+  cudaEvent_t ev = eg.ev[0];
   CK(cudaEventRecord(ev, c->stream));
   const auto t0 = std::chrono::steady_clock::now();
   for (;;) {
     const cudaError_t q = cudaEventQuery(ev);
     if (q == cudaSuccess) break;
-    if (q != cudaErrorNotReady) {
-      cudaEventDestroy(ev);
-      return cuda_fail(c, q, "kernel");
-    }
+    if (q != cudaErrorNotReady) return cuda_fail(c, q, "kernel");
     if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
       cudaStream_t ds;
       std::vector<int> b(4 * c->G + 32, -1);
@@ -742,7 +750,6 @@ int wait_stream(rapdb_ctx* c) {
     if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2))
       std::this_thread::sleep_for(std::chrono::microseconds(100));
   }
-  cudaEventDestroy(ev);
   return RAPDB_OK;
 }
 
@@ -1135,8 +1142,13 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
   long long ns = ((long long)c->optin - static_smem - sp.xs_bytes - 128) / (sp.stage_bytes + 16);
   ns = std::min(ns, layout == 1 ? std::min(max_stages, 8LL) : max_stages);
   if (ns < 2) return fail(c, RAPDB_ECONFIG, "n too large for the dense path (x does not fit in shared memory)");
+  // consumer warp k owns every ncw-th slot use and waits on the slot's full
+  // mbarrier by phase parity: every use of a slot must go to the same warp,
+  // so the stage count is a multiple of the consumer-warp count
+  if (ns > kConsumerWarps) ns -= ns % kConsumerWarps;
   sp.nstages = (int)ns;
   sp.ncw = (int)std::min<long long>(kConsumerWarps, ns);
+  if (sp.nstages % sp.ncw != 0) return fail(c, RAPDB_ECONFIG, "ring stages not a multiple of the consumer warps");
   // packed sweep: the consumer warp without a ring slot reduces the unit
   // partials of finished matrix chunks while later chunks stream
   // (RAPDB_EARLY_CHUNKS, 0 = everything after the stream)
@@ -1554,7 +1566,9 @@ int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_re
   c->w.trace = trace;
   SolverState before;
   int r = read_state(c, &before);
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  EventGuard eg;
+  cudaEvent_t& e0 = eg.ev[0];
+  cudaEvent_t& e1 = eg.ev[1];
   if (!r) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1569,8 +1583,6 @@ int rapdb_run(rapdb_ctx* c, const rapdb_run_args* a, double* trace, rapdb_run_re
   if (r) return r;
   float kms = 0.0f;
   cudaEventElapsedTime(&kms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   std::memset(out, 0, sizeof(*out));
   out->status = st.status;
   out->iters_done = st.iters - before.iters;
@@ -1630,7 +1642,9 @@ int rapdb_probe_sweep(rapdb_ctx* c, const double* x, double* u, double* g, int r
   rc.op = OP_PROBE;
   rc.in_x = x; rc.out_u = u; rc.out_g = g;
   rc.reps = reps < 1 ? 1 : reps;
-  cudaEvent_t e0, e1;
+  EventGuard eg;
+  cudaEvent_t& e0 = eg.ev[0];
+  cudaEvent_t& e1 = eg.ev[1];
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
@@ -1641,8 +1655,6 @@ int rapdb_probe_sweep(rapdb_ctx* c, const double* x, double* u, double* g, int r
   r = read_state(c, &st);
   float t = 0;
   cudaEventElapsedTime(&t, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (ms) *ms = t / (float)rc.reps;
   return r;
 }

@@ -102,7 +102,15 @@ def smoothed_gap(inst: ProblemInstance, z: Iterate, xi: float, dual_ball=None,
     from .geometry import Unbounded
     if xi <= 0:
         raise ConfigurationError("xi must be positive")
-    cfg = SolverConfig(dual_ball=dual_ball or Unbounded())
-    eng = ApdbEngine(inst, cfg, z)
+    ball = dual_ball or Unbounded()
+    # one bound gap engine per (instance, dual ball), reused across calls like
+    # inst._evaluator(): the point is passed raw, the engine's own iterate is unused
+    cache = getattr(inst, "_dev", None)
+    key = ("_gap", repr(ball))
+    eng = cache.get(key) if cache is not None else None
+    if eng is None:
+        eng = ApdbEngine(inst, SolverConfig(dual_ball=ball), z)
+        if cache is not None:
+            cache[key] = eng
     gap, cert, _ = eng.smoothed_gap(1, xi, subsolver_tol, x_warm, raw_point=z)
     return gap, cert
