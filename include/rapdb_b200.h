@@ -199,62 +199,73 @@ long long rapdb_packed_doubles(int n);
 int rapdb_pack_symmetric(int n, long long count, const double* src, long long ld,
                          long long mat_stride, double* dst, void* stream);
 
+/* Sliced ELLPACK (slice height 32) of a sparse operand, all arrays on the
+ * device: slots are grouped 32 to a slice (one warp, lane = slot); entry t of
+ * slot s lives at sp[s / 32] + 32 t + s % 32, a slice being as wide as its
+ * longest slot (shorter slots are padded; len says where each stops).  Every
+ * slot's entries are in the operand's stored order, which is the order they
+ * are summed in (no FMA: the bits of scipy's csr_matvec).                   */
+typedef struct rapdb_sell {
+  long long nslots;      /* multiple of 32                                   */
+  const long long* sp;   /* [nslots / 32 + 1] entry offset of each slice     */
+  const int* idx;        /* [sp[nslots / 32]] gathered index of each entry   */
+  const double* val;     /* [sp[nslots / 32]]                                */
+  const int* len;        /* [nslots] entries of each slot                    */
+  const int* map;        /* [nslots] output index of each slot, -1 = padding;
+                            NULL where the slot number is the output index   */
+} rapdb_sell;
+
 /* Factored sparse problem data (BASELINE config 3): replaces a ProblemInstance
  * whose Q_i are sparse operators (_as_operator problem.py:31-40 keeps them as
  * CSR) with Q_i = R_i^T R_i, plus L linear inequality rows a_j x <= b_j that
  * the reference would hold as Q = 0 orthant constraints (problem.py:38-39:
  * an all-zero Q becomes an empty CSR).  Constraint order: m = mq + L, rows
  * 1..mq quadratic (q = C[1..mq], r = d[1..mq]), rows mq+1..m linear.
- *   R     CSR [nr x n] of the stacked R_0..R_mq: r_ptr[nr+1] (int64),
- *         r_col[nnz] (int32), r_val[nnz]; block i owns rows rblk[i]..rblk[i+1]
- *   R^T   CSR [n x nr] of the same matrix: rt_ptr[n+1], rt_row, rt_val
+ *   R     [nr x n], the stacked R_0..R_mq; block i owns rows rblk[i]..rblk[i+1].
+ *         Sell with idx = column and the slots laid out per block in chunks
+ *         of 128 rows: slot = 128 * (chunks of the earlier blocks) + row
+ *         inside the block, each block padded to a multiple of 128 slots
+ *         (nslots = 128 * sum_i ceil(rows_i / 128)), map = NULL
  *   rmat  [nr] block id of each stacked row (int32)
  *   rblk  HOST [mq+2] row offsets of the blocks (rblk[0] = 0, rblk[mq+1] = nr)
  *   C     [(mq+1) x n] linear terms, d [mq+1] constants
- *   A     CSR [L x n] (a_ptr[L+1], a_col, a_val), A^T CSR [n x L], b [L]
- * All other pointers are device pointers.  No equality block (p = 0), and
- * the smoothed gap is not available (its n x n H does not fit at this n):
- * adaptive restarts need a dense instance.  Dual balls are supported (the
- * trial multipliers are scaled in place after one norm reduction).
+ *   A     [L x n], Sell with idx = column, slot = row, nslots = L rounded up
+ *         to 32, map = NULL; b [L]
+ * All other pointers are device pointers.  R^T and A^T follow with
+ * rapdb_set_factored_transpose (required before any op).  No equality block
+ * (p = 0), and the smoothed gap is not available (its n x n H does not fit at
+ * this n): adaptive restarts need a dense instance.  Dual balls are supported
+ * (the trial multipliers are scaled in place after one norm reduction).
  * Equivalent to rapdb_bind_factored_range over the whole instance.          */
 int rapdb_bind_factored(rapdb_ctx* ctx, int n, int mq, int L, long long nr,
-                        const long long* r_ptr, const int* r_col, const double* r_val,
-                        const long long* rt_ptr, const int* rt_row, const double* rt_val,
-                        const int* rmat, const long long* rblk,
-                        const double* C, const double* d,
-                        const long long* a_ptr, const int* a_col, const double* a_val,
-                        const long long* at_ptr, const int* at_row, const double* at_val,
+                        const rapdb_sell* R, const int* rmat, const long long* rblk,
+                        const double* C, const double* d, const rapdb_sell* A,
                         const double* b, const double* lower, const double* upper, double mu);
 
 /* The same, holding only a constraint shard: blocks
  * [fb0, fb1) of the mq+1 quadratic blocks (R rows, rblk with fb1-fb0+1
  * entries, rmat LOCAL block ids, C and d rows fb0..fb1-1) and linear rows
- * [l0, l1) of the L (A, A^T with local row ids, b).  mq and L are the global
+ * [l0, l1) of the L (A with local row ids, b).  mq and L are the global
  * counts; x and the m multipliers are replicated.  The context exchanges the
  * gradient partial (n) and g (m+1, zero outside this rank's rows) per trial. */
 int rapdb_bind_factored_range(rapdb_ctx* ctx, int n, int mq, int L, int fb0, int fb1, int l0, int l1,
-                              long long nr,
-                              const long long* r_ptr, const int* r_col, const double* r_val,
-                              const long long* rt_ptr, const int* rt_row, const double* rt_val,
-                              const int* rmat, const long long* rblk,
-                              const double* C, const double* d,
-                              const long long* a_ptr, const int* a_col, const double* a_val,
-                              const long long* at_ptr, const int* at_row, const double* at_val,
+                              long long nr, const rapdb_sell* R, const int* rmat, const long long* rblk,
+                              const double* C, const double* d, const rapdb_sell* A,
                               const double* b, const double* lower, const double* upper, double mu);
 
-/* Row-phased layout of R^T for the gradient gather (after a factored bind;
- * optional -- the plain CSR passed to the bind is one untagged phase).  The
- * stacked rows are split into nph ranges ph_bounds[0..nph] (HOST, 0 .. nr);
- * pptr (device, [nph][n+1] int64) holds one CSR of R^T per phase over ONE
- * pair of entry arrays prow / pval (phase-major), so column j's phase-p
- * entries are [pptr[p (n+1) + j], pptr[p (n+1) + j + 1]) and walking the
- * phases in order walks the column in sorted row order.  Each phase's
- * gathers touch only its slice of the W-cache, which then stays in L2.
- * tagged: prow holds r | (local block of r) << 23 (needs nr <= 2^23, at most
- * 256 local blocks) and the gather weights W by the block's multiplier on the
- * fly instead of reading a separately weighted copy.                        */
-int rapdb_set_factored_transpose(rapdb_ctx* ctx, int nph, const long long* ph_bounds, const long long* pptr,
-                                 const int* prow, const double* pval, int tagged);
+/* The transposed operands of the gradient gather grad_x Phi = sum_i w_i
+ * (R_i^T W_i + c_i) + A^T mu (no atomics, fixed summation order), after a
+ * factored bind.  The stacked rows of R are split into nph <= 8 ROW PHASES
+ * ph_bounds[0..nph] (HOST, 0 .. nr) so that each phase gathers from an
+ * L2-sized slice of the W-cache; RT[ph] is the Sell of (rows of phase ph of
+ * R)^T: nslots = n rounded up to 32, the columns sorted by their entry count
+ * in the phase (map[slot] = column, every column exactly once), entries of a
+ * column in row order with idx = stacked row -- or, `tagged`, row | (local
+ * block of the row) << 23, which lets the gather weight W on the fly (needs
+ * nr <= 2^23 and at most 256 local blocks).  AT is the Sell of A^T (local
+ * rows) over the same kind of column slots.                                 */
+int rapdb_set_factored_transpose(rapdb_ctx* ctx, int nph, const long long* ph_bounds, const rapdb_sell* RT,
+                                 const rapdb_sell* AT, int tagged);
 
 /* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
  * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */

@@ -216,8 +216,8 @@ def load(path: str = LIB_PATH):
     lib.rapdb_exchange_count.argtypes = [P]
     lib.rapdb_exchange_count.restype = LL
     lib.rapdb_step_profile.argtypes = [P, C.POINTER(D), C.POINTER(LL), I]
-    lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 19 + [D]
-    lib.rapdb_bind_factored_range.argtypes = [P, I, I, I, I, I, I, I, LL] + [P] * 19 + [D]
+    lib.rapdb_bind_factored.argtypes = [P, I, I, I, LL] + [P] * 9 + [D]
+    lib.rapdb_bind_factored_range.argtypes = [P, I, I, I, I, I, I, I, LL] + [P] * 9 + [D]
     lib.rapdb_egm.argtypes = [P, D, LL, I, P, C.POINTER(LL), C.POINTER(I)]
     lib.rapdb_peer_region_bytes.argtypes = [P]
     lib.rapdb_peer_region_bytes.restype = LL
@@ -234,13 +234,19 @@ def load(path: str = LIB_PATH):
     lib.rapdb_comm_destroy.restype = None
     lib.rapdb_comm_allreduce_ordered.argtypes = [P, P, LL, P]
     lib.rapdb_set_comm_exchange.argtypes = [P, P, I]
-    lib.rapdb_set_factored_transpose.argtypes = [P, I, P, P, P, P, I]
+    lib.rapdb_set_factored_transpose.argtypes = [P, I, P, P, P, I]
     lib.rapdb_spectral_norm.argtypes = [P, LL, LL, LL, I, D, P, C.POINTER(D)]
     lib.rapdb_kkt_at.argtypes = [P, P, P, P, I, D, C.POINTER(D)]
     lib.rapdb_eq_residual.argtypes = [P, P, P]
     lib.rapdb_check_guards.argtypes = [P, C.c_char_p, I]
     _lib = lib
     return lib
+
+
+class SellDescriptor(C.Structure):
+    """``rapdb_sell`` of include/rapdb_b200.h (device pointers)."""
+    _fields_ = [("nslots", C.c_longlong), ("sp", C.c_void_p), ("idx", C.c_void_p), ("val", C.c_void_p),
+                ("len", C.c_void_p), ("map", C.c_void_p)]
 
 
 def _ptr(t) -> Optional[int]:
@@ -356,17 +362,14 @@ class Context:
             rblk = np.ascontiguousarray(data.rblk, dtype=np.int64)
             self._check(self.lib.rapdb_bind_factored_range(
                 self.h, data.n, data.mq, data.L, data.k0, data.k1, data.l0, data.l1, data.nr,
-                _ptr(data.r_ptr), _ptr(data.r_col), _ptr(data.r_val),
-                _ptr(data.rt_ptr), _ptr(data.rt_row), _ptr(data.rt_val),
-                _ptr(data.rmat), rblk.ctypes.data_as(C.c_void_p), _ptr(data.C), _ptr(data.d),
-                _ptr(data.a_ptr), _ptr(data.a_col), _ptr(data.a_val),
-                _ptr(data.at_ptr), _ptr(data.at_row), _ptr(data.at_val),
+                C.byref(data.sell_R.descriptor()), _ptr(data.rmat), rblk.ctypes.data_as(C.c_void_p),
+                _ptr(data.C), _ptr(data.d), C.byref(data.sell_A.descriptor()),
                 _ptr(data.b), _ptr(data.lower), _ptr(data.upper), float(data.mu)))
-            if getattr(data, "rt_nph", None):
-                bounds = np.ascontiguousarray(data.rt_bounds, dtype=np.int64)
-                self._check(self.lib.rapdb_set_factored_transpose(
-                    self.h, int(data.rt_nph), bounds.ctypes.data_as(C.c_void_p), _ptr(data.rt_ptr),
-                    _ptr(data.rt_row), _ptr(data.rt_val), int(data.rt_tag)))
+            bounds = np.ascontiguousarray(data.rt_bounds, dtype=np.int64)
+            rt = (SellDescriptor * int(data.rt_nph))(*[t.descriptor() for t in data.sell_RT])
+            self._check(self.lib.rapdb_set_factored_transpose(
+                self.h, int(data.rt_nph), bounds.ctypes.data_as(C.c_void_p), rt,
+                C.byref(data.sell_AT.descriptor()), int(data.rt_tag)))
         else:
             k1 = data.m + 1 if k1 is None else k1
             zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)

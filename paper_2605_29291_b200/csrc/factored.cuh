@@ -7,23 +7,28 @@
 // and the linear block A x <= b enters as orthant constraints with Q = 0
 // (g = A x - b, multipliers mu = lam[mq:]).
 //
-// Kernels (host-launched at a stop of the persistent kernel; the same
-// arithmetic also exists in-kernel for RAPDB_FAC_HOST=0):
-//   gradient     fac_grad_kernel: warps in two roles -- 8 lanes per column
-//                walk its R^T entries (gather w_blk(r) W[r]) and A^T mu,
-//                while every 4th warp streams the block-weighted c_i part;
+// Kernels (host-launched at a stop of the persistent kernel -- a request in
+// the solver state, like an exchange point -- because these latency-bound
+// gathers want more resident warps and registers than the persistent CTAs have):
+//   gradient     fac_grad_kernel, one launch per row phase of R^T: warps in
+//                two roles -- a warp per 32-column slice of R^T (lane = column,
+//                gather w_blk(r) W[r] in row order) and of A^T, while every
+//                4th warp streams the block-weighted c_i part;
 //                fac_grad_fin_kernel combines them into grad_x Phi and, in a
 //                fused yx trial, takes the primal step x_new = clip(x_k -
 //                tau grad) with the D_p / <grad, dx> partials
 //   row pass     fac_row_kernel: warps in two roles -- W = R x (+ |W_i|^2
-//                partials per 128-row chunk) and A x - b, and the c_i . x
-//                chunk partials -- so the pure HBM stream over C runs beside
-//                the gather-bound CSR rows
-// The CSR passes are bound by the L2 request rate of their 8-byte gathers
-// (~65 M per pass at C3; tools/csr_probe2.cu), not by HBM bytes: fusing the
-// dense C streams into them costs little and saves a pass and a stop.
-// Per yx trial ~2.2 GB (R and R^T 780 MB each, C 520 MB, A, A^T) and one
-// stop of the persistent kernel.  Every reduction has a fixed order.
+//                partials per 128-row chunk) and A x - b (lane = row), and the
+//                c_i . x chunk partials -- so the pure HBM stream over C runs
+//                beside the gather-bound sparse rows
+// The sparse operands are sliced ELLPACK (rapdb_dev.cuh Sell): coalesced
+// streams with no staging, each row / column summed in stored order without
+// FMA.  The passes are bound by the L1 wavefront rate of their 8-byte gathers
+// (~65 M per pass at C3, one line lookup each; tools/gather_probe.cu), not by
+// HBM bytes: fusing the dense C streams into them costs little and saves a
+// pass and a stop.  Per yx trial ~2.7 GB (R and R^T 780 MB each, C 2 x 520 MB,
+// A, A^T) and one stop of the persistent kernel.  Every reduction has a fixed
+// order.
 #pragma once
 #include "solver_kernel.cuh"
 
@@ -34,69 +39,75 @@ __device__ __forceinline__ long long nwarps() { return (long long)gridDim.x * kW
 
 constexpr int kWChunk = 128;    // rows of W per |W_i|^2 partial (inside one block)
 constexpr int kCxCols = 1024;   // columns per c_i . x partial
-constexpr int kGxLanes = 8;     // lanes per column in the gradient
+constexpr int kRowU = 5;       // gathers in flight per lane in the row pass (C3: 10 per row of R)
 
-// sum_k val[k] * x[col[k]] over CSR row r, in stored order, no FMA (the
-// operation order of scipy's csr_matvec, so W = R x matches the factored
-// restatement bit for bit); evict-first streams keep the gathered x in L2
-__device__ __forceinline__ double csr_row_dot(const long long* __restrict__ ptr, const int* __restrict__ col,
-                                              const double* __restrict__ val, const double* x, long long r,
-                                              uint64_t ef) {
-  long long k = __ldg(ptr + r);
-  const long long k1 = __ldg(ptr + r + 1);
-  double s = 0.0;
-  for (; k + 8 <= k1; k += 8) {
-    int c[8];
-    double v[8], xv[8];
+// One slice of a Sell operand against a gathered vector: lane l folds the
+// entries of slot 32 * slice + l in stored order without FMA -- the operation
+// order of scipy's csr_matvec, so W = R x and the R^T / A^T column sums match
+// the factored restatement bit for bit -- starting from s.  The t-th loads of
+// val / idx are one coalesced access per warp (no shared-memory staging), U
+// gathers in flight per lane; evict-first streams keep the gathered vector in
+// L2.  The CSR passes are bound by the L1 wavefront rate of their 8-byte
+// gathers (one 128-byte line lookup per lane: ~245 G gathers/s measured on a
+// B200, tools/gather_probe.cu), so every wavefront spent on anything else --
+// staging stores, bank-conflicted shared loads, uncoalesced streams -- is time.
+template <int U>
+__device__ __forceinline__ double sell_dot(const Sell& M, long long slice, const double* x, double s, uint64_t ef) {
+  const int lane = threadIdx.x & 31;
+  const long long base = __ldg(M.sp + slice);
+  const int width = (int)((__ldg(M.sp + slice + 1) - base) >> 5);
+  const int len = __ldg(M.len + slice * 32 + lane);
+  const int* ip = M.idx + base + lane;
+  const double* vp = M.val + base + lane;
+  for (int t0 = 0; t0 < width; t0 += U) {
+    int c[U];
+    double v[U], xv[U];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) { c[t] = ld_stream(col + k + t, ef); v[t] = ld_stream(val + k + t, ef); }
+    for (int u = 0; u < U; ++u)
+      if (t0 + u < len) { c[u] = ld_stream(ip + (long long)(t0 + u) * 32, ef); v[u] = ld_stream(vp + (long long)(t0 + u) * 32, ef); }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) xv[t] = ldcg(x + c[t]);
+    for (int u = 0; u < U; ++u)
+      if (t0 + u < len) xv[u] = ldcg(x + c[u]);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) s = __dadd_rn(s, __dmul_rn(v[t], xv[t]));
+    for (int u = 0; u < U; ++u)
+      if (t0 + u < len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
   }
-  for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(ld_stream(val + k, ef), ldcg(x + ld_stream(col + k, ef))));
   return s;
 }
 
-// The same row sums with coalesced CSR loads (standalone kernel): a warp
-// takes 32 consecutive rows [r0, min(r0 + 32, rend)), copies their
-// contiguous (val, col) range into its shared-memory buffer (CAP entries per
-// pass, evict-first), then each lane sums its own row in stored order
-// without FMA from shared memory, 4 gathers in flight -- the bits of
-// csr_row_dot.  The fastest of the C3 row-pass variants measured
-// (tools/csr_probe.cu, tools/csr_probe2.cu: 0.30 ms for R x).
-constexpr int kStageCap = 320;
-__device__ __forceinline__ double csr_group32(const long long* __restrict__ ptr, const int* __restrict__ col,
-                                              const double* __restrict__ val, const double* x, long long r0,
-                                              long long rend, double* sv, int* sc, uint64_t ef) {
+constexpr int kRtTagShift = 23;
+constexpr int kRtRowMask = (1 << kRtTagShift) - 1;
+
+// The same over a slice of R^T with tagged rows: entry (r | blk << 23, v)
+// adds v * (wq[blk] * W[r]).  A zero weight adds +-0 to a sum that starts at
+// +0 -- a no-op -- so its gather is skipped: the pass costs the active blocks.
+template <int U>
+__device__ __forceinline__ double sell_dot_tagged(const Sell& M, long long slice, const double* W, const double* wq,
+                                                  double s, uint64_t ef) {
   const int lane = threadIdx.x & 31;
-  const long long r = r0 + lane;
-  const long long kb = __ldg(ptr + r0);
-  const long long ke = __ldg(ptr + min(r0 + 32, rend));
-  long long k = r < rend ? __ldg(ptr + r) : ke;
-  const long long k1 = r < rend ? __ldg(ptr + r + 1) : ke;
-  double s = 0.0;
-  for (long long base = kb; base < ke; base += kStageCap) {
-    const long long lim = min(base + kStageCap, ke);
-    for (long long e = base + lane; e < lim; e += 32) {
-      sv[e - base] = ld_stream(val + e, ef);
-      sc[e - base] = ld_stream(col + e, ef);
-    }
-    __syncwarp();
-    const long long kend = min(k1, lim);
-    for (; k + 4 <= kend; k += 4) {
-      double xv[4], vv[4];
+  const long long base = __ldg(M.sp + slice);
+  const int width = (int)((__ldg(M.sp + slice + 1) - base) >> 5);
+  const int len = __ldg(M.len + slice * 32 + lane);
+  const int* ip = M.idx + base + lane;
+  const double* vp = M.val + base + lane;
+  for (int t0 = 0; t0 < width; t0 += U) {
+    int c[U];
+    double v[U], xv[U], wt[U];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        vv[t] = sv[k + t - base];
-        xv[t] = ldcg(x + sc[k + t - base]);
+    for (int u = 0; u < U; ++u) {
+      wt[u] = 0.0;
+      if (t0 + u < len) {
+        c[u] = ld_stream(ip + (long long)(t0 + u) * 32, ef);
+        v[u] = ld_stream(vp + (long long)(t0 + u) * 32, ef);
+        wt[u] = wq[c[u] >> kRtTagShift];
       }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) s = __dadd_rn(s, __dmul_rn(vv[t], xv[t]));
     }
-    for (; k < kend; ++k) s = __dadd_rn(s, __dmul_rn(sv[k - base], ldcg(x + sc[k - base])));
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (wt[u] != 0.0) xv[u] = ldcg(W + (c[u] & kRtRowMask));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (wt[u] != 0.0) s = __dadd_rn(s, __dmul_rn(v[u], __dmul_rn(wt[u], xv[u])));
   }
   return s;
 }
@@ -133,17 +144,7 @@ __device__ __forceinline__ void fac_wq(const DevProblem& P, const double* lam, d
   }
 }
 
-constexpr int kRtTagShift = 23;
-constexpr int kRtRowMask = (1 << kRtTagShift) - 1;
-
-// w_blk(r) W[r] of one R^T entry (tagged rows), or the weighted W-cache
-template <bool TAG>
-__device__ __forceinline__ double rt_weighted(const double* Wsrc, const double* wq, int idx) {
-  if (TAG) return wq[idx >> kRtTagShift] * ldcg(Wsrc + (idx & kRtRowMask));
-  return ldcg(Wsrc + idx);
-}
-
-// Wl[r] = w_blk(r) W[r] (untagged R^T only)
+// Wl[r] = w_blk(r) W[r] (untagged R^T only: more than 2^23 rows or 256 blocks)
 __device__ __forceinline__ void fac_wl(const DevProblem& P, const Work& w, const double* Wpar, const double* wq) {
   const uint64_t ef = evict_first_policy();
   const uint64_t el = sym::evict_last_policy();
@@ -153,16 +154,25 @@ __device__ __forceinline__ void fac_wl(const DevProblem& P, const Work& w, const
 
 // grad_x Phi column j = (acc + s) + t, every path the same bits:
 //   acc  sum_i w_i c_ij over the blocks in order, skipping zero weights
-//        (one thread per column: a plain HBM stream over C);
-//   s    the R^T gather sum_r v w_blk(r) W[r]: the 8 lanes sub = 0..7 of a
-//        lane group fold entries k0 + sub, + 8, ... with fma (two in flight)
-//        over the row phases in order, then an xor tree over the 8 lanes;
-//   t    A^T mu the same way.
-__device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, uint64_t ef) {
+//        (one thread per column: a plain HBM stream over C), in phase p the
+//        blocks [fnb p / nph, fnb (p + 1) / nph) continuing the chain;
+//   s    the R^T gather sum_r v (w_blk(r) W[r]), the column's entries folded
+//        one by one in row order across the row phases (sell_dot_tagged);
+//   t    A^T mu the same way (sell_dot).
+// The gather of phase p reads only rows [rt_b[p], rt_b[p+1]) of the W-cache:
+// phases run one after the other over the whole grid (separate launches), so
+// the gathered slice stays L2-resident.
+constexpr int kGxU = 4;       // gathers in flight per lane in the transposed passes
+// resident CTAs per SM of the standalone kernels: the gather rate needs only a
+// few dozen warp-gathers in flight per SM (one costs 32 L1 wavefronts), so
+// registers for the unrolled loads matter more than occupancy
+constexpr int kRowCtas = 3, kGradCtas = 4;
+
+__device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, int i0, int i1,
+                                            double acc, uint64_t ef) {
   const long long n = P.n;
-  double acc = 0.0;
-  int i = 0;
-  for (; i + 8 <= P.fnb; i += 8) {        // 8 independent loads in flight
+  int i = i0;
+  for (; i + 8 <= i1; i += 8) {           // 8 independent loads in flight
     double c[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
@@ -172,7 +182,7 @@ __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* w
       acc = (l != 0.0) ? acc + l * c[k] : acc;
     }
   }
-  for (; i < P.fnb; ++i) {
+  for (; i < i1; ++i) {
     const double l = wq[i];
     const double c = ld_stream(P.q + (long long)i * n + j, ef);
     acc = (l != 0.0) ? acc + l * c : acc;
@@ -180,117 +190,60 @@ __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* w
   return acc;
 }
 
+// gather item `it` of phase ph for the warp: the slices of R^T's phase, then
+// (phase 0 only) the slices of A^T.  s continues in out[], t goes to aux2[].
 template <bool TAG>
-__device__ __forceinline__ void fac_gather_col(const DevProblem& P, const double* Wsrc, const double* wq,
-                                               const double* lam, long long j, int sub, uint64_t ef,
-                                               double& s, double& t) {
-  const long long n = P.n;
-  s = 0.0;
-  t = 0.0;
-  if (j < n) {
-    for (int ph = 0; ph < P.rt_nph; ++ph) {
-      const long long* ptr = P.rt_ptr + (long long)ph * (n + 1);
-      const long long k1 = __ldg(ptr + j + 1);
-      long long k = __ldg(ptr + j) + sub;
-      for (; k + kGxLanes < k1; k += 2 * kGxLanes) {
-        const int r0 = ld_stream(P.rt_row + k, ef), r1 = ld_stream(P.rt_row + k + kGxLanes, ef);
-        const double v0 = ld_stream(P.rt_val + k, ef), v1 = ld_stream(P.rt_val + k + kGxLanes, ef);
-        const double w0 = rt_weighted<TAG>(Wsrc, wq, r0), w1 = rt_weighted<TAG>(Wsrc, wq, r1);
-        s = fma(v0, w0, s);
-        s = fma(v1, w1, s);
-      }
-      if (k < k1) s = fma(ld_stream(P.rt_val + k, ef), rt_weighted<TAG>(Wsrc, wq, ld_stream(P.rt_row + k, ef)), s);
-    }
-    const long long a0 = __ldg(P.at_ptr + j), a1 = __ldg(P.at_ptr + j + 1);
-    for (long long k = a0 + sub; k < a1; k += kGxLanes)
-      t = fma(ld_stream(P.at_val + k, ef), ldcg(lam + P.mq + P.l0 + ld_stream(P.at_row + k, ef)), t);
-  }
-#pragma unroll
-  for (int o = kGxLanes / 2; o >= 1; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    t += __shfl_xor_sync(0xffffffffu, t, o);
-  }
-}
-
-// In-kernel version (RAPDB_FAC_HOST=0): the same lane groups over the
-// persistent grid, lane sub == 0 adds its column's c_i part.
-template <bool TAG>
-__device__ __forceinline__ void fac_gx_cols(const DevProblem& P, const double* Wsrc, const double* wq,
-                                            const double* lam, double* out) {
+__device__ __forceinline__ void fac_gather_item(const DevProblem& P, const Work& w, const double* Wsrc,
+                                                const double* wq, const double* lam, double* out, int ph,
+                                                long long it, uint64_t ef) {
   const int lane = threadIdx.x & 31;
-  const int sub = lane & (kGxLanes - 1), grp = lane / kGxLanes;
-  const uint64_t ef = evict_first_policy();
-  for (long long jb = gwarp() * (32 / kGxLanes); jb < P.n; jb += nwarps() * (32 / kGxLanes)) {
-    const long long j = jb + grp;
-    double s, t;
-    fac_gather_col<TAG>(P, Wsrc, wq, lam, j, sub, ef, s, t);
-    if (j < P.n && sub == 0) out[j] = (fac_c_acc(P, wq, j, ef) + s) + t;
+  const Sell& M = P.sell[kSellRt + ph];
+  const long long nrt = M.nslots >> 5;
+  if (it < nrt) {
+    const int j = __ldg(M.map + it * 32 + lane);
+    double s = (ph > 0 && j >= 0) ? ldcg(out + j) : 0.0;
+    s = TAG ? sell_dot_tagged<kGxU>(M, it, Wsrc, wq, s, ef) : sell_dot<kGxU>(M, it, Wsrc, s, ef);
+    if (j >= 0) out[j] = s;
+  } else {
+    const long long sl = it - nrt;
+    const Sell& T = P.sell[kSellAt];
+    const int j = __ldg(T.map + sl * 32 + lane);
+    const double t = sell_dot<kGxU>(T, sl, lam + P.mq + P.l0, 0.0, ef);
+    if (j >= 0) w.aux2[j] = t;
   }
 }
-
-__device__ __noinline__ bool recombine_factored(const KArgs& K, Sm& S, const double* Wpar, const double* lam,
-                                                double* out) {
-  double* wq = S.stage;
-  __syncthreads();
-  fac_wq(K.P, lam, wq, kThreads);
-  __syncthreads();
-  if (K.P.rt_tag) {
-    fac_gx_cols<true>(K.P, Wpar, wq, lam, out);
-    return true;
-  }
-  fac_wl(K.P, K.w, Wpar, wq);
-  if (!gsync(K, S)) return false;
-  fac_gx_cols<false>(K.P, K.w.wl, wq, lam, out);
-  return true;
+__device__ __forceinline__ long long fac_gather_items(const DevProblem& P, int ph) {
+  return (P.sell[kSellRt + ph].nslots >> 5) + (ph == 0 ? (P.sell[kSellAt].nslots >> 5) : 0);
 }
 
-// ---------------------------------------------------------------- in-kernel sweep
-// "Sweep" at x into parity par, part A: W = R x (thread per row), A x - b
-// into the linear part of gval[par], the c_i . x chunk partials (warp per
-// item).  Part B (after a grid barrier): the |W_i|^2 chunk partials.  Used
-// when the persistent kernel runs the factored path itself (RAPDB_FAC_HOST=0).
-__device__ __forceinline__ void fac_sweep_a(const DevProblem& P, const Work& w, const double* x, int par) {
-  double* W = w.W + (long long)par * P.nr;
-  const uint64_t ef = evict_first_policy();
-  const uint64_t el = sym::evict_last_policy();
-  for (long long r = gtid(); r < P.nr; r += gstride())
-    st_keep(W + r, csr_row_dot(P.r_ptr, P.r_col, P.r_val, x, r, ef), el);
-  double* gv = w.gval + (long long)par * (P.m + 1);
-  for (long long j = gtid(); j < P.Lloc; j += gstride())
-    gv[1 + P.mq + P.l0 + j] = csr_row_dot(P.a_ptr, P.a_col, P.a_val, x, j, ef) - __ldg(P.b + j);
-  const long long items = (long long)P.fnb * P.nchx;
-  for (long long it = gwarp(); it < items; it += nwarps()) {
-    const double s = cx_item(P, x, it);
-    if ((threadIdx.x & 31) == 0) w.pcx[it] = s;
-  }
-}
-
+// ---------------------------------------------------------------- row pass
 // |W_i|^2 over chunk c: lane r0 + lane, + 32, ... with fma, then the butterfly
-__device__ __forceinline__ double w2_chunk(const double* W, long long r0, long long r1) {
-  double s = 0.0;
-  for (long long r = r0 + (threadIdx.x & 31); r < r1; r += 32) {
-    const double v = ldcg(W + r);
-    s = fma(v, v, s);
+// (formed on the fly by the row pass: 4 slices of 32 rows per chunk)
+__device__ __forceinline__ void fac_chunk(const DevProblem& P, const Work& w, const double* x, double* W,
+                                          long long c, uint64_t ef, uint64_t el) {
+  const int lane = threadIdx.x & 31;
+  long long r0, r1;
+  wchunk_rows(P, c, r0, r1);
+  double s2 = 0.0;
+  for (int g = 0; g < kWChunk / 32; ++g) {
+    const long long row = r0 + 32 * g + lane;
+    if (r0 + 32 * g >= r1) break;
+    const double v = sell_dot<kRowU>(P.sell[kSellR], c * (kWChunk / 32) + g, x, 0.0, ef);
+    if (row < r1) {
+      st_keep(W + row, v, el);
+      s2 = fma(v, v, s2);
+    }
   }
-  return warp_sum(s);
+  s2 = warp_sum(s2);
+  if (lane == 0) w.pw2[c] = s2;
 }
 
-__device__ __forceinline__ void fac_sweep_b(const DevProblem& P, const Work& w, int par) {
-  const double* W = w.W + (long long)par * P.nr;
-  const long long nch = __ldg(P.wch + P.fnb);
-  for (long long c = gwarp(); c < nch; c += nwarps()) {
-    long long r0, r1;
-    wchunk_rows(P, c, r0, r1);
-    const double s = w2_chunk(W, r0, r1);
-    if ((threadIdx.x & 31) == 0) w.pw2[c] = s;
-  }
-}
-
-__device__ __noinline__ bool sweep_factored(const KArgs& K, Sm& S, const double* x, int par) {
-  fac_sweep_a(K.P, K.w, x, par);
-  if (!gsync(K, S)) return false;
-  fac_sweep_b(K.P, K.w, par);
-  return gsync(K, S);
+// 32 rows of A x - b into the linear part of gval
+__device__ __forceinline__ void fac_arows(const DevProblem& P, const double* x, double* gv_lin, long long sl,
+                                          uint64_t ef) {
+  const long long j = sl * 32 + (threadIdx.x & 31);
+  const double v = sell_dot<kRowU>(P.sell[kSellA], sl, x, 0.0, ef);
+  if (j < P.Lloc) gv_lin[j] = v - __ldg(P.b + j);
 }
 
 // g_i (i = 0..mq, 0 = f) at parity par from the chunk partials: one CTA per
@@ -335,16 +288,14 @@ __device__ void g_factored(const KArgs& K, int par) {
 // ---- standalone kernels the host launches at a factored stop (fq requests)
 
 // Row pass at x into parity par.  Warps with gwarp % 4 == 3 form the c_i . x
-// items (1024-column chunks of each c_i row: a pure HBM stream); the others
-// take the W chunks (128 rows of R as 4 staged 32-row groups, W stored with
-// an evict-last hint for the next gradient's gather, lane-ordered |W|^2 fma
-// chain and a butterfly -- w2_chunk's bits) and then the 32-row groups of A.
-__global__ void __launch_bounds__(kThreads, 4) fac_row_kernel(DevProblem P, Work w, const double* x, int par) {
-  __shared__ double sv[kWarps][kStageCap];
-  __shared__ int sc[kWarps][kStageCap];
+// items (1024-column chunks of each c_i row: a pure HBM stream beside the
+// gather-bound rows); the others take the W chunks (4 slices of R each, W
+// stored with an evict-last hint for the next gradient's gather, lane-ordered
+// |W|^2 fma chain and a butterfly) and then the slices of A.
+__global__ void __launch_bounds__(kThreads, kRowCtas) fac_row_kernel(DevProblem P, Work w, const double* x, int par) {
   const uint64_t ef = evict_first_policy();
   const uint64_t el = sym::evict_last_policy();
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const long long gw = gwarp(), nw = nwarps();
   if ((gw & 3) == 3) {                       // c_i . x role
     const long long items = (long long)P.fnb * P.nchx;
@@ -359,36 +310,21 @@ __global__ void __launch_bounds__(kThreads, 4) fac_row_kernel(DevProblem P, Work
   double* W = w.W + (long long)par * P.nr;
   double* gv = w.gval + (long long)par * (P.m + 1) + 1 + P.mq + P.l0;
   const long long nch = __ldg(P.wch + P.fnb);
-  const long long items = nch + (P.Lloc + 31) / 32;
+  const long long items = nch + (P.sell[kSellA].nslots >> 5);
   for (long long it = me; it < items; it += nrole) {
-    if (it < nch) {
-      long long r0, r1;
-      wchunk_rows(P, it, r0, r1);
-      double s2 = 0.0;
-      for (long long g0 = r0; g0 < r1; g0 += 32) {
-        const double v = csr_group32(P.r_ptr, P.r_col, P.r_val, x, g0, r1, sv[wp], sc[wp], ef);
-        if (g0 + lane < r1) {
-          st_keep(W + g0 + lane, v, el);
-          s2 = fma(v, v, s2);
-        }
-      }
-      s2 = warp_sum(s2);
-      if (lane == 0) w.pw2[it] = s2;
-    } else {
-      const long long a0 = (it - nch) * 32, a1 = min(a0 + 32, (long long)P.Lloc);
-      const double v = csr_group32(P.a_ptr, P.a_col, P.a_val, x, a0, a1, sv[wp], sc[wp], ef);
-      if (a0 + lane < a1) gv[a0 + lane] = v - __ldg(P.b + a0 + lane);
-    }
+    if (it < nch) fac_chunk(P, w, x, W, it, ef, el);
+    else fac_arows(P, x, gv, it - nch, ef);
   }
 }
 
-// Gradient part 1 (lam = the trial multipliers) at the W-cache Wsrc, two warp
-// roles in one launch so the HBM stream over C runs beside the gather-bound
-// R^T walk: warps with gwarp % 4 == 3 form acc (thread per column) into aux;
-// the others form s into out and t into aux2.  Dynamic shared memory: wq [fnb].
+// Gradient part 1, row phase ph (lam = the trial multipliers) at the W-cache
+// Wsrc, two warp roles in one launch so the HBM stream over C runs beside the
+// gather-bound R^T walk: warps with gwarp % 4 == 3 continue acc over this
+// phase's share of the blocks (thread per column) in aux; the others continue
+// s in out and (phase 0) form t in aux2.  Dynamic shared memory: wq [fnb].
 template <bool TAG>
-__global__ void __launch_bounds__(kThreads, 8) fac_grad_kernel(DevProblem P, Work w, const double* Wsrc,
-                                                               const double* lam, double* out) {
+__global__ void __launch_bounds__(kThreads, kGradCtas) fac_grad_kernel(DevProblem P, Work w, const double* Wsrc,
+                                                               const double* lam, double* out, int ph) {
   extern __shared__ double wq[];
   fac_wq(P, lam, wq, kThreads);
   __syncthreads();
@@ -397,20 +333,14 @@ __global__ void __launch_bounds__(kThreads, 8) fac_grad_kernel(DevProblem P, Wor
   const long long n = P.n;
   const long long gw = gwarp(), nw = nwarps();
   if ((gw & 3) == 3) {
-    for (long long j = (gw >> 2) * 32 + lane; j < n; j += (nw >> 2) * 32) w.aux[j] = fac_c_acc(P, wq, j, ef);
+    const int i0 = (int)((long long)P.fnb * ph / P.rt_nph), i1 = (int)((long long)P.fnb * (ph + 1) / P.rt_nph);
+    for (long long j = (gw >> 2) * 32 + lane; j < n; j += (nw >> 2) * 32)
+      w.aux[j] = fac_c_acc(P, wq, j, i0, i1, ph > 0 ? ldcg(w.aux + j) : 0.0, ef);
     return;
   }
-  const int sub = lane & (kGxLanes - 1), grp = lane / kGxLanes;
   const long long me = (gw >> 2) * 3 + (gw & 3), nrole = (nw >> 2) * 3;
-  for (long long jb = me * (32 / kGxLanes); jb < n; jb += nrole * (32 / kGxLanes)) {
-    const long long j = jb + grp;
-    double s, t;
-    fac_gather_col<TAG>(P, Wsrc, wq, lam, j, sub, ef, s, t);
-    if (j < n && sub == 0) {
-      out[j] = s;
-      w.aux2[j] = t;
-    }
-  }
+  const long long items = fac_gather_items(P, ph);
+  for (long long it = me; it < items; it += nrole) fac_gather_item<TAG>(P, w, Wsrc, wq, lam, out, ph, it, ef);
 }
 
 // Gradient part 2, thread per column: gx = (acc + s) + t into out.  With

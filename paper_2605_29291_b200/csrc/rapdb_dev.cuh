@@ -92,6 +92,21 @@ enum Step {
 // exchange kinds: what the host must all-reduce (sum) across ranks before resuming
 enum Xkind { X_NONE = 0, X_GX = 1, X_G = 2, X_GX2 = 3, X_H = 4 };
 
+// Sliced ELLPACK with slices of 32 slots (one warp, lane = slot): entry t of
+// slot s lives at sp[s >> 5] + 32 t + (s & 31), so a warp's t-th loads of val
+// and idx are one coalesced 256 / 128 byte access and every slot folds its own
+// entries in stored order.  A slice is as wide as its longest slot.
+struct Sell {
+  long long nslots;      // multiple of 32
+  const long long* sp;   // [nslots / 32 + 1] entry offset of each slice
+  const int* idx;        // gathered index of each entry
+  const double* val;
+  const int* len;        // [nslots] entries of each slot
+  const int* map;        // [nslots] output index of each slot (-1: padding); null = the slot itself
+};
+constexpr int kMaxRtPhases = 8;
+constexpr int kSellR = 0, kSellA = 1, kSellAt = 2, kSellRt = 3;   // DevProblem::sell slots
+
 struct DevProblem {
   int n, m, p, k0, k1, nloc, nact, nzero;
   long long ld;
@@ -111,17 +126,22 @@ struct DevProblem {
   int L;                 // linear rows A x <= b (orthant constraints with Q = 0)
   int nchx;              // chunks of kCxCols columns for c_i . x (factored.cuh)
   int nfpart;            // warps of a fused-trial gradient launch (its D_p / <gx, dx> partials)
-  const long long* r_ptr; const int* r_col; const double* r_val;    // CSR R   [nr x n]
-  const long long* rt_ptr; const int* rt_row; const double* rt_val; // CSR R^T [n x nr], rt_nph row phases:
-  // rt_ptr [rt_nph][n+1] -- column j's entries with rows in phase p are
-  // [rt_ptr[p (n+1) + j], rt_ptr[p (n+1) + j + 1]), phases in row order, so
-  // walking the phases walks each column in sorted row order; rt_tag: rt_row
-  // holds r | (local block of r) << 23 (the gather weights W on the fly)
+  // The sparse operands are held as sliced ELLPACK (Sell, slice height 32):
+  //   sr   R   [nr x n]: slot = 128 * (W chunk) + row inside the chunk, so every
+  //        chunk of a block (wch / rblk) is 4 slices and no slice spans two blocks
+  //   sa   A   [Lloc x n]: slot = local row
+  //   srt  R^T [n x nr] in rt_nph ROW PHASES (rows [rt_b[p], rt_b[p+1]) of the
+  //        stacked R): one Sell per phase over the columns sorted by their
+  //        entry count in that phase (map = column of the slot); entries of a
+  //        column in row order, so walking the phases walks each column in
+  //        sorted row order; rt_tag: idx holds r | (local block of r) << 23
+  //        (the gather weights W on the fly)
+  //   sat  A^T [n x Lloc], columns sorted by entry count (map = column)
+  // (a device table, so a phase can be indexed at run time without a local copy)
+  const Sell* sell;      // [kSellRt + rt_nph]: R, A, A^T, then the phases of R^T
   int rt_nph, rt_tag;
   const int* rmat;                                                  // [nr] block of each R row
   const long long* rblk;                                            // [mq+2] first row of block i
-  const long long* a_ptr; const int* a_col; const double* a_val;    // CSR A   [L x n]
-  const long long* at_ptr; const int* at_row; const double* at_val; // CSR A^T [n x L]
   const long long* wch;  // [fnb+1] prefix count of 1024-row chunks of W per local block
   // constraint sharding of a factored instance: this rank holds blocks
   // [fb0, fb0+fnb) of the mq+1 (R, C, d local, rmat local ids) and linear rows

@@ -373,6 +373,9 @@ struct rapdb_ctx {
   Work w{};
   int* d_ints = nullptr;
   long long* d_ll = nullptr;   // factored: rblk and W-chunk prefix tables
+  Sell* d_sell = nullptr;      // factored: the Sell descriptors (DevProblem::sell)
+  Sell h_sell[kSellRt + kMaxRtPhases];
+  long long grad_bytes = 0;    // factored: bytes one gradient streams (R^T, A^T, C, column partials)
   sym::Unit* d_units = nullptr;  // packed layout: unit table
   SolverState* h_state = nullptr;  // page-locked copy of the device state (+ abort flag)
   long long ws_bytes = 0;
@@ -618,12 +621,15 @@ int fac_gradient(rapdb_ctx* c, const Work& w, const double* Wpar, const double* 
     Wsrc = w.wl;
     ++g_launches;
   }
-  if (P.rt_tag) fac_grad_kernel<true><<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out);
-  else fac_grad_kernel<false><<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out);
+  for (int ph = 0; ph < P.rt_nph; ++ph) {   // one launch per row phase: its slice of the W-cache stays in L2
+    if (P.rt_tag) fac_grad_kernel<true><<<c->nsm * kGradCtas, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out, ph);
+    else fac_grad_kernel<false><<<c->nsm * kGradCtas, kThreads, wq, c->stream>>>(P, w, Wsrc, lam, out, ph);
+    ++g_launches;
+  }
   const int fgrid = P.nfpart / kWarps;
   if (trial) fac_grad_fin_kernel<true><<<fgrid, kThreads, 0, c->stream>>>(P, w, out, tau, cur);
   else fac_grad_fin_kernel<false><<<fgrid, kThreads, 0, c->stream>>>(P, w, out, tau, cur);
-  g_launches += 2;
+  ++g_launches;
   return RAPDB_OK;
 }
 
@@ -631,7 +637,7 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   const DevProblem& P = c->P;
   const Work& w = c->w;
   const long long n = P.n, np = (long long)P.p + P.m;
-  const int rgrid = c->nsm * 4;   // row pass: 4 CTAs per SM (a multiple of 4 warps)
+  const int rgrid = c->nsm * kRowCtas;   // row pass: all CTAs resident (8 warps each: a multiple of 4 warps)
   if (st.fq[0] == 1) {
     const int par = st.fq[1];
     const double* x = st.fq[2] ? rc.in_x : w.x + (long long)par * n;
@@ -684,6 +690,8 @@ int comm_exchange(rapdb_ctx* c, int kind) {
 // (NCCL over NVLink in the Python binding) and the op resumes in a new launch.
 int launch(rapdb_ctx* c, RunCfg rc) {
   if (!c->bound || !c->have_params || !c->have_ws) return fail(c, RAPDB_ECONFIG, "context not fully bound");
+  if (c->P.kind == 1 && c->P.rt_nph < 1)
+    return fail(c, RAPDB_ECONFIG, "factored context has no R^T / A^T (rapdb_set_factored_transpose)");
   rc.split = c->split;
   rc.fac_host = c->fac_host;
   rc.p2p = c->p2p;
@@ -993,6 +1001,7 @@ void rapdb_destroy(rapdb_ctx* c) {
   if (!c) return;
   table_free(c->d_ints, c->stream);
   table_free(c->d_ll, c->stream);
+  table_free(c->d_sell, c->stream);
   table_free(c->d_units, c->stream);
   table_free(c->d_px, c->stream);
   pinned_put(c->h_state);
@@ -1250,23 +1259,34 @@ int bind_dense_impl(rapdb_ctx* c, int layout, int n, int m, int p, int k0, int k
 }
 }  // namespace
 
-int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const long long* r_ptr, const int* r_col,
-                        const double* r_val, const long long* rt_ptr, const int* rt_row, const double* rt_val,
-                        const int* rmat, const long long* rblk, const double* C, const double* d,
-                        const long long* a_ptr, const int* a_col, const double* a_val, const long long* at_ptr,
-                        const int* at_row, const double* at_val, const double* b, const double* lower,
-                        const double* upper, double mu) {
-  return rapdb_bind_factored_range(c, n, mq, L, 0, mq + 1, 0, L, nr, r_ptr, r_col, r_val, rt_ptr, rt_row, rt_val,
-                                   rmat, rblk, C, d, a_ptr, a_col, a_val, at_ptr, at_row, at_val, b, lower,
-                                   upper, mu);
+int rapdb_bind_factored(rapdb_ctx* c, int n, int mq, int L, long long nr, const rapdb_sell* R, const int* rmat,
+                        const long long* rblk, const double* C, const double* d, const rapdb_sell* A,
+                        const double* b, const double* lower, const double* upper, double mu) {
+  return rapdb_bind_factored_range(c, n, mq, L, 0, mq + 1, 0, L, nr, R, rmat, rblk, C, d, A, b, lower, upper, mu);
+}
+
+// a caller's Sell descriptor checked against the expected slot count; the
+// entry total (sp[last]) is read back for the byte accounting
+static int take_sell(rapdb_ctx* c, const rapdb_sell* in, long long want_slots, bool need_map, const char* name,
+                     Sell* out, long long* entries) {
+  *out = Sell{};
+  *entries = 0;
+  if (!in) return fail(c, RAPDB_EINPUT, std::string("null Sell descriptor: ") + name);
+  if (in->nslots != want_slots || (in->nslots & 31))
+    return fail(c, RAPDB_EINPUT, std::string("Sell slot count mismatch: ") + name);
+  if (!in->sp || (in->nslots > 0 && (!in->len || (need_map && !in->map))))
+    return fail(c, RAPDB_EINPUT, std::string("null Sell array: ") + name);
+  CK(cudaMemcpy(entries, in->sp + (in->nslots >> 5), 8, cudaMemcpyDeviceToHost));
+  if (*entries < 0 || (*entries & 31) || (*entries > 0 && (!in->idx || !in->val)))
+    return fail(c, RAPDB_EINPUT, std::string("bad Sell entry arrays: ") + name);
+  out->nslots = in->nslots; out->sp = in->sp; out->idx = in->idx; out->val = in->val;
+  out->len = in->len; out->map = in->map;
+  return RAPDB_OK;
 }
 
 int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int fb1, int l0, int l1, long long nr,
-                              const long long* r_ptr, const int* r_col, const double* r_val,
-                              const long long* rt_ptr, const int* rt_row, const double* rt_val,
-                              const int* rmat, const long long* rblk, const double* C, const double* d,
-                              const long long* a_ptr, const int* a_col, const double* a_val,
-                              const long long* at_ptr, const int* at_row, const double* at_val, const double* b,
+                              const rapdb_sell* R, const int* rmat, const long long* rblk, const double* C,
+                              const double* d, const rapdb_sell* A, const double* b,
                               const double* lower, const double* upper, double mu) {
   if (!c) return RAPDB_EINPUT;
   if (n <= 0 || mq < 0 || L < 0 || nr < 0) return fail(c, RAPDB_EINPUT, "need n > 0, mq >= 0, L >= 0, nr >= 0");
@@ -1277,9 +1297,7 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   if (c->nranks == 1 && !whole && !c->split)
     return fail(c, RAPDB_EINPUT, "a single-rank context must hold the whole instance (or be split)");
   if (c->nranks > 1) c->split = 1;
-  if (!rblk || (fnb > 0 && (!C || !d)) || !lower || !upper || !rt_ptr || !at_ptr ||
-      (nr > 0 && (!r_ptr || !r_col || !r_val || !rt_row || !rt_val || !rmat)) ||
-      (Lloc > 0 && (!a_ptr || !a_col || !a_val || !at_row || !at_val || !b)))
+  if (!rblk || (fnb > 0 && (!C || !d)) || !lower || !upper || (nr > 0 && !rmat) || (Lloc > 0 && !b))
     return fail(c, RAPDB_EINPUT, "null data pointer");
   if (rblk[0] != 0 || rblk[fnb] != nr) return fail(c, RAPDB_EINPUT, "rblk must run from 0 to nr");
   // d_ll: [fnb+1] local block row offsets, then [fnb+1] prefix counts of W chunks
@@ -1300,9 +1318,14 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   c->d_ints = nullptr;
   CK(table_alloc(reinterpret_cast<void**>(&c->d_ints), 16, c->stream));
   CK(cudaMemsetAsync(c->d_ints, 0, 16, c->stream));
-  long long nnz_r = 0, nnz_a = 0;
-  if (nr > 0) CK(cudaMemcpy(&nnz_r, r_ptr + nr, 8, cudaMemcpyDeviceToHost));
-  if (Lloc > 0) CK(cudaMemcpy(&nnz_a, a_ptr + Lloc, 8, cudaMemcpyDeviceToHost));
+  long long nnz_r = 0, nnz_a = 0;   // stored entries incl. slice padding: the bytes actually streamed
+  Sell sr{}, sa{};
+  {
+    int e = take_sell(c, R, nchw * kWChunk, false, "R", &sr, &nnz_r);
+    if (e) return e;
+    e = take_sell(c, A, ((long long)Lloc + 31) / 32 * 32, false, "A", &sa, &nnz_a);
+    if (e) return e;
+  }
   // no streamed sweep: the ring degenerates to the multiplier staging area
   SweepPlan sp{};
   sp.TR = 1; sp.cpr = 1; sp.chunk = 2; sp.nstages = 1; sp.ncw = 1; sp.segmax = 1;
@@ -1330,20 +1353,26 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   P.kind = 1; P.mq = mq; P.nr = nr; P.L = L; P.nchx = (n + kCxCols - 1) / kCxCols;
   P.nfpart = c->nsm * 4 * kWarps;   // fused-trial gradient grid: 4 CTAs per SM
   P.fb0 = fb0; P.fnb = fnb; P.l0 = l0; P.Lloc = Lloc;
-  P.r_ptr = r_ptr; P.r_col = r_col; P.r_val = r_val;
-  P.rt_ptr = rt_ptr; P.rt_row = rt_row; P.rt_val = rt_val;
-  P.rt_nph = 1; P.rt_tag = 0;   // plain CSR of R^T until rapdb_set_factored_transpose
+  // the Sell descriptors live in a device table (DevProblem::sell); R^T / A^T
+  // arrive with rapdb_set_factored_transpose (required before any op)
+  std::memset(c->h_sell, 0, sizeof c->h_sell);
+  c->h_sell[kSellR] = sr; c->h_sell[kSellA] = sa;
+  table_free(c->d_sell, c->stream);
+  c->d_sell = nullptr;
+  CK(table_alloc(reinterpret_cast<void**>(&c->d_sell), sizeof c->h_sell, c->stream));
+  CK(cudaMemcpyAsync(c->d_sell, c->h_sell, sizeof c->h_sell, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  P.sell = c->d_sell;
+  P.rt_nph = 0; P.rt_tag = 0;
   P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (fnb + 1);
-  P.a_ptr = a_ptr; P.a_col = a_col; P.a_val = a_val;
-  P.at_ptr = at_ptr; P.at_row = at_row; P.at_val = at_val;
   c->P = P;
   c->sp = sp;
   c->nchw = nchw;
-  const char* env_fh = std::getenv("RAPDB_FAC_HOST");
-  c->fac_host = (env_fh && env_fh[0] == '0') ? 0 : 1;
+  c->fac_host = 1;   // every factored sweep / gradient is a stop served by standalone kernels
   // one factored sweep: R (12 B/nnz + row pointers) streamed, W written and
   // re-read, C and A (+ b) read, x gathered once
-  c->sweep_bytes = 12 * nnz_r + 8 * (nr + 1) + 16 * nr + 8LL * fnb * n + 12 * nnz_a + 16LL * Lloc + 8 + 8LL * n;
+  c->sweep_bytes = 12 * nnz_r + 4 * sr.nslots + 16 * nr + 8LL * fnb * n + 12 * nnz_a + 4 * sa.nslots + 16LL * Lloc +
+                   8LL * n;
   {
     const int ra = fac_kernel_attrs(c);
     if (ra) return ra;
@@ -1396,19 +1425,31 @@ int rapdb_spectral_norm(const double* M, long long rows, long long cols, long lo
   return rc;
 }
 
-int rapdb_set_factored_transpose(rapdb_ctx* c, int nph, const long long* ph_bounds, const long long* pptr,
-                                 const int* prow, const double* pval, int tagged) {
+int rapdb_set_factored_transpose(rapdb_ctx* c, int nph, const long long* ph_bounds, const rapdb_sell* RT,
+                                 const rapdb_sell* AT, int tagged) {
   if (!c) return RAPDB_EINPUT;
   if (!c->bound || c->P.kind != 1) return fail(c, RAPDB_ECONFIG, "bind a factored instance first");
   DevProblem& P = c->P;
-  if (nph < 1 || !ph_bounds || !pptr || (P.nr > 0 && (!prow || !pval)))
-    return fail(c, RAPDB_EINPUT, "need nph >= 1 phases and their arrays");
+  if (nph < 1 || nph > kMaxRtPhases || !ph_bounds || !RT || !AT)
+    return fail(c, RAPDB_EINPUT, "need 1..8 row phases of R^T and A^T");
   if (ph_bounds[0] != 0 || ph_bounds[nph] != P.nr) return fail(c, RAPDB_EINPUT, "phase bounds must run from 0 to nr");
   for (int i = 0; i < nph; ++i)
     if (ph_bounds[i + 1] < ph_bounds[i]) return fail(c, RAPDB_EINPUT, "phase bounds must be nondecreasing");
   if (tagged && (P.nr > kRtRowMask + 1LL || P.fnb > (1 << (31 - kRtTagShift))))
     return fail(c, RAPDB_EINPUT, "tagged R^T rows need nr <= 2^23 and at most 256 local blocks");
-  P.rt_ptr = pptr; P.rt_row = prow; P.rt_val = pval;
+  const long long cols = ((long long)P.n + 31) / 32 * 32;
+  long long ent = 0;
+  c->grad_bytes = 8LL * P.fnb * P.n + 24LL * P.n;   // C once, the three column partials
+  for (int ph = 0; ph < nph; ++ph) {
+    const int e = take_sell(c, RT + ph, cols, true, "R^T phase", &c->h_sell[kSellRt + ph], &ent);
+    if (e) return e;
+    c->grad_bytes += 12 * ent + 8 * cols;
+  }
+  const int e = take_sell(c, AT, cols, true, "A^T", &c->h_sell[kSellAt], &ent);
+  if (e) return e;
+  c->grad_bytes += 12 * ent + 8 * cols;
+  CK(cudaMemcpyAsync(c->d_sell, c->h_sell, sizeof c->h_sell, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   P.rt_nph = nph; P.rt_tag = tagged ? 1 : 0;
   return RAPDB_OK;
 }

@@ -28,7 +28,7 @@ __device__ __forceinline__ bool sweep_sync(const KArgs& K, Sm& S, const double* 
   unsigned long long t0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer();
   bool ok;
-  if (K.P.kind == 1 && K.rc.fac_host) {   // the host runs the sweep kernels at the next stop
+  if (K.P.kind == 1) {   // the host runs the row-pass kernel at the next stop (factored.cuh)
     if (threadIdx.x == 0) {
       SolverState& st = *S.st;
       st.fq[0] = 1;
@@ -37,8 +37,6 @@ __device__ __forceinline__ bool sweep_sync(const KArgs& K, Sm& S, const double* 
     }
     __syncthreads();
     ok = true;
-  } else if (K.P.kind == 1) {
-    ok = sweep_factored(K, S, xsrc, par);
   } else {
     sweep(K, S, xsrc, par);
     ok = gsync(K, S);
@@ -146,7 +144,7 @@ __device__ __forceinline__ void g_local(const KArgs& K, int par) {
 __device__ __forceinline__ bool gx_part(const KArgs& K, Sm& S, int par, const double* lam_g, const double* lam_s,
                                         double* out) {
   const DevProblem& P = K.P;
-  if (P.kind == 1 && K.rc.fac_host) {   // queue it for the host (factored.cuh, fac_gx_*)
+  if (P.kind == 1) {   // queue it for the host (factored.cuh, fac_grad_*)
     if (threadIdx.x == 0) {
       SolverState& st = *S.st;
       const int np = P.p + P.m;
@@ -162,7 +160,6 @@ __device__ __forceinline__ bool gx_part(const KArgs& K, Sm& S, int par, const do
     __syncthreads();
     return true;
   }
-  if (P.kind == 1) return recombine_factored(K, S, K.w.W + (long long)par * P.nr, lam_g, out);
   const double* U = K.w.U + (long long)par * P.nloc * P.n;
   if (K.sp.rc_cols) recombine_cols(K, S, U, lam_s, out);
   else for (long long j = gtid(); j < P.n; j += gstride()) out[j] = recombine_local(K, U, lam_s, j);
@@ -531,7 +528,7 @@ __device__ int ty_dual(const KArgs& K, Sm& S) {
 // C) and the row pass at x_new (factored.cuh fac_trial_kernel /
 // fac_row_kernel); ty_primal_fac_fused then adds the dual-side partials.
 __device__ __forceinline__ bool fac_fused_trial(const KArgs& K) {
-  return K.P.kind == 1 && K.rc.fac_host && !K.rc.split && K.prm.mode == 0;
+  return K.P.kind == 1 && !K.rc.split && K.prm.mode == 0;
 }
 
 __device__ int ty_gxpart(const KArgs& K, Sm& S, int& xk) {

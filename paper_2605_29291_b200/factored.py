@@ -12,15 +12,17 @@ config 3 is new capability built on the same operator contract
 ``FactoredInstance`` exposes the same surface the solver layers use from
 ``problem.ProblemInstance`` (n, m, p, primal_set, cone, mu, f/g evaluation,
 device upload), so ``ApdbEngine`` / ``run_restarted`` / ``kkt_residual`` take
-either.  HBM layout (``FactoredDeviceData``): the stacked R as CSR (int64 row
-pointers, int32 columns, fp64 values) plus R^T as a gather (no atomics, fixed
-summation order) in ROW PHASES: the stacked rows are cut into ranges of at
-most ``RT_PHASE_ROWS`` (12 MB of the W-cache), with one CSR of R^T per phase
-over phase-major entry arrays, each entry's row tagged with its block id
-(``rapdb_set_factored_transpose``) -- so each gather phase touches an
-L2-sized slice of W, and walking the phases walks every column in sorted row
-order; plus the block id of every stacked row, C [(mq+1) x n], and A / A^T
-as CSR.
+either.  HBM layout (``FactoredDeviceData``): every sparse operand as sliced
+ELLPACK with slices of 32 slots (``SellMatrix`` / ``rapdb_sell``: a warp's
+loads are coalesced with no staging, every row / column is summed in stored
+order) -- the stacked R with its rows laid out per block in 128-row chunks,
+A by row, and the transposes for the gradient gather (no atomics, fixed
+summation order): R^T in ROW PHASES of at most ``RT_PHASE_ROWS`` stacked rows
+(one Sell per phase over the columns sorted by entry count, each entry's row
+tagged with its block id), so that each gather phase touches an L2-sized
+slice of the W-cache and walking the phases walks every column in sorted row
+order, and A^T the same way; plus the block id of every stacked row and
+C [(mq+1) x n].
 """
 
 from __future__ import annotations
@@ -34,29 +36,131 @@ from .geometry import Box, NonnegOrthant
 
 import os as _os
 
-# W-cache rows gathered per R^T phase (RAPDB_RT_PHASE_ROWS overrides; A/B runs)
-RT_PHASE_ROWS = int(_os.environ.get("RAPDB_RT_PHASE_ROWS", str(1 << 23)))
+# W-cache rows gathered per R^T phase (RAPDB_RT_PHASE_ROWS overrides; A/B
+# runs): 2^22 rows = 32 MB of W, which stays resident in one half of the L2
+RT_PHASE_ROWS = 1 << 22
+
+
+def rt_phase_rows() -> int:
+    return int(_os.environ.get("RAPDB_RT_PHASE_ROWS", str(RT_PHASE_ROWS)))
+
+
+RT_MAX_PHASES = 8              # rapdb_set_factored_transpose
 RT_TAG_SHIFT = 23              # tagged R^T rows: r | block << 23
+W_CHUNK = 128                  # rows of W per |W_i|^2 partial (csrc/factored.cuh kWChunk)
+
+
+class SellMatrix:
+    """Sliced ELLPACK (slice height 32) of a CSR operand, host arrays.
+
+    ``slot_rows[s]`` is the CSR row held by slot s (-1: padding); entry t of
+    slot s is stored at ``sp[s // 32] + 32 t + s % 32`` and a slice is as wide
+    as its longest slot.  Entries keep the CSR's stored order."""
+
+    def __init__(self, M, slot_rows, idx_of=None, with_map=False):
+        slot_rows = np.asarray(slot_rows, dtype=np.int64)
+        nslots = slot_rows.size
+        if nslots % 32:
+            raise InputError("Sell needs a multiple of 32 slots")
+        indptr = M.indptr.astype(np.int64)
+        lens_rows = np.diff(indptr)
+        valid = slot_rows >= 0
+        ln = np.zeros(nslots, dtype=np.int32)
+        ln[valid] = lens_rows[slot_rows[valid]]
+        width = ln.reshape(-1, 32).max(axis=1).astype(np.int64) if nslots else np.zeros(0, np.int64)
+        sp = np.zeros(nslots // 32 + 1, dtype=np.int64)
+        np.cumsum(width * 32, out=sp[1:])
+        tot = int(sp[-1])
+        idx = np.zeros(tot, dtype=np.int32)
+        val = np.zeros(tot, dtype=np.float64)
+        if M.nnz:
+            slot_of_row = np.full(M.shape[0], -1, dtype=np.int64)
+            slot_of_row[slot_rows[valid]] = np.nonzero(valid)[0]
+            row_of = np.repeat(np.arange(M.shape[0], dtype=np.int64), lens_rows)
+            s = slot_of_row[row_of]
+            if np.any(s < 0):
+                raise InputError("Sell slots must cover every nonempty row")
+            pos = sp[s >> 5] + (np.arange(M.nnz, dtype=np.int64) - indptr[row_of]) * 32 + (s & 31)
+            ind = M.indices.astype(np.int64)
+            idx[pos] = ind if idx_of is None else idx_of(ind)
+            val[pos] = M.data
+        self.nslots, self.sp, self.idx, self.val, self.len = nslots, sp, idx, val, ln
+        self.map = slot_rows.astype(np.int32) if with_map else None
+        self.entries = tot
+
+    @classmethod
+    def by_row(cls, M):
+        """slot = row, padded to a multiple of 32."""
+        nr = M.shape[0]
+        slots = np.full(-(-nr // 32) * 32, -1, dtype=np.int64)
+        slots[:nr] = np.arange(nr)
+        return cls(M, slots)
+
+    @classmethod
+    def by_block_chunks(cls, M, rblk):
+        """The stacked R: block i's rows start at slot 128 * (chunks of the
+        earlier blocks), each block padded to whole 128-row chunks."""
+        parts = []
+        for i in range(len(rblk) - 1):
+            r0, r1 = int(rblk[i]), int(rblk[i + 1])
+            pad = -(-(r1 - r0) // W_CHUNK) * W_CHUNK
+            part = np.full(pad, -1, dtype=np.int64)
+            part[:r1 - r0] = np.arange(r0, r1)
+            parts.append(part)
+        return cls(M, np.concatenate(parts) if parts else np.zeros(0, np.int64))
+
+    @classmethod
+    def by_sorted_length(cls, M, idx_of=None):
+        """Rows sorted by entry count (longest first, stable), so the slots
+        of a slice have near-equal length; map = row of the slot."""
+        nr = M.shape[0]
+        order = np.argsort(-np.diff(M.indptr), kind="stable")
+        slots = np.full(-(-nr // 32) * 32, -1, dtype=np.int64)
+        slots[:nr] = order
+        return cls(M, slots, idx_of=idx_of, with_map=True)
+
+
+class DeviceSell:
+    """A SellMatrix in HBM."""
+
+    def __init__(self, m: SellMatrix, device):
+        import torch
+
+        def up(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            return torch.from_numpy(a if a.size else np.zeros(1, dtype=dt)).to(device)
+
+        self.nslots, self.entries = m.nslots, m.entries
+        self.sp, self.idx, self.val = up(m.sp, np.int64), up(m.idx, np.int32), up(m.val, np.float64)
+        self.len = up(m.len, np.int32)
+        self.map = None if m.map is None else up(m.map, np.int32)
+        self._desc = None
+
+    def descriptor(self):
+        from ._capi import SellDescriptor
+        if self._desc is None:
+            self._desc = SellDescriptor(self.nslots, self.sp.data_ptr(), self.idx.data_ptr(), self.val.data_ptr(),
+                                        self.len.data_ptr(), None if self.map is None else self.map.data_ptr())
+        return self._desc
 
 
 def phased_transpose(R, rmat, nph: int, tag: bool):
-    """(bounds, ptr [nph][n+1], rows, vals) of R^T split into nph row phases,
-    entries phase-major; rows tagged with their block id when ``tag``."""
+    """(bounds, [SellMatrix per phase]) of R^T split into nph row phases; rows
+    tagged with their block id when ``tag``."""
     nr, n = R.shape
     bounds = np.array([nr * p // nph for p in range(nph + 1)], dtype=np.int64)
-    ptrs, rows, vals = [], [], []
-    off = 0
+    mats = []
     for p in range(nph):
         Rt = R[bounds[p]:bounds[p + 1]].T.tocsr()      # sorted rows per column
         Rt.sort_indices()
-        idx = Rt.indices.astype(np.int64) + bounds[p]
-        if tag:
-            idx = idx | (rmat[idx].astype(np.int64) << RT_TAG_SHIFT)
-        ptrs.append(Rt.indptr.astype(np.int64) + off)
-        rows.append(idx.astype(np.int32))
-        vals.append(Rt.data)
-        off += Rt.nnz
-    return bounds, np.concatenate(ptrs), np.concatenate(rows), np.concatenate(vals)
+        off = int(bounds[p])
+
+        def idx_of(ind, off=off):
+            ind = ind + off
+            return ind | (rmat[ind].astype(np.int64) << RT_TAG_SHIFT) if tag else ind
+
+        mats.append(SellMatrix.by_sorted_length(Rt, idx_of=idx_of))
+    return bounds, mats
 
 
 class FactoredInstance:
@@ -139,6 +243,7 @@ class FactoredInstance:
             raise ConfigurationError("a factored shard needs both its block range and its linear-row range")
         dev = torch.device("cuda", 0) if device is None else torch.device(device)
         key = str(dev) if (k0, k1, l0, l1) == (0, self.mq + 1, 0, self.L) else f"{dev}[{k0}:{k1}|{l0}:{l1}]"
+        key += f"/ph{rt_phase_rows()}"
         if key not in self._dev:
             self._dev[key] = FactoredDeviceData.upload(self, dev, k0, k1, l0, l1)
         return self._dev[key]
@@ -194,29 +299,26 @@ class FactoredDeviceData:
         def i32(a):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
 
-        def csr(M):
-            return i64(M.indptr), i32(M.indices), f64(M.data)
-
         r0, r1 = int(inst.rblk[k0]), int(inst.rblk[k1])
-        R = inst.R[r0:r1]
+        R = inst.R[r0:r1]              # stored entry order kept: it is the summation order of W = R x
         rblk = inst.rblk[k0:k1 + 1] - r0
         A = inst.A[l0:l1]
         At = A.T.tocsr()
+        At.sort_indices()              # a column's entries in row order
         nr = R.shape[0]
         rmat = np.repeat(np.arange(k1 - k0, dtype=np.int32), np.diff(rblk))
-        r_ptr, r_col, r_val = csr(R)
-        nph = max(1, -(-nr // RT_PHASE_ROWS))
+        nph = min(RT_MAX_PHASES, max(1, -(-nr // rt_phase_rows())))
         tag = nr <= (1 << RT_TAG_SHIFT) and (k1 - k0) <= 256
-        rt_bounds, pp, pr, pv = phased_transpose(R, rmat, nph, tag)
-        rt_ptr, rt_row, rt_val = i64(pp), i32(pr), f64(pv)
-        a_ptr, a_col, a_val = csr(A)
-        at_ptr, at_row, at_val = csr(At)
+        rt_bounds, rt_mats = phased_transpose(R, rmat, nph, tag)
+        sell_R = SellMatrix.by_block_chunks(R, rblk)
+        sell_A = SellMatrix.by_row(A)
+        sell_AT = SellMatrix.by_sorted_length(At)
         one = lambda t: t if t.numel() else torch.zeros(1, dtype=t.dtype, device=device)
         return cls(n=inst.n, m=inst.m, p=0, mq=inst.mq, L=inst.L, nr=nr, rblk=rblk.copy(),
                    k0=k0, k1=k1, l0=l0, l1=l1,
-                   r_ptr=r_ptr, r_col=one(r_col), r_val=one(r_val), rt_ptr=rt_ptr, rt_row=one(rt_row),
-                   rt_val=one(rt_val), rmat=one(i32(rmat)), C=one(f64(inst.C[k0:k1])), d=one(f64(inst.d[k0:k1])),
-                   a_ptr=a_ptr, a_col=one(a_col), a_val=one(a_val), at_ptr=at_ptr, at_row=one(at_row),
-                   at_val=one(at_val), b=one(f64(inst.b[l0:l1])), lower=f64(inst.primal_set.lower),
+                   sell_R=DeviceSell(sell_R, device), sell_A=DeviceSell(sell_A, device),
+                   sell_RT=[DeviceSell(t, device) for t in rt_mats], sell_AT=DeviceSell(sell_AT, device),
+                   rmat=one(i32(rmat)), C=one(f64(inst.C[k0:k1])), d=one(f64(inst.d[k0:k1])),
+                   b=one(f64(inst.b[l0:l1])), lower=f64(inst.primal_set.lower),
                    upper=f64(inst.primal_set.upper), mu=inst.mu, device=device,
                    nnz_r=int(R.nnz), nnz_a=int(A.nnz), rt_nph=nph, rt_bounds=rt_bounds, rt_tag=int(tag))

@@ -276,3 +276,52 @@ def test_c3_full_size_first_iterations():
     np.testing.assert_array_equal(tr[:, 1:5], tr_o[:, 1:5])
     assert rel(eng.last.x, res_o.x) <= 1e-9
     assert rel(eng.last.lam, res_o.lam) <= 1e-9
+
+
+def test_row_phases_do_not_change_bits(monkeypatch):
+    """The R^T gather continues every column's sum across the row phases in
+    row order (one launch per phase), and the c_i part continues its block
+    chain the same way: any phase count gives the same bits."""
+    arr = instances.factored_qcqp(n=1500, mq=5, rows=200, nnz_row=7, lin_rows=300, lin_nnz=4, seed=8,
+                                  x0_scale=0.1)
+    outs = []
+    for rows in ("100000", "500", "170"):            # 1, 3 and 8 phases of the 1200 stacked rows
+        monkeypatch.setenv("RAPDB_RT_PHASE_ROWS", rows)
+        inst = FactoredInstance.from_arrays(arr)
+        lam = np.abs(np.linspace(0.0, 1.0, inst.m))
+        lam[1] = 0.0                                  # a zero block weight: its gathers are skipped
+        x = np.linspace(-0.3, 0.4, arr.n)
+        gx = R.grad_x_coupling(inst, R.Iterate(x, np.zeros(0), lam))
+        eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.initial_iterate(inst))
+        eng.run_block(25)
+        outs.append((np.asarray(gx), trace_arr(eng.trace), np.asarray(eng.last.x), np.asarray(eng.last.lam),
+                     inst.device_data().rt_nph))
+    assert [o[4] for o in outs] == [1, 3, 8]
+    for o in outs[1:]:
+        for a, b in zip(outs[0][:4], o[:4]):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_gradient_matches_scipy_order(small):
+    """The three column parts of the device gradient -- sum_i w_i c_i (block
+    order), the R^T gather (row order, no FMA) and A^T mu -- restated with
+    scipy in the same order give the same bits."""
+    import scipy.sparse as sp
+    arr, inst, g = small
+    x, lam = g["probe_x"], g["probe_lam"]
+    gx = np.asarray(R.grad_x_coupling(inst, R.Iterate(x, np.zeros(0), lam)))
+    Rm = sp.csr_matrix(arr.R)
+    W = Rm @ x
+    wq = np.concatenate([[1.0], lam[:arr.mq]])
+    rmat = np.repeat(np.arange(arr.mq + 1), arr.rows)
+    Rt = Rm.T.tocsr()
+    Rt.sort_indices()
+    s = Rt @ (wq[rmat] * W)
+    acc = np.zeros(arr.n)
+    for i in range(arr.mq + 1):
+        if wq[i] != 0.0:
+            acc = acc + wq[i] * np.asarray(arr.C[i])
+    At = sp.csr_matrix(arr.A).T.tocsr()
+    At.sort_indices()
+    t = At @ lam[arr.mq:]
+    np.testing.assert_array_equal(gx, (acc + s) + t)

@@ -29,7 +29,7 @@ from paper_2605_29291_b200.sharding import Shard
 pytestmark = pytest.mark.gpu
 
 CASES = ["yx_nm", "xy_nm", "yx_mono_kkt", "adaptive_gap", "early", "rows", "factored_yx", "factored_xy",
-         "factored_inkernel", "peer", "comm", "egm", "points"]
+         "factored_phased", "peer", "comm", "egm", "points"]
 
 
 def _dense(n=130, m=9, rank=8, seed=3):
@@ -81,7 +81,7 @@ def _run_case(case):
         gap, cert, xc = eng.smoothed_gap(1, 0.04, 1e-9, None)
         out += _snapshot(eng) + [np.array([gap, cert.iterations, cert.residual])]
         guards.append(eng._ctx.check_guards())
-    elif case in ("factored_yx", "factored_xy", "factored_inkernel"):
+    elif case in ("factored_yx", "factored_xy", "factored_phased"):
         arr, inst = _factored()
         mode = "xy" if case == "factored_xy" else "yx"
         eng = R.ApdbEngine(inst, R.SolverConfig(mode=mode, nonmonotone=True), R.initial_iterate(inst))
@@ -114,8 +114,8 @@ def test_guards_and_determinism(case, monkeypatch):
         monkeypatch.setenv("RAPDB_EARLY_CHUNKS", "4")
     if case == "rows":
         monkeypatch.setenv("RAPDB_LAYOUT", "rows")
-    if case == "factored_inkernel":
-        monkeypatch.setenv("RAPDB_FAC_HOST", "0")
+    if case == "factored_phased":   # several row phases of R^T (one gradient launch each)
+        monkeypatch.setenv("RAPDB_RT_PHASE_ROWS", "300")
     a, ga = _run_case(case)
     b, gb = _run_case(case)
     for n_bad, rep in ga + gb:

@@ -76,16 +76,20 @@ def test_phased_transpose_walks_columns_in_row_order():
     full = R.T.tocsr()
     full.sort_indices()
     for nph, tag in ((1, False), (3, True), (7, True)):
-        bounds, ptr, rows, vals = phased_transpose(R, rmat, nph, tag)
-        assert bounds[0] == 0 and bounds[-1] == nr and ptr.shape == (nph * (n + 1),)
+        bounds, mats = phased_transpose(R, rmat, nph, tag)
+        assert bounds[0] == 0 and bounds[-1] == nr and len(mats) == nph
+        cols = [([], []) for _ in range(n)]
+        for S in mats:                      # Sell per phase: slot -> column via map
+            assert sorted(int(j) for j in S.map if j >= 0) == list(range(n))
+            for s_ in range(S.nslots):
+                j = int(S.map[s_])
+                pos = int(S.sp[s_ >> 5]) + 32 * np.arange(int(S.len[s_])) + (s_ & 31)
+                if j >= 0:
+                    cols[j][0].append(S.idx[pos])
+                    cols[j][1].append(S.val[pos])
         for j in range(n):
-            seg_r, seg_v = [], []
-            for p in range(nph):
-                a, b = ptr[p * (n + 1) + j], ptr[p * (n + 1) + j + 1]
-                seg_r.append(rows[a:b])
-                seg_v.append(vals[a:b])
-            r = np.concatenate(seg_r).astype(np.int64)
-            v = np.concatenate(seg_v)
+            r = np.concatenate(cols[j][0]).astype(np.int64)
+            v = np.concatenate(cols[j][1])
             if tag:
                 np.testing.assert_array_equal(r >> RT_TAG_SHIFT, rmat[r & ((1 << RT_TAG_SHIFT) - 1)])
                 r = r & ((1 << RT_TAG_SHIFT) - 1)

@@ -29,3 +29,5 @@ layout = getattr(ev.ctx.data, "layout", "rows")
 streamed = (arr.m + 1) * _capi.packed_doubles(arr.n) * 8 if layout == "packed" else dense
 print(f"{name} [{layout}]: {ms:.4f} ms/sweep  {streamed / ms / 1e6:.1f} GB/s streamed "
       f"({streamed / 1e9:.3f} GB)  {dense / ms / 1e6:.1f} GB/s dense-equivalent  (reps={reps})")
+os.makedirs("gpurun_out", exist_ok=True)
+open(f"gpurun_out/streamed_{name}.txt", "w").write(str(int(streamed)))

@@ -5,7 +5,7 @@
            smoothed gap inside an adaptive run), early (packed sweep with the
            early reduction forced on: 24 matrices), rows (row-major layout),
            factored (factored path, host-launched kernels), factored_fused
-           (RAPDB_FAC_HOST=0: everything in the persistent kernel), peer (in-kernel
+           (RAPDB_RT_PHASE_ROWS=300: several row phases of R^T), peer (in-kernel
            peer exchange at world size 1), comm (native NCCL exchange at world
            size 1), egm (extragradient op), probe (sweep / grad_x / kkt at a point)
 
@@ -24,7 +24,7 @@ if case == "early":
 if case == "rows":
     os.environ["RAPDB_LAYOUT"] = "rows"
 if case == "factored_fused":
-    os.environ["RAPDB_FAC_HOST"] = "0"
+    os.environ["RAPDB_RT_PHASE_ROWS"] = "300"
 
 import paper_2605_29291_b200 as R  # noqa: E402
 from paper_2605_29291_b200 import instances  # noqa: E402

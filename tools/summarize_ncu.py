@@ -72,9 +72,44 @@ def full(rep, out, alg_bytes):
     print(json.dumps({k: v for k, v in summ.items() if k != "metrics"}, indent=1))
 
 
+MULTI = KEYS + ["lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__data_pipe_lsu_wavefronts.sum",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+                "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "lts__t_sectors.sum",
+                "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg", "sm__cycles_active.avg",
+                "smsp__cycles_active.avg", "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed",
+                "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+                "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct", "launch__occupancy_limit_registers",
+                "sm__warps_active.avg.per_cycle_active"]
+
+
+def multi(rep, out):
+    """One row per captured kernel launch (a report with several kernels)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    res = []
+    for vals in rows[2:]:
+        if len(vals) <= ki:
+            continue
+        d = {"kernel": vals[ki]}
+        for i, h in enumerate(hdr):
+            if h in MULTI and i < len(vals):
+                d[h] = f"{vals[i]} {units[i]}".strip()
+        res.append(d)
+    json.dump(res, open(out + ".json", "w"), indent=1)
+    for d in res:
+        print(d["kernel"][:50], d.get("gpu__time_duration.sum"), d.get("dram__bytes_read.sum"),
+              d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+              d.get("l1tex__data_pipe_lsu_wavefronts.sum"))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "multi":
+        multi(sys.argv[2], sys.argv[3])
     else:
         ab = float(sys.argv[sys.argv.index("--bytes") + 1]) if "--bytes" in sys.argv else 0.0
         full(sys.argv[2], sys.argv[3], ab)
