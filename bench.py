@@ -17,6 +17,9 @@ timed on a fixed 1000-iteration budget and reported under ``nonmonotone``).
 * ``c2``           BASELINE C2 (n=4096, m=512, 69 GB dense / 34.7 GB packed),
                    generated on the device and sharded over the same N ranks:
                    it/s, time to KKT and sweep GB/s per GPU (the 6x target's basis).
+* ``c3f``          BASELINE C3 (factored sparse, n = 10^6; feasible x0 variant) on
+                   the same N ranks: it/s, time to KKT, time per test evaluation
+                   against its HBM bytes and against the measured gather ceiling.
 * ``ms_per_step``  = time-to-1e-6-KKT of one solve.
 * ``e2e``          the same solve through the public API with the instance on
                    the HOST: pinned H2D of the 6.4 GB Q stack + vectors, solve,
@@ -69,6 +72,7 @@ def parse():
                     help="wall-clock cap of the CPU solve to KKT (reported as not converged beyond it)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--c2-steps", type=int, default=1, help="timed C2 solves (0: no c2 block)")
+    ap.add_argument("--c3-steps", type=int, default=1, help="timed C3f solves (0: no c3f block)")
     return ap.parse_args()
 
 
@@ -388,6 +392,59 @@ def c2_block(R, args, dev, shard_fn, ranks, ws, peak):
     return out
 
 
+def c3f_block(R, args, dev, shard_fn, ranks, ws, peak):
+    """BASELINE C3 (factored sparse, n = 10^6) with x0 ~ U(-0.01, 0.01) -- the
+    config's own x0 ~ U(-1, 1) admits no feasible point (tools/c3_infeasibility.py)
+    -- constraint-sharded over the job's ranks.  Per test evaluation the path
+    gathers 2 (nnz R + nnz A) doubles (one L1 line lookup each: the bound of
+    the sparse passes, tools/gather_probe.cu) and streams eval_bytes from HBM."""
+    import torch
+    from paper_2605_29291_b200 import instances
+    t0 = time.perf_counter()
+    arr = instances.factored_qcqp(x0_scale=0.01)
+    inst = R.FactoredInstance.from_arrays(arr)
+    shard = shard_fn(inst)
+    kw = {} if shard is None else {"krange": (shard.k0, shard.k1), "lrange": (shard.l0, shard.l1)}
+    inst.device_data(dev, **kw)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    cfg = R.SolverConfig(mode="yx", nonmonotone=False)
+    crit = R.TerminationCriteria(criterion="conic", eps_kkt=1e-6, eps_feas=1e-6)
+    results, t_ms = timed_solves(R, inst, cfg, R.FixedRestart(500), crit, dev, shard, ranks,
+                                 args.c3_steps, 1, budget=5000)
+    res = results[-1]
+    nnz_r, nnz_a = int(inst.R.nnz), int(inst.A.nnz)
+    eval_bytes = 2 * 12 * nnz_r + 2 * 8 * (inst.mq + 1) * inst.n + 2 * 12 * nnz_a
+    gathers = 2 * (nnz_r + nnz_a)
+    evals = sum(r.evals for r in results)
+    per_eval_s = (t_ms / 1e3) / max(evals, 1)
+    ceiling = None
+    probe = os.path.join(ROOT, "profiles", "r02c_gather_probe.json")
+    if os.path.exists(probe):
+        try:
+            rows = json.load(open(probe))["results"]
+            ceiling = max(r["ggather_s"] for r in rows if r["variant"].startswith("ldg8idx"))
+        except Exception:
+            ceiling = None
+    out = {"workload": "C3f: factored sparse QCQP n=1e6, 64 quadratic rows R_i^T R_i (1e5 x n, 10 nnz/row), "
+                       "5e5 linear rows (5 nnz), x0 ~ U(-0.01, 0.01)",
+           "policy": "yx monotone + FixedRestart(500), conic KKT 1e-6",
+           "n_gpus": ws, "shard_range": None if shard is None else [shard.k0, shard.k1, shard.l0, shard.l1],
+           "iters_per_s": res.iterations * args.c3_steps / (t_ms / 1e3), "time_to_kkt_ms": t_ms / args.c3_steps,
+           "iterations": res.iterations, "evals": res.evals, "converged": bool(res.converged),
+           "final_kkt": res.metrics.kkt_residual, "us_per_eval": 1e6 * per_eval_s,
+           "eval_bytes": eval_bytes, "eval_gbs": eval_bytes / ws / per_eval_s / 1e9,
+           "eval_frac_of_hbm_peak": eval_bytes / ws / per_eval_s / 1e9 / peak,
+           "gathers_per_eval": gathers, "ggather_s": gathers / ws / per_eval_s / 1e9,
+           "gather_ceiling_ggather_s": ceiling,
+           "frac_of_gather_ceiling": None if not ceiling else gathers / ws / per_eval_s / 1e9 / ceiling,
+           "bound": "L1 wavefront rate of the 8-byte gathers (whole trial incl. control steps and launch gaps "
+                    "over the gathers alone); HBM bytes are below the stream's time",
+           "generate_upload_s": gen_s, "steps": args.c3_steps, "warmup": 1}
+    inst.drop_device_data()
+    return out
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -509,6 +566,10 @@ def main():
     if args.c2_steps > 0 and not device_generated:
         c2 = c2_block(R, args, dev, shard_fn, ranks, ws, peak)
 
+    c3f = None
+    if args.c3_steps > 0 and not device_generated:
+        c3f = c3f_block(R, args, dev, shard_fn, ranks, ws, peak)
+
     if rank == 0:
         cpu = None
         if not args.skip_cpu and ws == 1 and not device_generated:
@@ -567,6 +628,7 @@ def main():
             "nonmonotone": {"iters_per_s": rnm.iterations / tn, "iterations": rnm.iterations,
                             "evals": rnm.evals, "budget": 1000, "final_kkt": rnm.metrics.kkt_residual},
             "c2": c2,
+            "c3f": c3f,
             "gpu_launches": int(launches),
             "clocks": clk,
         }

@@ -61,7 +61,8 @@ STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GL
               "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
               "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN", "P_KKT",
               "E_INIT", "E_GX", "E_HALF", "E_HSWEEP", "E_HGLOC", "E_GXH", "E_PLUS", "E_PSWEEP", "E_PGLOC",
-              "E_POST", "DONE"] + [""] * 14 + ["sweep:stage_x", "sweep:stream", "sweep:reduce", ""]
+              "E_POST", "DONE"] + [""] * 14 + ["sweep:stage_x", "sweep:stream", "sweep:reduce"]
+assert len(STEP_NAMES) == 64 and STEP_NAMES[61] == "sweep:stage_x"   # SolverState::step_ns (rapdb_dev.cuh)
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4

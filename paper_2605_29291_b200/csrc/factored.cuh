@@ -46,44 +46,25 @@ constexpr int kRowU = 5;       // gathers in flight per lane in the row pass (C3
 // order of scipy's csr_matvec, so W = R x and the R^T / A^T column sums match
 // the factored restatement bit for bit -- starting from s.  The t-th loads of
 // val / idx are one coalesced access per warp (no shared-memory staging), U
-// gathers in flight per lane; evict-first streams keep the gathered vector in
-// L2.  The CSR passes are bound by the L1 wavefront rate of their 8-byte
-// gathers (one 128-byte line lookup per lane: ~245 G gathers/s measured on a
-// B200, tools/gather_probe.cu), so every wavefront spent on anything else --
-// staging stores, bank-conflicted shared loads, uncoalesced streams -- is time.
-template <int U>
-__device__ __forceinline__ double sell_dot(const Sell& M, long long slice, const double* x, double s, uint64_t ef) {
-  const int lane = threadIdx.x & 31;
-  const long long base = __ldg(M.sp + slice);
-  const int width = (int)((__ldg(M.sp + slice + 1) - base) >> 5);
-  const int len = __ldg(M.len + slice * 32 + lane);
-  const int* ip = M.idx + base + lane;
-  const double* vp = M.val + base + lane;
-  for (int t0 = 0; t0 < width; t0 += U) {
-    int c[U];
-    double v[U], xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (t0 + u < len) { c[u] = ld_stream(ip + (long long)(t0 + u) * 32, ef); v[u] = ld_stream(vp + (long long)(t0 + u) * 32, ef); }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (t0 + u < len) xv[u] = ldcg(x + c[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (t0 + u < len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
-  }
-  return s;
-}
-
+// entries per lane at a time.  The passes are bound by the L1 wavefront rate
+// (LSU data pipe, ~1 wavefront per cycle and SM): a gather costs one 128-byte
+// line lookup per lane (~250 G gathers/s measured on a B200,
+// tools/gather_probe.cu), so every wavefront spent on anything else -- staging
+// stores, bank-conflicted shared loads, uncoalesced streams -- is time.
+// Measured at C3 (profiles/r02*_c3*): both passes run at ~0.95 wavefronts
+// per cycle; of the variants tried (U = 2..10 at 2..8 CTAs per SM, double-
+// buffered loads with TMA L2 prefetch, TMA-fed shared-memory rings with 7 / 14
+// gather warps) this plain one -- U = 4..5, 4 CTAs per SM, a contiguous run of
+// slices per warp -- is the fastest.
 constexpr int kRtTagShift = 23;
 constexpr int kRtRowMask = (1 << kRtTagShift) - 1;
 
-// The same over a slice of R^T with tagged rows: entry (r | blk << 23, v)
-// adds v * (wq[blk] * W[r]).  A zero weight adds +-0 to a sum that starts at
-// +0 -- a no-op -- so its gather is skipped: the pass costs the active blocks.
-template <int U>
-__device__ __forceinline__ double sell_dot_tagged(const Sell& M, long long slice, const double* W, const double* wq,
-                                                  double s, uint64_t ef) {
+// TAG: entry (r | blk << 23, v) of R^T adds v * (wq[blk] * W[r]).  A zero
+// weight adds +-0 to a sum that starts at +0 -- a no-op -- so its gather is
+// skipped: the pass costs the active blocks.
+template <int U, bool TAG>
+__device__ __forceinline__ double sell_dot(const Sell& M, long long slice, const double* x, const double* wq,
+                                           double s, uint64_t ef) {
   const int lane = threadIdx.x & 31;
   const long long base = __ldg(M.sp + slice);
   const int width = (int)((__ldg(M.sp + slice + 1) - base) >> 5);
@@ -99,17 +80,23 @@ __device__ __forceinline__ double sell_dot_tagged(const Sell& M, long long slice
       if (t0 + u < len) {
         c[u] = ld_stream(ip + (long long)(t0 + u) * 32, ef);
         v[u] = ld_stream(vp + (long long)(t0 + u) * 32, ef);
-        wt[u] = wq[c[u] >> kRtTagShift];
+        wt[u] = TAG ? wq[c[u] >> kRtTagShift] : 1.0;
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (wt[u] != 0.0) xv[u] = ldcg(W + (c[u] & kRtRowMask));
+      if (wt[u] != 0.0) xv[u] = ldcg(x + (TAG ? (c[u] & kRtRowMask) : c[u]));
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (wt[u] != 0.0) s = __dadd_rn(s, __dmul_rn(v[u], __dmul_rn(wt[u], xv[u])));
+      if (wt[u] != 0.0) s = __dadd_rn(s, __dmul_rn(v[u], TAG ? __dmul_rn(wt[u], xv[u]) : xv[u]));
   }
   return s;
+}
+
+// the contiguous share [lo, hi) of `items` items for member `me` of `n`
+__device__ __forceinline__ void my_range(long long items, long long me, long long n, long long& lo, long long& hi) {
+  lo = items * me / n;
+  hi = items * (me + 1) / n;
 }
 
 // rows [r0, r1) of W chunk c (wch[i] = first chunk of local block i)
@@ -132,7 +119,15 @@ __device__ __forceinline__ double cx_item(const DevProblem& P, const double* x, 
   const long long j0 = ch * kCxCols, j1 = min(j0 + kCxCols, n);
   const double* ci = P.q + i * n;
   double s = 0.0;
-  for (long long j = j0 + lane; j < j1; j += 32) s = fma(__ldg(ci + j), ldcg(x + j), s);
+  long long j = j0 + lane;
+  for (; j + 7 * 32 < j1; j += 8 * 32) {   // 16 loads in flight, the same fma chain
+    double c[8], xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { c[k] = __ldg(ci + j + 32 * k); xv[k] = ldcg(x + j + 32 * k); }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = fma(c[k], xv[k], s);
+  }
+  for (; j < j1; j += 32) s = fma(__ldg(ci + j), ldcg(x + j), s);
   return warp_sum(s);
 }
 
@@ -166,7 +161,7 @@ constexpr int kGxU = 4;       // gathers in flight per lane in the transposed pa
 // resident CTAs per SM of the standalone kernels: the gather rate needs only a
 // few dozen warp-gathers in flight per SM (one costs 32 L1 wavefronts), so
 // registers for the unrolled loads matter more than occupancy
-constexpr int kRowCtas = 3, kGradCtas = 4;
+constexpr int kRowCtas = 4, kGradCtas = 4;
 
 __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, int i0, int i1,
                                             double acc, uint64_t ef) {
@@ -202,20 +197,16 @@ __device__ __forceinline__ void fac_gather_item(const DevProblem& P, const Work&
   if (it < nrt) {
     const int j = __ldg(M.map + it * 32 + lane);
     double s = (ph > 0 && j >= 0) ? ldcg(out + j) : 0.0;
-    s = TAG ? sell_dot_tagged<kGxU>(M, it, Wsrc, wq, s, ef) : sell_dot<kGxU>(M, it, Wsrc, s, ef);
+    s = sell_dot<kGxU, TAG>(M, it, Wsrc, wq, s, ef);
     if (j >= 0) out[j] = s;
   } else {
     const long long sl = it - nrt;
     const Sell& T = P.sell[kSellAt];
     const int j = __ldg(T.map + sl * 32 + lane);
-    const double t = sell_dot<kGxU>(T, sl, lam + P.mq + P.l0, 0.0, ef);
+    const double t = sell_dot<kGxU, false>(T, sl, lam + P.mq + P.l0, nullptr, 0.0, ef);
     if (j >= 0) w.aux2[j] = t;
   }
 }
-__device__ __forceinline__ long long fac_gather_items(const DevProblem& P, int ph) {
-  return (P.sell[kSellRt + ph].nslots >> 5) + (ph == 0 ? (P.sell[kSellAt].nslots >> 5) : 0);
-}
-
 // ---------------------------------------------------------------- row pass
 // |W_i|^2 over chunk c: lane r0 + lane, + 32, ... with fma, then the butterfly
 // (formed on the fly by the row pass: 4 slices of 32 rows per chunk)
@@ -228,7 +219,7 @@ __device__ __forceinline__ void fac_chunk(const DevProblem& P, const Work& w, co
   for (int g = 0; g < kWChunk / 32; ++g) {
     const long long row = r0 + 32 * g + lane;
     if (r0 + 32 * g >= r1) break;
-    const double v = sell_dot<kRowU>(P.sell[kSellR], c * (kWChunk / 32) + g, x, 0.0, ef);
+    const double v = sell_dot<kRowU, false>(P.sell[kSellR], c * (kWChunk / 32) + g, x, nullptr, 0.0, ef);
     if (row < r1) {
       st_keep(W + row, v, el);
       s2 = fma(v, v, s2);
@@ -242,7 +233,7 @@ __device__ __forceinline__ void fac_chunk(const DevProblem& P, const Work& w, co
 __device__ __forceinline__ void fac_arows(const DevProblem& P, const double* x, double* gv_lin, long long sl,
                                           uint64_t ef) {
   const long long j = sl * 32 + (threadIdx.x & 31);
-  const double v = sell_dot<kRowU>(P.sell[kSellA], sl, x, 0.0, ef);
+  const double v = sell_dot<kRowU, false>(P.sell[kSellA], sl, x, nullptr, 0.0, ef);
   if (j < P.Lloc) gv_lin[j] = v - __ldg(P.b + j);
 }
 
@@ -310,11 +301,11 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) fac_row_kernel(DevProblem 
   double* W = w.W + (long long)par * P.nr;
   double* gv = w.gval + (long long)par * (P.m + 1) + 1 + P.mq + P.l0;
   const long long nch = __ldg(P.wch + P.fnb);
-  const long long items = nch + (P.sell[kSellA].nslots >> 5);
-  for (long long it = me; it < items; it += nrole) {
-    if (it < nch) fac_chunk(P, w, x, W, it, ef, el);
-    else fac_arows(P, x, gv, it - nch, ef);
-  }
+  long long lo, hi;
+  my_range(nch, me, nrole, lo, hi);                       // a contiguous run of W chunks ...
+  for (long long it = lo; it < hi; ++it) fac_chunk(P, w, x, W, it, ef, el);
+  my_range(P.sell[kSellA].nslots >> 5, me, nrole, lo, hi);   // ... then one of A's slices
+  for (long long it = lo; it < hi; ++it) fac_arows(P, x, gv, it, ef);
 }
 
 // Gradient part 1, row phase ph (lam = the trial multipliers) at the W-cache
@@ -339,8 +330,14 @@ __global__ void __launch_bounds__(kThreads, kGradCtas) fac_grad_kernel(DevProble
     return;
   }
   const long long me = (gw >> 2) * 3 + (gw & 3), nrole = (nw >> 2) * 3;
-  const long long items = fac_gather_items(P, ph);
-  for (long long it = me; it < items; it += nrole) fac_gather_item<TAG>(P, w, Wsrc, wq, lam, out, ph, it, ef);
+  const long long nrt = P.sell[kSellRt + ph].nslots >> 5;
+  long long lo, hi;
+  my_range(nrt, me, nrole, lo, hi);                       // a contiguous run of R^T's slices ...
+  for (long long it = lo; it < hi; ++it) fac_gather_item<TAG>(P, w, Wsrc, wq, lam, out, ph, it, ef);
+  if (ph == 0) {                                          // ... then one of A^T's
+    my_range(P.sell[kSellAt].nslots >> 5, me, nrole, lo, hi);
+    for (long long it = lo; it < hi; ++it) fac_gather_item<TAG>(P, w, Wsrc, wq, lam, out, ph, nrt + it, ef);
+  }
 }
 
 // Gradient part 2, thread per column: gx = (acc + s) + t into out.  With

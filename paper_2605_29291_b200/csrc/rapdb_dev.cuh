@@ -98,6 +98,7 @@ enum Xkind { X_NONE = 0, X_GX = 1, X_G = 2, X_GX2 = 3, X_H = 4 };
 // entries in stored order.  A slice is as wide as its longest slot.
 struct Sell {
   long long nslots;      // multiple of 32
+  long long entries;     // sp[nslots / 32]: stored entries incl. padding
   const long long* sp;   // [nslots / 32 + 1] entry offset of each slice
   const int* idx;        // gathered index of each entry
   const double* val;

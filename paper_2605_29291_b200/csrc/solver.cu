@@ -633,16 +633,20 @@ int fac_gradient(rapdb_ctx* c, const Work& w, const double* Wpar, const double* 
   return RAPDB_OK;
 }
 
+// the row pass at x into parity par
+static void launch_row_pass(rapdb_ctx* c, const double* x, int par) {
+  fac_row_kernel<<<c->nsm * kRowCtas, kThreads, 0, c->stream>>>(c->P, c->w, x, par);
+  ++g_launches;
+}
+
 int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
   const DevProblem& P = c->P;
   const Work& w = c->w;
   const long long n = P.n, np = (long long)P.p + P.m;
-  const int rgrid = c->nsm * kRowCtas;   // row pass: all CTAs resident (8 warps each: a multiple of 4 warps)
   if (st.fq[0] == 1) {
     const int par = st.fq[1];
     const double* x = st.fq[2] ? rc.in_x : w.x + (long long)par * n;
-    fac_row_kernel<<<rgrid, kThreads, 0, c->stream>>>(P, w, x, par);
-    ++g_launches;
+    launch_row_pass(c, x, par);
   } else if (st.fq[0] == 2) {
     for (int k = 0; k < st.fq[1] && k < 2; ++k) {
       const int par = st.fq[2 + 3 * k], lid = st.fq[3 + 3 * k], oid = st.fq[4 + 3 * k];
@@ -655,8 +659,7 @@ int serve_factored(rapdb_ctx* c, const RunCfg& rc, const SolverState& st) {
     // pass (W, |W|^2, A x - b, c_i . x) at x_new
     const int cur = st.fq[1];
     fac_gradient(c, w, w.W + (long long)cur * P.nr, w.ytr + P.p, w.gxs, true, st.tau, cur);
-    fac_row_kernel<<<rgrid, kThreads, 0, c->stream>>>(P, w, w.x + (long long)(cur ^ 1) * n, cur ^ 1);
-    ++g_launches;
+    launch_row_pass(c, w.x + (long long)(cur ^ 1) * n, cur ^ 1);
   } else {
     return fail(c, RAPDB_EDEVICE, "unknown factored request");
   }
@@ -1279,7 +1282,7 @@ static int take_sell(rapdb_ctx* c, const rapdb_sell* in, long long want_slots, b
   CK(cudaMemcpy(entries, in->sp + (in->nslots >> 5), 8, cudaMemcpyDeviceToHost));
   if (*entries < 0 || (*entries & 31) || (*entries > 0 && (!in->idx || !in->val)))
     return fail(c, RAPDB_EINPUT, std::string("bad Sell entry arrays: ") + name);
-  out->nslots = in->nslots; out->sp = in->sp; out->idx = in->idx; out->val = in->val;
+  out->nslots = in->nslots; out->entries = *entries; out->sp = in->sp; out->idx = in->idx; out->val = in->val;
   out->len = in->len; out->map = in->map;
   return RAPDB_OK;
 }

@@ -39,3 +39,17 @@ print(f"{name}: {res.iterations} it, {res.evals} evals; span {span / 1e3:.2f} ms
       f"({100 * busy / span:.1f}% busy); per eval {span / max(res.evals, 1):.1f} us")
 for k, (c, t) in sorted(tot.items(), key=lambda kv: -kv[1][1])[:12]:
     print(f"  {c:6d}  {t / 1e3:9.2f} ms  {t / c:8.1f} us/launch  {t / max(res.evals, 1):7.1f} us/eval  {k}")
+# idle gap in front of each device activity (start - end of the previous one), by activity name
+evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+             key=lambda e: e.time_range.start)
+gap = defaultdict(lambda: [0, 0.0])
+prev_end = None
+for e in evs:
+    if prev_end is not None:
+        g = max(0.0, e.time_range.start - prev_end)
+        gap[e.name[:60]][0] += 1
+        gap[e.name[:60]][1] += g
+    prev_end = max(prev_end or 0, e.time_range.end)
+print("idle before:")
+for k, (c, t) in sorted(gap.items(), key=lambda kv: -kv[1][1])[:8]:
+    print(f"  {c:6d}  {t / 1e3:9.2f} ms  {t / c:8.1f} us each  {t / max(res.evals, 1):7.1f} us/eval  {k}")

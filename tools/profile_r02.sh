@@ -34,7 +34,7 @@ fi
 if has launches; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file gpurun_out/launches_$TAG.csv \
-      python bench.py --steps 2 --warmup 1 --skip-cpu --c2-steps 0 > gpurun_out/ncu_launch_$TAG.log 2>&1
+      python bench.py --steps 2 --warmup 1 --skip-cpu --c2-steps 0 --c3-steps 0 > gpurun_out/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?"
 fi
 if has c1; then
