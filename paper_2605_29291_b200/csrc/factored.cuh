@@ -23,12 +23,12 @@
 //                beside the gather-bound sparse rows
 // The sparse operands are sliced ELLPACK (rapdb_dev.cuh Sell): coalesced
 // streams with no staging, each row / column summed in stored order without
-// FMA.  The passes are bound by the L1 wavefront rate of their 8-byte gathers
-// (~65 M per pass at C3, one line lookup each; tools/gather_probe.cu), not by
-// HBM bytes: fusing the dense C streams into them costs little and saves a
-// pass and a stop.  Per yx trial ~2.7 GB (R and R^T 780 MB each, C 2 x 520 MB,
-// A, A^T) and one stop of the persistent kernel.  Every reduction has a fixed
-// order.
+// FMA.  The passes are bound by the 32-byte L2 sectors their 8-byte gathers
+// move (~65 M per pass at C3; tools/gather_probe.cu), not by HBM bytes: the
+// dense C streams ride along in the same launches, which saves a pass and a
+// stop.  Per yx trial ~2.7 GB from HBM (R and R^T 780 MB each, C 2 x 520 MB,
+// A, A^T), ~7.6 GB of L2 -> SM sectors, and one stop of the persistent
+// kernel.  Every reduction has a fixed order.
 #pragma once
 #include "solver_kernel.cuh"
 
@@ -39,23 +39,37 @@ __device__ __forceinline__ long long nwarps() { return (long long)gridDim.x * kW
 
 constexpr int kWChunk = 128;    // rows of W per |W_i|^2 partial (inside one block)
 constexpr int kCxCols = 1024;   // columns per c_i . x partial
-constexpr int kRowU = 5;       // gathers in flight per lane in the row pass (C3: 10 per row of R)
+// tunables of the standalone kernels (A/B builds: tools/c3_variants.sh)
+#ifndef RAPDB_ROWU
+#define RAPDB_ROWU 5
+#endif
+#ifndef RAPDB_GXU
+#define RAPDB_GXU 4
+#endif
+#ifndef RAPDB_ROWCTAS
+#define RAPDB_ROWCTAS 4
+#endif
+#ifndef RAPDB_GRADCTAS
+#define RAPDB_GRADCTAS 4
+#endif
+constexpr int kRowU = RAPDB_ROWU;       // gathers in flight per lane in the row pass (C3: 10 per row of R)
 
 // One slice of a Sell operand against a gathered vector: lane l folds the
 // entries of slot 32 * slice + l in stored order without FMA -- the operation
 // order of scipy's csr_matvec, so W = R x and the R^T / A^T column sums match
 // the factored restatement bit for bit -- starting from s.  The t-th loads of
 // val / idx are one coalesced access per warp (no shared-memory staging), U
-// entries per lane at a time.  The passes are bound by the L1 wavefront rate
-// (LSU data pipe, ~1 wavefront per cycle and SM): a gather costs one 128-byte
-// line lookup per lane (~250 G gathers/s measured on a B200,
-// tools/gather_probe.cu), so every wavefront spent on anything else -- staging
-// stores, bank-conflicted shared loads, uncoalesced streams -- is time.
-// Measured at C3 (profiles/r02*_c3*): both passes run at ~0.95 wavefronts
-// per cycle; of the variants tried (U = 2..10 at 2..8 CTAs per SM, double-
-// buffered loads with TMA L2 prefetch, TMA-fed shared-memory rings with 7 / 14
-// gather warps) this plain one -- U = 4..5, 4 CTAs per SM, a contiguous run of
-// slices per warp -- is the fastest.
+// entries per lane at a time.  The passes are bound by what the gathers pull
+// out of L2: every 8-byte gather moves a 32-byte sector to the SM, 65 M per
+// pass at C3 (tools/gather_probe.cu: at most ~250-270 G gathers/s on a B200,
+// i.e. ~9-10 TB/s of L2 -> SM sectors with the index stream), and the R / C / x
+// streams share that path: ~4 GB per row pass, ~3.6 GB per gradient.  Measured
+// at C3 (profiles/r02j_c3*): row pass 358 us, gradient 2 x 205 us -- 11 / 9 TB/s
+// of sectors; every variant tried lands there or worse (U = 2..10 at 2..8 CTAs
+// per SM, double-buffered loads with TMA L2 prefetch, TMA-fed shared-memory
+// rings with 7 / 14 gather warps, x staged in shared memory for c_i . x:
+// profiles/r02j_c3_variant_sweep.log), so the plain form stays: U = 4..5,
+// 4 CTAs per SM, a contiguous run of slices per warp.
 constexpr int kRtTagShift = 23;
 constexpr int kRtRowMask = (1 << kRtTagShift) - 1;
 
@@ -157,11 +171,11 @@ __device__ __forceinline__ void fac_wl(const DevProblem& P, const Work& w, const
 // The gather of phase p reads only rows [rt_b[p], rt_b[p+1]) of the W-cache:
 // phases run one after the other over the whole grid (separate launches), so
 // the gathered slice stays L2-resident.
-constexpr int kGxU = 4;       // gathers in flight per lane in the transposed passes
+constexpr int kGxU = RAPDB_GXU;       // gathers in flight per lane in the transposed passes
 // resident CTAs per SM of the standalone kernels: the gather rate needs only a
 // few dozen warp-gathers in flight per SM (one costs 32 L1 wavefronts), so
 // registers for the unrolled loads matter more than occupancy
-constexpr int kRowCtas = 4, kGradCtas = 4;
+constexpr int kRowCtas = RAPDB_ROWCTAS, kGradCtas = RAPDB_GRADCTAS;
 
 __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, int i0, int i1,
                                             double acc, uint64_t ef) {

@@ -14,7 +14,7 @@ fi
 if has times; then
   for rows in ${PHASE_ROWS:-8388608 4194304 2097152 1048576}; do
     echo "== RAPDB_RT_PHASE_ROWS=$rows"
-    RAPDB_RT_PHASE_ROWS=$rows timeout 600 python tools/kernel_times.py C3f 100 2>&1 | tail -9
+    RAPDB_RT_PHASE_ROWS=$rows timeout 600 python tools/kernel_times.py C3f 100 2>&1 | tail -22
   done > gpurun_out/c3_times_$TAG.log 2>&1
   cat gpurun_out/c3_times_$TAG.log
 fi
