@@ -13,7 +13,7 @@ reset).
 Small instances of: yx / xy, monotone / non-monotone, fixed restarts, KKT,
 the smoothed gap (adaptive), the packed sweep's early reduction, the
 row-major layout, the factored path (fused host-launched trial, generic
-stops, in-kernel), the peer exchange and the native NCCL exchange at world
+stops, several row phases of R^T), the peer exchange and the native NCCL exchange at world
 size 1, EGM and the point evaluations.
 """
 

@@ -1,7 +1,7 @@
 """One-off full-size parity check of a BASELINE config against the CPU oracle
 (too slow for the test suite): the first K accepted iterations of yx
 monotone and non-monotone, step sizes bitwise, iterates to 1e-9.
-python tools/validate_full.py C2 20  -> prints one JSON line"""
+python tools/validate_full.py C2 20 [mono|nm]  -> prints one JSON line"""
 import json
 import os
 import sys
@@ -16,6 +16,7 @@ from oracle import rapdb_oracle as O  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+only = sys.argv[3] if len(sys.argv) > 3 else None      # "mono" / "nm": one case only
 t0 = time.time()
 arr = instances.config_instance(name)
 gen_s = time.time() - t0
@@ -23,6 +24,8 @@ inst = R.ProblemInstance.from_arrays(arr, validate=False)
 P = O.Problem.from_arrays(arr)
 out = {"config": name, "n": arr.n, "m": arr.m, "iterations": K, "generate_s": gen_s, "cases": {}}
 for nm in (False, True):
+    if only is not None and only != ("nm" if nm else "mono"):
+        continue
     t0 = time.time()
     eng = O.Engine(P, O.Options(mode="yx", nonmonotone=nm), *O.initial_point(P))
     for _ in range(K):
