@@ -777,10 +777,16 @@ int read_state(rapdb_ctx* c, SolverState* st) {
   }
   int* h_ab = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_state) + sizeof(SolverState));
   CK(cudaMemcpyAsync(c->h_state, c->w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(h_ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *st = *c->h_state;
-  ab = *h_ab;
+  // a stop on the way (exchange point / factored request) left through the
+  // normal exit: every abort path sets ST_ABORT, so the watchdog flag is only
+  // fetched when the op ended -- one copy less per stop
+  if (st->status != ST_EXCHANGE) {
+    CK(cudaMemcpyAsync(h_ab, c->w.abort_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    ab = *h_ab;
+  }
   if (ab) {
     int info[20] = {0};
     cudaMemcpy(info, c->w.abort_flag, sizeof(info), cudaMemcpyDeviceToHost);
