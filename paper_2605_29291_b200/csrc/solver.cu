@@ -558,8 +558,18 @@ int launch_once(rapdb_ctx* c, const RunCfg& rc) {
   K.w = c->w;
   K.rc = rc;
   K.px = c->px;
-  CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
-  CK(cudaMemsetAsync(c->w.abort_flag, 0, 128, c->stream));
+  // grid-barrier word and watchdog flag: neighbours in the workspace (one
+  // memset unless guard zones sit between them)
+  {
+    const char* b0 = reinterpret_cast<const char*>(c->w.bar);
+    const char* a0 = reinterpret_cast<const char*>(c->w.abort_flag);
+    if (!c->guard && a0 > b0 && a0 - b0 <= 1024) {
+      CK(cudaMemsetAsync(c->w.bar, 0, (size_t)(a0 - b0) + 128, c->stream));
+    } else {
+      CK(cudaMemsetAsync(c->w.bar, 0, 64, c->stream));
+      CK(cudaMemsetAsync(c->w.abort_flag, 0, 128, c->stream));
+    }
+  }
   // an aborted launch can leave the early-reduction counters mid-sweep
   if (c->sp.layout == 1) CK(cudaMemsetAsync(c->w.ccnt, 0, early_bytes(c), c->stream));
   void* args[] = {&K};
