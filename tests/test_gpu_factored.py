@@ -325,3 +325,56 @@ def test_gradient_matches_scipy_order(small):
     At.sort_indices()
     t = At @ lam[arr.mq:]
     np.testing.assert_array_equal(gx, (acc + s) + t)
+
+
+def test_ragged_blocks_and_variable_rows_match_scipy():
+    """A factored instance that is not the generator's regular shape: blocks of
+    70 / 200 / 0 / 33 rows (no multiple of the 32-slot slice or the 128-row
+    chunk, one empty block), rows with 0..25 entries, empty columns, a linear
+    block with empty rows.  g and the gradient against scipy in the device's
+    order (gradient bitwise, g to rounding: the |W_i|^2 chunk sums differ)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(12)
+    n, rows = 257, [70, 200, 0, 33]
+    rblk = np.concatenate([[0], np.cumsum(rows)])
+    dens = rng.uniform(0.0, 0.1, size=rblk[-1])
+    mask = rng.uniform(size=(rblk[-1], n)) < dens[:, None]
+    mask[5] = False                                   # an empty row
+    mask[:, 100:110] = False                          # empty columns
+    Rm = sp.csr_matrix(np.where(mask, rng.normal(size=mask.shape), 0.0))
+    Am = sp.random(40, n, density=0.05, format="csr", random_state=3)
+    Am = sp.vstack([Am[:20], sp.csr_matrix((3, n)), Am[20:]], format="csr")   # empty rows inside
+    mq = len(rows) - 1
+    C = rng.normal(size=(mq + 1, n)) / np.sqrt(n)
+    d = np.concatenate([[0.0], -rng.uniform(1, 2, mq)])
+    b = rng.uniform(0.5, 1.5, Am.shape[0])
+    inst = FactoredInstance(n, mq, Rm, rblk, C, d, Am, b, np.full(n, -10.0), np.full(n, 10.0))
+    x = rng.uniform(-0.5, 0.5, n)
+    lam = np.abs(rng.normal(size=inst.m))
+    lam[1] = 0.0
+    W = Rm @ x
+    g_ref = np.array([0.5 * float(W[rblk[i]:rblk[i + 1]] @ W[rblk[i]:rblk[i + 1]]) + float(C[i] @ x) + d[i]
+                      for i in range(mq + 1)])
+    g = inst.g_value(x)
+    np.testing.assert_allclose(inst.f_value(x), g_ref[0], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(g[:mq], g_ref[1:], rtol=1e-13, atol=1e-13)
+    np.testing.assert_array_equal(g[mq:], Am @ x - b)
+    wq = np.concatenate([[1.0], lam[:mq]])
+    rmat = np.repeat(np.arange(mq + 1), rows)
+    Rt = Rm.T.tocsr()
+    Rt.sort_indices()
+    acc = np.zeros(n)
+    for i in range(mq + 1):
+        if wq[i] != 0.0:
+            acc = acc + wq[i] * C[i]
+    At = Am.T.tocsr()
+    At.sort_indices()
+    gx = np.asarray(R.grad_x_coupling(inst, R.Iterate(x, np.zeros(0), lam)))
+    np.testing.assert_array_equal(gx, (acc + Rt @ (wq[rmat] * W)) + At @ lam[mq:])
+    # and it runs: a few accepted iterations, deterministic
+    eng = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.initial_iterate(inst))
+    eng.run_block(15)
+    eng2 = R.ApdbEngine(inst, R.SolverConfig(mode="yx", nonmonotone=True), R.initial_iterate(inst))
+    eng2.run_block(15)
+    np.testing.assert_array_equal(trace_arr(eng.trace), trace_arr(eng2.trace))
+    np.testing.assert_array_equal(eng.last.x, eng2.last.x)
