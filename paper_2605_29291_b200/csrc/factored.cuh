@@ -52,7 +52,7 @@ constexpr int kCxCols = 1024;   // columns per c_i . x partial
 #ifndef RAPDB_GRADCTAS
 #define RAPDB_GRADCTAS 4
 #endif
-constexpr int kRowU = RAPDB_ROWU;       // gathers in flight per lane in the row pass (C3: 10 per row of R)
+constexpr int kRowU = RAPDB_ROWU;       // gathers in flight per lane in the row pass (C3: 10 entries per row of R)
 
 // One slice of a Sell operand against a gathered vector: lane l folds the
 // entries of slot 32 * slice + l in stored order without FMA -- the operation
@@ -166,15 +166,16 @@ __device__ __forceinline__ void fac_wl(const DevProblem& P, const Work& w, const
 //        (one thread per column: a plain HBM stream over C), in phase p the
 //        blocks [fnb p / nph, fnb (p + 1) / nph) continuing the chain;
 //   s    the R^T gather sum_r v (w_blk(r) W[r]), the column's entries folded
-//        one by one in row order across the row phases (sell_dot_tagged);
-//   t    A^T mu the same way (sell_dot).
+//        one by one in row order across the row phases (sell_dot<., true>);
+//   t    A^T mu the same way (sell_dot<., false>).
 // The gather of phase p reads only rows [rt_b[p], rt_b[p+1]) of the W-cache:
 // phases run one after the other over the whole grid (separate launches), so
 // the gathered slice stays L2-resident.
 constexpr int kGxU = RAPDB_GXU;       // gathers in flight per lane in the transposed passes
-// resident CTAs per SM of the standalone kernels: the gather rate needs only a
-// few dozen warp-gathers in flight per SM (one costs 32 L1 wavefronts), so
-// registers for the unrolled loads matter more than occupancy
+// resident CTAs per SM of the standalone kernels: the latency chain of a slice
+// (offsets -> (idx, val) -> gathers) is hidden by warps, not by unrolling --
+// 4 CTAs (32 warps, 64 registers) beat both 2-3 CTAs with U = 8..10 and 6-8
+// CTAs whose 32-40 registers spill (profiles/r02j_c3_variant_sweep.log)
 constexpr int kRowCtas = RAPDB_ROWCTAS, kGradCtas = RAPDB_GRADCTAS;
 
 __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, int i0, int i1,
