@@ -59,17 +59,19 @@ constexpr int kRowU = RAPDB_ROWU;       // gathers in flight per lane in the row
 // order of scipy's csr_matvec, so W = R x and the R^T / A^T column sums match
 // the factored restatement bit for bit -- starting from s.  The t-th loads of
 // val / idx are one coalesced access per warp (no shared-memory staging), U
-// entries per lane at a time.  The passes are bound by what the gathers pull
-// out of L2: every 8-byte gather moves a 32-byte sector to the SM, 65 M per
-// pass at C3 (tools/gather_probe.cu: at most ~250-270 G gathers/s on a B200,
-// i.e. ~9-10 TB/s of L2 -> SM sectors with the index stream), and the R / C / x
-// streams share that path: ~4 GB per row pass, ~3.6 GB per gradient.  Measured
-// at C3 (profiles/r02j_c3*): row pass 358 us, gradient 2 x 205 us -- 11 / 9 TB/s
-// of sectors; every variant tried lands there or worse (U = 2..10 at 2..8 CTAs
-// per SM, double-buffered loads with TMA L2 prefetch, TMA-fed shared-memory
-// rings with 7 / 14 gather warps, x staged in shared memory for c_i . x:
-// profiles/r02j_c3_variant_sweep.log), so the plain form stays: U = 4..5,
-// 4 CTAs per SM, a contiguous run of slices per warp.
+// entries per lane at a time.  The passes are bound by their gathers: every
+// 8-byte gather is one L1 wavefront (a 128-byte line lookup per lane) and
+// moves a 32-byte sector from L2 to the SM; tools/gather_probe.cu puts the
+// ceiling at ~250-270 G gathers/s on a B200 (~1 wavefront per cycle and SM,
+// ~9-10 TB/s of sectors with the index stream), whatever the width,
+// instruction or occupancy.  At C3 the row pass issues ~83 M wavefronts, 67.5 M
+// of them gathers (the rest: the R, C and x streams), in 355-360 us: 0.92 per
+// cycle and SM, 3.65 GB of sectors at 10.3 TB/s; the gradient 2 x 205 us.  Every
+// variant tried lands there or worse (U = 2..10 at 2..8 CTAs per SM, double-
+// buffered loads with TMA L2 prefetch, TMA-fed shared-memory rings with 7 / 14
+// gather warps, dedicated c_i . x CTAs: profiles/r02j_c3_variant_sweep.log),
+// so the plain form stays: U = 4..5, 4 CTAs per SM, a contiguous run of slices
+// per warp.
 constexpr int kRtTagShift = 23;
 constexpr int kRtRowMask = (1 << kRtTagShift) - 1;
 
@@ -125,11 +127,13 @@ __device__ __forceinline__ void wchunk_rows(const DevProblem& P, long long c, lo
 }
 
 // c_i . x over columns [ch*1024, +1024): lane-strided fma chain, butterfly
-// (the partial of item it = i * nchx + ch)
-__device__ __forceinline__ double cx_item(const DevProblem& P, const double* x, long long it) {
+// (the partial pcx[i * nchx + ch]).  x is read through L1 (ld.global.ca): a
+// warp walks the blocks i of ONE column chunk back to back (fac_row_kernel), so
+// the 8 KB chunk of x is fetched from L2 once instead of once per block --
+// 520 MB of L2 -> SM sectors per pass at C3, on the path the gathers saturate.
+__device__ __forceinline__ double cx_item(const DevProblem& P, const double* x, long long i, long long ch) {
   const int lane = threadIdx.x & 31;
   const long long n = P.n;
-  const long long i = it / P.nchx, ch = it - i * P.nchx;
   const long long j0 = ch * kCxCols, j1 = min(j0 + kCxCols, n);
   const double* ci = P.q + i * n;
   double s = 0.0;
@@ -137,11 +141,11 @@ __device__ __forceinline__ double cx_item(const DevProblem& P, const double* x, 
   for (; j + 7 * 32 < j1; j += 8 * 32) {   // 16 loads in flight, the same fma chain
     double c[8], xv[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { c[k] = __ldg(ci + j + 32 * k); xv[k] = ldcg(x + j + 32 * k); }
+    for (int k = 0; k < 8; ++k) { c[k] = __ldcs(ci + j + 32 * k); xv[k] = __ldca(x + j + 32 * k); }
 #pragma unroll
     for (int k = 0; k < 8; ++k) s = fma(c[k], xv[k], s);
   }
-  for (; j < j1; j += 32) s = fma(__ldg(ci + j), ldcg(x + j), s);
+  for (; j < j1; j += 32) s = fma(__ldcs(ci + j), __ldca(x + j), s);
   return warp_sum(s);
 }
 
@@ -304,10 +308,15 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) fac_row_kernel(DevProblem 
   const int lane = threadIdx.x & 31;
   const long long gw = gwarp(), nw = nwarps();
   if ((gw & 3) == 3) {                       // c_i . x role
+    // items in chunk-major order (ch, i), a contiguous run per warp: the
+    // blocks of one column chunk back to back, its x chunk L1-resident
     const long long items = (long long)P.fnb * P.nchx;
-    for (long long it = gw >> 2; it < items; it += nw >> 2) {
-      const double s = cx_item(P, x, it);
-      if (lane == 0) w.pcx[it] = s;
+    long long lo, hi;
+    my_range(items, gw >> 2, nw >> 2, lo, hi);
+    for (long long it = lo; it < hi; ++it) {
+      const long long ch = it / P.fnb, i = it - ch * P.fnb;
+      const double s = cx_item(P, x, i, ch);
+      if (lane == 0) w.pcx[i * P.nchx + ch] = s;
     }
     return;
   }

@@ -328,12 +328,12 @@ __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 // once-per-pass streams must not push small gathered vectors out of L2)
 __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
   int v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
