@@ -55,14 +55,17 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_spectral_norm", "rapdb_kkt_at", "rapdb_eq_residual",
            "rapdb_check_guards"]
 
-STEP_NAMES = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
-              "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
-              "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
-              "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
-              "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN", "P_KKT",
-              "E_INIT", "E_GX", "E_HALF", "E_HSWEEP", "E_HGLOC", "E_GXH", "E_PLUS", "E_PSWEEP", "E_PGLOC",
-              "E_POST", "DONE"] + [""] * 14 + ["sweep:stage_x", "sweep:stream", "sweep:reduce"]
-assert len(STEP_NAMES) == 64 and STEP_NAMES[61] == "sweep:stage_x"   # SolverState::step_ns (rapdb_dev.cuh)
+_STEPS = ["T_BEGIN", "TY_DUAL", "TY_GXPART", "TY_PRIMAL", "TY_SWEEP", "TY_GLOCAL", "TY_GY", "TY_DECIDE",
+          "TX_PRIMAL", "TX_SWEEP", "TX_GLOCAL", "TX_DUAL", "TX_GXPART", "TX_NORMS", "TX_DECIDE",
+          "A_POST", "K_GXPART", "K_FINISH", "A_RESTART", "A_END",
+          "R_POINT", "R_SWEEP", "R_GLOCAL", "R_CACHE", "R_GXPART", "R_GXCACHE", "R_FINISH",
+          "G_CAND", "G_GLOCAL", "G_HPART", "G_SOLVE", "P_SWEEP", "P_OUT", "P_GRAD", "P_GFIN", "P_KKT",
+          "E_INIT", "E_GX", "E_HALF", "E_HSWEEP", "E_HGLOC", "E_GXH", "E_PLUS", "E_PSWEEP", "E_PGLOC",
+          "E_POST", "DONE"]            # enum Step (csrc/rapdb_dev.cuh), in order
+# SolverState::step_ns has 64 slots: the steps, then the packed sweep's
+# sub-phases at 60, 61, 62 (sub_time in csrc/solver_kernel.cuh)
+STEP_NAMES = _STEPS + [""] * (60 - len(_STEPS)) + ["sweep:stage_x", "sweep:stream", "sweep:reduce", ""]
+assert len(STEP_NAMES) == 64 and STEP_NAMES[60] == "sweep:stage_x"
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 X_GX, X_G, X_GX2, X_H = 1, 2, 3, 4
