@@ -99,3 +99,47 @@ def test_phased_transpose_walks_columns_in_row_order(nph, tag):
     Rt = R.T.tocsr()
     Rt.sort_indices()
     np.testing.assert_array_equal(out, Rt @ (wq[rmat] * w))
+
+
+# ---- property tests (hypothesis): any CSR, any block partition, any phase count
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@st.composite
+def csr_cases(draw):
+    rows = draw(st.integers(0, 70))
+    cols = draw(st.integers(1, 50))
+    seed = draw(st.integers(0, 2 ** 16))
+    density = draw(st.sampled_from([0.0, 0.02, 0.1, 0.4, 1.0]))
+    rng = np.random.default_rng(seed)
+    dense = np.where(rng.uniform(size=(rows, cols)) < density, rng.normal(size=(rows, cols)), 0.0)
+    M = sp.csr_matrix(dense)
+    cuts = sorted(draw(st.lists(st.integers(0, rows), max_size=4)))
+    rblk = np.array([0] + cuts + [rows], dtype=np.int64)
+    return M, rblk, rng.normal(size=cols), rng.normal(size=rows), draw(st.integers(1, 5))
+
+
+@settings(max_examples=60, deadline=None)
+@given(csr_cases())
+def test_sell_forms_agree_with_scipy(case):
+    M, rblk, x, w, nph = case
+    rows, cols = M.shape
+    ref = M @ x
+    for S in (SellMatrix.by_row(M), SellMatrix.by_sorted_length(M)):
+        got, _ = walk(S, lambda c: x[c], rows)
+        np.testing.assert_array_equal(got, ref)
+        assert S.entries == int(S.sp[-1]) and np.all(np.diff(S.sp) % 32 == 0)
+    S = SellMatrix.by_block_chunks(M, rblk)
+    assert S.nslots == 128 * sum(-(-(int(rblk[i + 1]) - int(rblk[i])) // 128) for i in range(len(rblk) - 1))
+    # the transposed gather in row phases, weights per block
+    nb = len(rblk) - 1
+    rmat = np.repeat(np.arange(nb, dtype=np.int32), np.diff(rblk))
+    wq = np.linspace(0.0, 1.5, nb) if nb else np.zeros(0)
+    _, mats = phased_transpose(M, rmat, nph, True)
+    out = np.zeros(cols)
+    for T in mats:
+        out, seen = walk(T, lambda idx: wq[idx >> RT_TAG_SHIFT] * w[idx & ((1 << RT_TAG_SHIFT) - 1)], cols, s0=out)
+        assert np.all(seen == 1)
+    Mt = M.T.tocsr()
+    Mt.sort_indices()
+    np.testing.assert_array_equal(out, Mt @ (wq[rmat] * w) if rows else np.zeros(cols))
