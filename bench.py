@@ -562,13 +562,27 @@ def main():
     if not device_generated:
         inst.drop_device_data()
 
+    # the side blocks must not take the headline line down with them (single
+    # rank only: in a sharded job a rank that skipped a block would leave the
+    # others waiting in its collectives, so there a failure stays fatal)
+    def guarded(fn):
+        if ws > 1:
+            return fn(R, args, dev, shard_fn, ranks, ws, peak)
+        try:
+            return fn(R, args, dev, shard_fn, ranks, ws, peak)
+        except Exception as exc:   # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            torch.cuda.empty_cache()
+            return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     c2 = None
     if args.c2_steps > 0 and not device_generated:
-        c2 = c2_block(R, args, dev, shard_fn, ranks, ws, peak)
+        c2 = guarded(c2_block)
 
     c3f = None
     if args.c3_steps > 0 and not device_generated:
-        c3f = c3f_block(R, args, dev, shard_fn, ranks, ws, peak)
+        c3f = guarded(c3f_block)
 
     if rank == 0:
         cpu = None
