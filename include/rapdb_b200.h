@@ -267,6 +267,16 @@ int rapdb_bind_factored_range(rapdb_ctx* ctx, int n, int mq, int L, int fb0, int
 int rapdb_set_factored_transpose(rapdb_ctx* ctx, int nph, const long long* ph_bounds, const rapdb_sell* RT,
                                  const rapdb_sell* AT, int tagged);
 
+/* Sparse symmetric Q stack (the reference keeps a Q_i below 25 % density as
+ * CSR, _as_operator problem.py:31-40): bind the stacked Q_0..Q_m through
+ * rapdb_bind_factored as the "R" operand with n rows per block (mq = m,
+ * C = q, d = r), pass empty transposes, and set this flag.  The blocks are
+ * then applied as Q_i themselves: the W-cache holds u_i = Q_i x (each row
+ * summed in CSR order: the bits of scipy's csr_matvec the reference calls),
+ * g_i = 1/2 x . u_i + q_i . x + r_i, and grad_x Phi = sum_i w_i (u_i + q_i)
+ * + A^T mu in the reference's operation order (problem.py:205-214).        */
+int rapdb_set_factored_symmetric(rapdb_ctx* ctx, int symmetric);
+
 /* SolverConfig.resolved() (engine.py:33-63); mode 0 = yx, 1 = xy;
  * ball_kind 0/1/2 = Unbounded / JointBall(r1) / SplitBall(r1=v, r2=lam)       */
 int rapdb_set_params(rapdb_ctx* ctx, int mode, double c_alpha, double c_beta, double delta,

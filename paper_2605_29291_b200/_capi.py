@@ -51,7 +51,7 @@ EXPORTS = ["rapdb_abi_version", "rapdb_create", "rapdb_destroy", "rapdb_last_err
            "rapdb_bind_factored_range", "rapdb_egm", "rapdb_peer_region_bytes", "rapdb_ipc_handle",
            "rapdb_ipc_open", "rapdb_ipc_close", "rapdb_set_peer_exchange", "rapdb_region_alloc",
            "rapdb_region_free", "rapdb_comm_unique_id", "rapdb_comm_create", "rapdb_comm_destroy",
-           "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange", "rapdb_set_factored_transpose",
+           "rapdb_comm_allreduce_ordered", "rapdb_set_comm_exchange", "rapdb_set_factored_transpose", "rapdb_set_factored_symmetric",
            "rapdb_spectral_norm", "rapdb_kkt_at", "rapdb_eq_residual",
            "rapdb_check_guards"]
 
@@ -239,6 +239,7 @@ def load(path: str = LIB_PATH):
     lib.rapdb_comm_allreduce_ordered.argtypes = [P, P, LL, P]
     lib.rapdb_set_comm_exchange.argtypes = [P, P, I]
     lib.rapdb_set_factored_transpose.argtypes = [P, I, P, P, P, I]
+    lib.rapdb_set_factored_symmetric.argtypes = [P, I]
     lib.rapdb_spectral_norm.argtypes = [P, LL, LL, LL, I, D, P, C.POINTER(D)]
     lib.rapdb_kkt_at.argtypes = [P, P, P, P, I, D, C.POINTER(D)]
     lib.rapdb_eq_residual.argtypes = [P, P, P]
@@ -374,6 +375,8 @@ class Context:
             self._check(self.lib.rapdb_set_factored_transpose(
                 self.h, int(data.rt_nph), bounds.ctypes.data_as(C.c_void_p), rt,
                 C.byref(data.sell_AT.descriptor()), int(data.rt_tag)))
+            if getattr(data, "sym", False):
+                self._check(self.lib.rapdb_set_factored_symmetric(self.h, 1))
         else:
             k1 = data.m + 1 if k1 is None else k1
             zero = np.ascontiguousarray(data.zero_flags, dtype=np.uint8)

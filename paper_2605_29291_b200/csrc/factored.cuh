@@ -116,13 +116,15 @@ __device__ __forceinline__ void my_range(long long items, long long me, long lon
 }
 
 // rows [r0, r1) of W chunk c (wch[i] = first chunk of local block i)
-__device__ __forceinline__ void wchunk_rows(const DevProblem& P, long long c, long long& r0, long long& r1) {
+__device__ __forceinline__ void wchunk_rows(const DevProblem& P, long long c, long long& r0, long long& r1,
+                                            long long& rb) {
   int lo = 0, hi = P.fnb;                 // local block of chunk c: wch[lo] <= c < wch[lo+1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (__ldg(P.wch + mid) <= c) lo = mid; else hi = mid;
   }
-  r0 = __ldg(P.rblk + lo) + (c - __ldg(P.wch + lo)) * kWChunk;
+  rb = __ldg(P.rblk + lo);                // first row of the block
+  r0 = rb + (c - __ldg(P.wch + lo)) * kWChunk;
   r1 = min(r0 + kWChunk, __ldg(P.rblk + lo + 1));
 }
 
@@ -182,14 +184,21 @@ constexpr int kGxU = RAPDB_GXU;       // gathers in flight per lane in the trans
 // CTAs whose 32-40 registers spill (profiles/r02j_c3_variant_sweep.log)
 constexpr int kRowCtas = RAPDB_ROWCTAS, kGradCtas = RAPDB_GRADCTAS;
 
-__device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, long long j, int i0, int i1,
-                                            double acc, uint64_t ef) {
+// U (symmetric stacks only, else null): the W-cache, whose block i is u_i =
+// Q_i x -- the term becomes w_i (u_ij + c_ij), the reference's own grouping
+// (problem.py:205-214: out + lam_i * (Q_i x + q_i)).
+__device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* wq, const double* U, long long j,
+                                            int i0, int i1, double acc, uint64_t ef) {
   const long long n = P.n;
   int i = i0;
-  for (; i + 8 <= i1; i += 8) {           // 8 independent loads in flight
+  for (; i + 8 <= i1; i += 8) {           // 8 (16) independent loads in flight
     double c[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) c[k] = ld_stream(P.q + (long long)(i + k) * n + j, ef);
+    if (U) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = ldcg(U + (long long)(i + k) * n + j) + c[k];
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const double l = wq[i + k];
@@ -198,7 +207,8 @@ __device__ __forceinline__ double fac_c_acc(const DevProblem& P, const double* w
   }
   for (; i < i1; ++i) {
     const double l = wq[i];
-    const double c = ld_stream(P.q + (long long)i * n + j, ef);
+    double c = ld_stream(P.q + (long long)i * n + j, ef);
+    if (U) c = ldcg(U + (long long)i * n + j) + c;
     acc = (l != 0.0) ? acc + l * c : acc;
   }
   return acc;
@@ -228,12 +238,13 @@ __device__ __forceinline__ void fac_gather_item(const DevProblem& P, const Work&
 }
 // ---------------------------------------------------------------- row pass
 // |W_i|^2 over chunk c: lane r0 + lane, + 32, ... with fma, then the butterfly
-// (formed on the fly by the row pass: 4 slices of 32 rows per chunk)
+// (formed on the fly by the row pass: 4 slices of 32 rows per chunk); for a
+// symmetric stack (P.sym: the blocks are the Q_i) the chunk's part of x . Q_i x
 __device__ __forceinline__ void fac_chunk(const DevProblem& P, const Work& w, const double* x, double* W,
                                           long long c, uint64_t ef, uint64_t el) {
   const int lane = threadIdx.x & 31;
-  long long r0, r1;
-  wchunk_rows(P, c, r0, r1);
+  long long r0, r1, rb;
+  wchunk_rows(P, c, r0, r1, rb);
   double s2 = 0.0;
   for (int g = 0; g < kWChunk / 32; ++g) {
     const long long row = r0 + 32 * g + lane;
@@ -241,7 +252,7 @@ __device__ __forceinline__ void fac_chunk(const DevProblem& P, const Work& w, co
     const double v = sell_dot<kRowU, false>(P.sell[kSellR], c * (kWChunk / 32) + g, x, nullptr, 0.0, ef);
     if (row < r1) {
       st_keep(W + row, v, el);
-      s2 = fma(v, v, s2);
+      s2 = P.sym ? fma(ldcg(x + (row - rb)), v, s2) : fma(v, v, s2);   // x . (Q_i x), or |R_i x|^2
     }
   }
   s2 = warp_sum(s2);
@@ -350,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, kGradCtas) fac_grad_kernel(DevProble
   if ((gw & 3) == 3) {
     const int i0 = (int)((long long)P.fnb * ph / P.rt_nph), i1 = (int)((long long)P.fnb * (ph + 1) / P.rt_nph);
     for (long long j = (gw >> 2) * 32 + lane; j < n; j += (nw >> 2) * 32)
-      w.aux[j] = fac_c_acc(P, wq, j, i0, i1, ph > 0 ? ldcg(w.aux + j) : 0.0, ef);
+      w.aux[j] = fac_c_acc(P, wq, P.sym ? Wsrc : nullptr, j, i0, i1, ph > 0 ? ldcg(w.aux + j) : 0.0, ef);
     return;
   }
   const long long me = (gw >> 2) * 3 + (gw & 3), nrole = (nw >> 2) * 3;

@@ -141,6 +141,8 @@ struct DevProblem {
   // (a device table, so a phase can be indexed at run time without a local copy)
   const Sell* sell;      // [kSellRt + rt_nph]: R, A, A^T, then the phases of R^T
   int rt_nph, rt_tag;
+  int sym;               // the blocks are the symmetric Q_i themselves (n rows each), not factors R_i:
+                         // W = Q x is the U-cache, g_i = 1/2 x . W_i + ..., grad = sum w_i (W_i + c_i), no R^T
   const int* rmat;                                                  // [nr] block of each R row
   const long long* rblk;                                            // [mq+2] first row of block i
   const long long* wch;  // [fnb+1] prefix count of 1024-row chunks of W per local block

@@ -626,7 +626,7 @@ int fac_gradient(rapdb_ctx* c, const Work& w, const double* Wpar, const double* 
   const DevProblem& P = c->P;
   const size_t wq = (size_t)std::max(P.fnb, 1) * 8;
   const double* Wsrc = Wpar;
-  if (!P.rt_tag) {   // block-weighted W-cache first
+  if (!P.rt_tag && !P.sym) {   // block-weighted W-cache first (a symmetric stack has no R^T to gather for)
     fac_wl_kernel<<<c->nsm * 8, kThreads, wq, c->stream>>>(P, w, Wpar, lam);
     Wsrc = w.wl;
     ++g_launches;
@@ -1382,6 +1382,7 @@ int rapdb_bind_factored_range(rapdb_ctx* c, int n, int mq, int L, int fb0, int f
   CK(cudaMemcpyAsync(c->d_sell, c->h_sell, sizeof c->h_sell, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   P.sell = c->d_sell;
+  P.sym = 0;
   P.rt_nph = 0; P.rt_tag = 0;
   P.rmat = rmat; P.rblk = c->d_ll; P.wch = c->d_ll + (fnb + 1);
   c->P = P;
@@ -1470,6 +1471,15 @@ int rapdb_set_factored_transpose(rapdb_ctx* c, int nph, const long long* ph_boun
   CK(cudaMemcpyAsync(c->d_sell, c->h_sell, sizeof c->h_sell, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   P.rt_nph = nph; P.rt_tag = tagged ? 1 : 0;
+  return RAPDB_OK;
+}
+
+int rapdb_set_factored_symmetric(rapdb_ctx* c, int symmetric) {
+  if (!c) return RAPDB_EINPUT;
+  if (!c->bound || c->P.kind != 1) return fail(c, RAPDB_ECONFIG, "bind a factored instance first");
+  if (symmetric && c->P.nr != (long long)c->P.fnb * c->P.n)
+    return fail(c, RAPDB_EINPUT, "a symmetric stack needs n rows per block");
+  c->P.sym = symmetric ? 1 : 0;
   return RAPDB_OK;
 }
 

@@ -276,6 +276,64 @@ class FactoredInstance:
         return np.maximum(np.asarray(lam, dtype=float), 0.0)
 
 
+class SparseQInstance(FactoredInstance):
+    """A QCQP whose quadratic forms are sparse symmetric matrices, kept sparse.
+
+    The reference stores a ``Q_i`` with fewer than 25 % nonzeros as CSR
+    (``_as_operator`` problem.py:31-40) and applies it with scipy's
+    ``csr_matvec``; ``problem.ProblemInstance`` here densifies every ``Q_i``
+    for the packed dense sweep, which a large sparse stack does not survive.
+    This instance keeps the stack sparse on the device: the stacked
+    ``Q_0..Q_m`` ride the factored path's row pass as one Sell operand with n
+    rows per block (``rapdb_set_factored_symmetric``) -- ``u_i = Q_i x`` summed
+    in CSR order (the bits of the reference's products), ``g_i = 1/2 x.u_i +
+    q_i.x + r_i``, ``grad_x Phi = sum_i w_i (u_i + q_i) + A^T mu`` in the
+    reference's operation order (problem.py:205-214), no transposed gather.
+    Constraints: ``m`` quadratic rows plus optional sparse linear rows
+    ``A x <= b`` (orthant cone), box primal set, no equality block, no
+    adaptive restart (as for every factored instance)."""
+
+    sym = True
+
+    def __init__(self, n, m, Q, q, r, lower, upper, A=None, b=None, mu=0.0, name="", symmetry_tol=1e-12):
+        import scipy.sparse as sp
+        n, m = int(n), int(m)
+        if len(Q) != m + 1:
+            raise InputError("need m+1 quadratic forms (objective plus m constraints)")
+        mats = []
+        for i, M in enumerate(Q):
+            M = sp.csr_matrix(M)
+            if M.shape != (n, n):
+                raise InputError(f"quadratic form {i} has wrong dimensions")
+            d = abs(M - M.T)
+            if d.nnz and d.max() > symmetry_tol * max(1.0, abs(M).max()):
+                raise InputError(f"quadratic form {i} is not symmetric")
+            mats.append(M)
+        R = sp.vstack(mats, format="csr") if mats else sp.csr_matrix((0, n))
+        rblk = np.arange(m + 2, dtype=np.int64) * n
+        q = np.asarray(q, dtype=np.float64).reshape(m + 1, n)
+        L = 0 if A is None else sp.csr_matrix(A).shape[0]
+        super().__init__(n, m, R, rblk, q, np.asarray(r, dtype=np.float64), A,
+                         np.zeros(0) if b is None else b, lower, upper, mu=mu, name=name)
+        assert self.L == L
+
+    @classmethod
+    def from_problem(cls, inst, density_limit: float = 0.25):
+        """From a ``problem.ProblemInstance`` (box primal set, orthant cone, p = 0)
+        whose forms are all below the reference's CSR density limit."""
+        import scipy.sparse as sp
+        if inst.p != 0:
+            raise ConfigurationError("a sparse-Q instance has no equality block")
+        if not isinstance(inst.primal_set, Box) or not isinstance(inst.cone, NonnegOrthant):
+            raise ConfigurationError("a sparse-Q instance needs a box primal set and the orthant cone")
+        Q = [sp.csr_matrix(inst.Q[i]) for i in range(inst.m + 1)]
+        for i, M in enumerate(Q):
+            if M.nnz > density_limit * inst.n * inst.n:
+                raise ConfigurationError(f"quadratic form {i} is not sparse (the reference would keep it dense)")
+        return cls(inst.n, inst.m, Q, inst.q, inst.r, inst.primal_set.lower, inst.primal_set.upper,
+                   mu=inst.mu, name=getattr(inst, "name", ""))
+
+
 class FactoredDeviceData:
     """A FactoredInstance resident in HBM (see module docstring)."""
 
@@ -307,9 +365,16 @@ class FactoredDeviceData:
         At.sort_indices()              # a column's entries in row order
         nr = R.shape[0]
         rmat = np.repeat(np.arange(k1 - k0, dtype=np.int32), np.diff(rblk))
-        nph = min(RT_MAX_PHASES, max(1, -(-nr // rt_phase_rows())))
-        tag = nr <= (1 << RT_TAG_SHIFT) and (k1 - k0) <= 256
-        rt_bounds, rt_mats = phased_transpose(R, rmat, nph, tag)
+        sym = bool(getattr(inst, "sym", False))
+        if sym:     # the blocks are the Q_i themselves: nothing to gather through R^T
+            import scipy.sparse as sp
+            nph, tag = 1, False
+            rt_bounds = np.array([0, nr], dtype=np.int64)
+            rt_mats = [SellMatrix.by_sorted_length(sp.csr_matrix((inst.n, nr)))]
+        else:
+            nph = min(RT_MAX_PHASES, max(1, -(-nr // rt_phase_rows())))
+            tag = nr <= (1 << RT_TAG_SHIFT) and (k1 - k0) <= 256
+            rt_bounds, rt_mats = phased_transpose(R, rmat, nph, tag)
         sell_R = SellMatrix.by_block_chunks(R, rblk)
         sell_A = SellMatrix.by_row(A)
         sell_AT = SellMatrix.by_sorted_length(At)
@@ -321,4 +386,4 @@ class FactoredDeviceData:
                    rmat=one(i32(rmat)), C=one(f64(inst.C[k0:k1])), d=one(f64(inst.d[k0:k1])),
                    b=one(f64(inst.b[l0:l1])), lower=f64(inst.primal_set.lower),
                    upper=f64(inst.primal_set.upper), mu=inst.mu, device=device,
-                   nnz_r=int(R.nnz), nnz_a=int(A.nnz), rt_nph=nph, rt_bounds=rt_bounds, rt_tag=int(tag))
+                   nnz_r=int(R.nnz), nnz_a=int(A.nnz), rt_nph=nph, rt_bounds=rt_bounds, rt_tag=int(tag), sym=sym)

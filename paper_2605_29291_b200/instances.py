@@ -269,6 +269,28 @@ def factored_qcqp(n: int = 1_000_000, mq: int = 64, rows: int = 100_000, nnz_row
                                 "lin_nnz": lin_nnz})
 
 
+def sparse_qcqp(n: int = 400, m: int = 6, rows: int = 60, nnz_row: int = 4, seed: int = 0, box: float = 10.0):
+    """A QCQP with SPARSE quadratic forms (below the reference's 25 % CSR
+    limit, problem.py:31-40): Q_i = B_i^T B_i + 0.1 I with B_i [rows x n],
+    nnz_row entries per row (the streams of factored_qcqp), q_i ~ N(0,1)/sqrt(n),
+    r_i = -U(1,2) (r_0 = 0), box [-box, box].  Returns (Q list of CSR with
+    sorted indices, q [(m+1) x n], r [m+1], lower, upper)."""
+    import scipy.sparse as sp
+    Q, q, r = [], np.empty((m + 1, n)), np.zeros(m + 1)
+    for i in range(m + 1):
+        B = _csr_uniform(CounterRng(seed, 4 * i), CounterRng(seed, 4 * i + 1), rows, n, nnz_row,
+                         1.0 / np.sqrt(nnz_row))
+        M = (B.T @ B + 0.1 * sp.identity(n, format="csr")).tocsr()
+        M = ((M + M.T) * 0.5).tocsr()
+        M.sum_duplicates()
+        M.sort_indices()
+        Q.append(M)
+        q[i] = CounterRng(seed, 4 * i + 2).normal(n) / np.sqrt(n)
+        if i > 0:
+            r[i] = -float(CounterRng(seed, 4 * i + 3).uniform(1, 1.0, 2.0)[0])
+    return Q, q, r, np.full(n, -box), np.full(n, box)
+
+
 # BASELINE.json configs[0..2], [4]; config 3 (factored sparse) is factored_qcqp()
 CONFIGS = {
     "C0": dict(n=200, m=10, rank=20),
