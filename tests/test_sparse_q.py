@@ -147,3 +147,29 @@ def test_sharded_sparse_stack(case):
         np.testing.assert_array_equal(trace_arr(res.trace)[:, TAU], trace_arr(fused.trace)[:, TAU])
         assert rel(res.solution.x, fused.solution.x) <= 1e-12
     np.testing.assert_array_equal(emu[0].solution.x, emu[1].solution.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,nm,ball", [("xy", False, None), ("xy", True, None), ("yx", True, ("joint", 0.6)),
+                                          ("xy", False, ("split", 1.0, 0.5))])
+def test_modes_and_dual_balls_vs_oracle(case, mode, nm, ball):
+    """APDB-xy and the dual balls (geometry.py:263-311) on the sparse stack,
+    against the oracle run on the same CSR forms: step sizes and evaluation
+    counts identical, iterates within 1e-9."""
+    from paper_2605_29291_b200.geometry import JointBall, SplitBall
+    Q, q, r, lo, hi, g = case
+    n, m = SPARSE_SMALL["n"], SPARSE_SMALL["m"]
+    inst = SparseQInstance(n, m, Q, q, r, lo, hi)
+    dev_ball = None if ball is None else (JointBall(ball[1]) if ball[0] == "joint" else SplitBall(ball[1], ball[2]))
+    ob = O.Ball() if ball is None else (O.Ball(1, ball[1]) if ball[0] == "joint" else O.Ball(2, ball[1], ball[2]))
+    kw = {} if dev_ball is None else {"dual_ball": dev_ball}
+    cfg = R.SolverConfig(mode=mode, nonmonotone=nm, **kw)
+    res = R.run_restarted(inst, cfg, R.FixedRestart(50), budget=120)
+    P = O.Problem(Q, [q[i] for i in range(m + 1)], r, np.zeros((0, n)), np.zeros(0), lo, hi, 0.0)
+    ref = O.run_restarted(P, O.Options(mode=mode, nonmonotone=nm, ball=ob), O.Policy("fixed", period=50), budget=120)
+    tr = np.array([[t.iter, t.tau_start, t.tau, t.sigma, t.gamma, t.evals_iter, t.evals_total] for t in ref.trace])
+    np.testing.assert_array_equal(trace_arr(res.trace)[:, TAU], tr[:, TAU])
+    assert rel(res.solution.x, ref.x) <= 1e-9
+    assert rel(res.solution.lam, ref.lam) <= 1e-9
+    if ball is not None:                                   # the ball binds somewhere along the run
+        assert np.linalg.norm(res.solution.lam) <= (ball[1] if ball[0] == "joint" else ball[2]) * (1 + 1e-12)
